@@ -1,0 +1,208 @@
+/*
+ * sutradhara_b200.h — C-ABI of the B200-native engine-side hot path of
+ * Sutradhara (arXiv 2601.12967): paged-KV block pool + block table, prefix
+ * block hashing and prefix match, hint-aware (tiered) eviction scoring, and
+ * the continuation-prefill attention over the paged KV pool.
+ *
+ * Plain C types only (no torch types).  Device pointers are raw CUDA device
+ * addresses; `stream` is a cudaStream_t passed as void* (0 = legacy stream).
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to the reference tree proj/).  Status codes mirror the
+ * reference's exception hierarchy (include/agentsim/common.hpp:72-115) so a
+ * binding can re-raise the same exception type.
+ */
+#ifndef SUTRADHARA_B200_H_
+#define SUTRADHARA_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mirror common.hpp exception classes) ---------------- */
+enum {
+  SB_OK = 0,
+  SB_ERR_CACHE_FULL = 1,       /* CacheFull        common.hpp:77  */
+  SB_ERR_UNKNOWN_BLOCK = 2,    /* UnknownBlock     common.hpp:82  */
+  SB_ERR_ZERO_REF_RELEASE = 3, /* ZeroRefRelease   common.hpp:87  */
+  SB_ERR_CACHE = 4,            /* CacheError       common.hpp:72  */
+  SB_ERR_CONFIG = 5,           /* ConfigError      common.hpp:25  */
+  SB_ERR_CUDA = 6,             /* CUDA runtime / launch failure   */
+  SB_ERR_INVALID = 7,          /* bad argument to this C-ABI      */
+  SB_ERR_UNSUPPORTED = 8       /* shape/config outside the kernels' range */
+};
+
+/* ---- semantic tags (order == agentsim::KvTag, kv_cache.hpp:220-227) ---- */
+enum {
+  SB_TAG_RESPONSE = 0,
+  SB_TAG_TOOL_OUTPUT = 1,
+  SB_TAG_USER_QUERY = 2,
+  SB_TAG_SYSTEM_PROMPT = 3,
+  SB_TAG_PARTIAL_PREFILL = 4,
+  SB_TAG_HISTORY = 5
+};
+
+/* ---- eviction policy (agentsim::EvictionPolicy, kv_cache.hpp:235) ------ */
+enum { SB_POLICY_LRU = 0, SB_POLICY_TIERED = 1 };
+
+/* Half-open token range with a tag (agentsim::TagRange, kv_cache.hpp:244). */
+typedef struct sb_tag_range {
+  int64_t begin;
+  int64_t end;
+  int32_t tag;
+  int32_t _pad;
+} sb_tag_range;
+
+/* Read-back of one block's metadata (agentsim::KvBlock, kv_cache.hpp:250). */
+typedef struct sb_block_info {
+  int32_t block_id;
+  int32_t tag;
+  int32_t tier;
+  int32_t ref_count;
+  int64_t last_used;
+  uint64_t chain_hash;
+  uint64_t parent_hash;
+  int32_t pinned;
+  int32_t n_tokens;
+} sb_block_info;
+
+typedef struct sb_kv_cache sb_kv_cache; /* opaque, device-resident pool */
+
+/* Last error message of the calling thread (never NULL). */
+const char* sb_last_error(void);
+/* Library version string. */
+const char* sb_version(void);
+
+/* ---- hashing (common.hpp:136-145, kv_cache.cpp:368-374, trace.cpp:60-83) */
+uint64_t sb_kv_root_hash(void);
+/* Host-side single chain hash, for bindings that need one value. */
+uint64_t sb_kv_chain_hash_host(uint64_t parent, const uint64_t* tokens, int64_t n);
+
+/* Batched chain hashing on the device.  Sequence s spans
+ * d_tokens[d_seq_offsets[s] .. d_seq_offsets[s+1]); its blocks of
+ * `block_size` tokens (last one partial) get their chain hashes written to
+ * d_block_hashes[d_block_offsets[s] + j].  The chain for sequence s starts
+ * from d_parent[s] (NULL = kv_root_hash()).  Replaces the per-block
+ * kv_chain_hash loop inside KvCache::lookup_prefix / insert
+ * (kv_cache.cpp:423-431, 471-475). */
+int sb_chain_hash_batch(const uint64_t* d_tokens, const int64_t* d_seq_offsets,
+                        const int64_t* d_block_offsets, const uint64_t* d_parent,
+                        int32_t n_seqs, int64_t block_size, uint64_t* d_block_hashes,
+                        void* stream);
+
+/* Device-side synthetic token materialisation (trace.cpp:70-78 and
+ * decode_token trace.cpp:80-83).  section_tag uses agentsim::SectionTag order
+ * (trace.hpp:18): 0 system, 1 user, 2 tool_output, 3 history. */
+int sb_materialize_tokens(int32_t section_tag, int64_t length, uint64_t content_key,
+                          int32_t src_iteration, uint64_t* d_out, void* stream);
+int sb_decode_tokens(uint64_t stream_key, int64_t first_index, int64_t count, uint64_t* d_out,
+                     void* stream);
+
+/* ---- KV block pool / block table: agentsim::KvCache (kv_cache.hpp:269) -- */
+/* KvCache::KvCache(const CacheConfig&)          kv_cache.cpp:376 */
+int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, int32_t device,
+                 sb_kv_cache** out);
+void sb_kv_destroy(sb_kv_cache* cache);
+
+/* KvCache::lookup_prefix(tokens, now)            kv_cache.cpp:418  (host tokens) */
+int sb_kv_lookup_prefix(sb_kv_cache* cache, const uint64_t* tokens, int64_t n_tokens,
+                        int64_t now, int64_t* hit_tokens);
+/* KvCache::insert(tokens, tags, now)             kv_cache.cpp:436
+ * out_ids must hold ceil(n_tokens / block_size) entries.  On CacheFull the
+ * reference's rollback is reproduced (kv_cache.cpp:463-469, 481-487). */
+int sb_kv_insert(sb_kv_cache* cache, const uint64_t* tokens, int64_t n_tokens,
+                 const sb_tag_range* tags, int64_t n_tags, int64_t now, int32_t* out_ids,
+                 int64_t* n_out);
+/* KvCache::evict(needed)                         kv_cache.cpp:510
+ * out_ids must hold `needed` entries; *n_out < needed signals shortfall. */
+int sb_kv_evict(sb_kv_cache* cache, int64_t needed, int32_t* out_ids, int64_t* n_out);
+/* KvCache::set_reuse_priority(ids, update)       kv_cache.cpp:542
+ * pinned: -1 = leave, 0 = unpin, 1 = pin; tier_override: -1 = none, else tag. */
+int sb_kv_set_reuse_priority(sb_kv_cache* cache, const int32_t* ids, int64_t n, int32_t pinned,
+                             int32_t tier_override);
+/* KvCache::set_tag(id, tag)                      kv_cache.cpp:555 */
+int sb_kv_set_tag(sb_kv_cache* cache, int32_t id, int32_t tag);
+/* KvCache::release(ids)                          kv_cache.cpp:561 */
+int sb_kv_release(sb_kv_cache* cache, const int32_t* ids, int64_t n);
+/* KvCache::touch(ids, now)                       kv_cache.cpp:571 */
+int sb_kv_touch(sb_kv_cache* cache, const int32_t* ids, int64_t n, int64_t now);
+
+int64_t sb_kv_block_size(const sb_kv_cache* cache);
+int64_t sb_kv_resident_blocks(const sb_kv_cache* cache); /* kv_cache.hpp:300 */
+int64_t sb_kv_capacity_blocks(const sb_kv_cache* cache); /* kv_cache.hpp:301 */
+int64_t sb_kv_free_blocks(const sb_kv_cache* cache);     /* kv_cache.hpp:302 */
+uint64_t sb_kv_total_evicted(const sb_kv_cache* cache);  /* kv_cache.hpp:303 */
+int32_t sb_kv_policy(const sb_kv_cache* cache);
+/* KvCache::contains(id) — 1 resident, 0 not      kv_cache.hpp:305 */
+int sb_kv_contains(const sb_kv_cache* cache, int32_t id);
+/* KvCache::block(id); tokens_out may be NULL, else holds block_size u64. */
+int sb_kv_block(const sb_kv_cache* cache, int32_t id, sb_block_info* info, uint64_t* tokens_out);
+/* KvCache::audit()                                kv_cache.cpp:575 */
+int sb_kv_audit(const sb_kv_cache* cache);
+/* KvCache::dump() — byte-identical text; *len receives the full length
+ * (call with buf=NULL to size).                   kv_cache.cpp:601 */
+int sb_kv_dump(const sb_kv_cache* cache, char* buf, int64_t cap, int64_t* len);
+
+/* ---- batched, stream-ordered engine path (no host round trip) --------- */
+/* Batched lookup_prefix: sequence s is d_tokens[d_seq_offsets[s]..[s+1]);
+ * d_hit_tokens[s] receives its hit length.  Touch semantics are identical to
+ * calling lookup_prefix for each sequence at the same `now`. */
+int sb_kv_lookup_prefix_batch(sb_kv_cache* cache, const uint64_t* d_tokens,
+                              const int64_t* d_seq_offsets, int32_t n_seqs, int64_t now,
+                              int64_t* d_hit_tokens, void* stream);
+/* Batched insert with the reference's sequential semantics (sequence 0 is
+ * applied first).  Tag ranges for sequence s are
+ * d_tags[d_tag_offsets[s]..[s+1]) with sequence-local token positions.
+ * d_out_ids[d_block_offsets[s] + j] receive block ids; d_status[s] a status
+ * code.  Optional d_block_hashes (NULL = computed here) are precomputed chain
+ * hashes laid out like d_out_ids. */
+int sb_kv_insert_batch(sb_kv_cache* cache, const uint64_t* d_tokens,
+                       const int64_t* d_seq_offsets, const sb_tag_range* d_tags,
+                       const int64_t* d_tag_offsets, const int64_t* d_block_offsets,
+                       const uint64_t* d_block_hashes, int32_t n_seqs, int64_t now,
+                       int32_t* d_out_ids, int32_t* d_status, void* stream);
+/* Batched release of d_ids[0..n). */
+int sb_kv_release_batch(sb_kv_cache* cache, const int32_t* d_ids, int64_t n, int32_t* d_status,
+                        void* stream);
+/* Counters for the cross-GPU statistics reduction: [lookups, hit_tokens,
+ * looked_up_tokens, inserted_blocks, evicted_blocks, cache_full_events]. */
+int sb_kv_stats(const sb_kv_cache* cache, uint64_t out[6]);
+
+/* ---- continuation-prefill attention over the paged pool --------------- */
+/* Replaces the prefill cost model of the reference engine
+ * (CostModel::chunk_ms, engine.cpp:35-39; charged in Engine::start_step,
+ * engine.cpp:424-427) with the real computation for extend_prefill
+ * (engine.cpp:184-223): each sequence's new (suffix) tokens attend to its
+ * cached prefix plus causally to themselves.
+ *
+ *  q        [total_q, n_q_heads, head_dim] bf16 (suffix queries, packed)
+ *  k_pool,v_pool [n_pool_blocks, n_kv_heads, page_size, head_dim] bf16
+ *  out      [total_q, n_q_heads, head_dim] bf16
+ *  d_q_offsets[s]..[s+1]   rows of q for sequence s (n_q_heads rows each token)
+ *  d_kv_lens[s]            total keys of s (prefix + suffix); the suffix
+ *                          occupies the last (q_len) positions
+ *  d_block_table[s*max_blocks + j]  pool block of key positions
+ *                          [j*page_size, (j+1)*page_size)
+ * head_dim must be 128, page_size 16, n_q_heads % n_kv_heads == 0. */
+int sb_continuation_attention(const void* q, const void* k_pool, const void* v_pool, void* out,
+                              const int32_t* d_q_offsets, const int32_t* d_kv_lens,
+                              const int32_t* d_block_table, int32_t n_seqs,
+                              int32_t max_blocks_per_seq, int32_t max_q_len, int32_t n_q_heads,
+                              int32_t n_kv_heads, int32_t head_dim, int32_t page_size,
+                              int64_t n_pool_blocks, float softmax_scale, void* stream);
+
+/* Scatter the suffix K/V rows into their pool pages (the KV write of
+ * extend_prefill).  k_new/v_new [total_q, n_kv_heads, head_dim]. */
+int sb_kv_append(const void* k_new, const void* v_new, void* k_pool, void* v_pool,
+                 const int32_t* d_q_offsets, const int32_t* d_kv_lens,
+                 const int32_t* d_block_table, int32_t n_seqs, int32_t max_blocks_per_seq,
+                 int32_t n_kv_heads, int32_t head_dim, int32_t page_size, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SUTRADHARA_B200_H_ */

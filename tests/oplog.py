@@ -1,0 +1,115 @@
+"""Replays a golden KvCache op log (tests/golden/oplog_*.jsonl.gz, produced by
+the reference itself — see oracle/gen_golden.py) against any cache object with
+the reference's call surface and reports every divergence.
+
+The cache factory receives (block_size, capacity, policy).  Methods used:
+lookup_prefix, insert, evict, set_reuse_priority, set_tag, release, touch,
+block, dump, audit, total_evicted.  Status codes follow
+include/sutradhara_b200.h.
+"""
+from __future__ import annotations
+
+import base64
+import gzip
+import json
+import os
+from typing import Callable, List
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def fnv(s: str) -> str:
+    from oracle import oracle as O  # C implementation of FNV-1a (test infrastructure)
+
+    return str(O.fnv1a(s))
+
+
+def load(name: str) -> List[dict]:
+    with gzip.open(os.path.join(GOLDEN, name), "rt") as f:
+        return [json.loads(line) for line in f if line.strip()]
+
+
+def golden_logs(prefix: str = "oplog_") -> List[str]:
+    return sorted(n for n in os.listdir(GOLDEN) if n.startswith(prefix) and n.endswith(".jsonl.gz"))
+
+
+def tokens_of(rec: dict) -> np.ndarray:
+    return np.frombuffer(base64.b64decode(rec["tokens"]), dtype=np.uint64).copy()
+
+
+def replay(ops: List[dict], factory: Callable, check_dump: bool = True, max_errors: int = 5) -> List[str]:
+    errs: List[str] = []
+    cache = None
+
+    def bad(i, what):
+        errs.append(f"op#{i} {ops[i]['op']}: {what}")
+
+    for i, r in enumerate(ops):
+        op = r["op"]
+        if op == "create":
+            cache = factory(r["block_size"], r["capacity"], r["policy"])
+            continue
+        if op == "lookup":
+            got = cache.lookup_prefix(tokens_of(r), r["now"])
+            if got != r["ret"]:
+                bad(i, f"hit {got} != {r['ret']}")
+        elif op == "insert":
+            tags = [tuple(t) for t in r["tags"]]
+            st, ids = cache.insert(tokens_of(r), tags, r["now"])
+            if st != r["status"]:
+                bad(i, f"status {st} != {r['status']}")
+            elif st == 0 and list(ids) != list(r["ids"]):
+                bad(i, f"ids {list(ids)[:8]}.. != {r['ids'][:8]}..")
+        elif op == "evict":
+            st, ids = cache.evict(r["needed"])
+            if list(ids) != list(r["ret"]):
+                bad(i, f"evicted {list(ids)[:8]} != {r['ret'][:8]}")
+        elif op == "set_priority":
+            st = cache.set_reuse_priority(r["ids"], r["pinned"], r["tier"])
+            if st != r["status"]:
+                bad(i, f"status {st} != {r['status']}")
+        elif op == "set_tag":
+            st = cache.set_tag(r["id"], r["tag"])
+            if st != r["status"]:
+                bad(i, f"status {st} != {r['status']}")
+        elif op == "release":
+            st = cache.release(r["ids"])
+            if st != r["status"]:
+                bad(i, f"status {st} != {r['status']}")
+        elif op == "touch":
+            st = cache.touch(r["ids"], r["now"])
+            if st != r["status"]:
+                bad(i, f"status {st} != {r['status']}")
+        elif op == "block":
+            st, info = cache.block(r["id"])
+            if st != r["status"]:
+                bad(i, f"status {st} != {r['status']}")
+            elif st == 0:
+                for k in ("tag", "tier", "ref", "pinned", "ntok", "last"):
+                    if info[k] != r[k]:
+                        bad(i, f"{k} {info[k]} != {r[k]}")
+                if str(info["chain"]) != r["chain"] or str(info["parent"]) != r["parent"]:
+                    bad(i, "chain/parent hash mismatch")
+            continue
+        elif op == "audit":
+            st = cache.audit()
+            if st != r["status"]:
+                bad(i, f"audit {st} != {r['status']}")
+            continue
+        elif op == "final":
+            d = cache.dump()
+            if d != r["dump"]:
+                bad(i, "final dump differs")
+            if cache.total_evicted() != r["total_evicted"]:
+                bad(i, f"total_evicted {cache.total_evicted()} != {r['total_evicted']}")
+            continue
+        if check_dump and "dump_fnv" in r:
+            if fnv(cache.dump()) != r["dump_fnv"]:
+                bad(i, "cache state (dump digest) differs")
+        if len(errs) >= max_errors:
+            break
+    if cache is not None and hasattr(cache, "close"):
+        cache.close()
+    return errs
