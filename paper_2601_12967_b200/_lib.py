@@ -1,0 +1,93 @@
+"""Loader for the in-tree sm_100a library (paper_2601_12967_b200/_build).
+
+No fallback: if the CUDA library is missing the import of any op fails
+loudly with the command that builds it."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from . import errors
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "_build", "libsutradhara_b200.so")
+
+_lock = threading.Lock()
+_lib = None
+
+U64P = C.POINTER(C.c_uint64)
+I64P = C.POINTER(C.c_int64)
+I32P = C.POINTER(C.c_int32)
+VP = C.c_void_p
+
+
+class TagRange(C.Structure):
+    _fields_ = [("begin", C.c_int64), ("end", C.c_int64), ("tag", C.c_int32), ("_pad", C.c_int32)]
+
+
+class BlockInfo(C.Structure):
+    _fields_ = [("block_id", C.c_int32), ("tag", C.c_int32), ("tier", C.c_int32), ("ref_count", C.c_int32),
+                ("last_used", C.c_int64), ("chain_hash", C.c_uint64), ("parent_hash", C.c_uint64),
+                ("pinned", C.c_int32), ("n_tokens", C.c_int32)]
+
+
+# name -> (restype, argtypes); mirrors include/sutradhara_b200.h
+SIGNATURES = {
+    "sb_last_error": (C.c_char_p, []),
+    "sb_version": (C.c_char_p, []),
+    "sb_kv_root_hash": (C.c_uint64, []),
+    "sb_kv_chain_hash_host": (C.c_uint64, [C.c_uint64, U64P, C.c_int64]),
+    "sb_chain_hash_batch": (C.c_int, [VP, VP, VP, VP, C.c_int32, C.c_int64, VP, VP]),
+    "sb_materialize_tokens": (C.c_int, [C.c_int32, C.c_int64, C.c_uint64, C.c_int32, VP, VP]),
+    "sb_decode_tokens": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, VP, VP]),
+    "sb_kv_create": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.POINTER(VP)]),
+    "sb_kv_destroy": (None, [VP]),
+    "sb_kv_lookup_prefix": (C.c_int, [VP, U64P, C.c_int64, C.c_int64, I64P]),
+    "sb_kv_insert": (C.c_int, [VP, U64P, C.c_int64, C.POINTER(TagRange), C.c_int64, C.c_int64, I32P, I64P]),
+    "sb_kv_evict": (C.c_int, [VP, C.c_int64, I32P, I64P]),
+    "sb_kv_set_reuse_priority": (C.c_int, [VP, I32P, C.c_int64, C.c_int32, C.c_int32]),
+    "sb_kv_set_tag": (C.c_int, [VP, C.c_int32, C.c_int32]),
+    "sb_kv_release": (C.c_int, [VP, I32P, C.c_int64]),
+    "sb_kv_touch": (C.c_int, [VP, I32P, C.c_int64, C.c_int64]),
+    "sb_kv_block_size": (C.c_int64, [VP]),
+    "sb_kv_resident_blocks": (C.c_int64, [VP]),
+    "sb_kv_capacity_blocks": (C.c_int64, [VP]),
+    "sb_kv_free_blocks": (C.c_int64, [VP]),
+    "sb_kv_total_evicted": (C.c_uint64, [VP]),
+    "sb_kv_policy": (C.c_int32, [VP]),
+    "sb_kv_contains": (C.c_int, [VP, C.c_int32]),
+    "sb_kv_block": (C.c_int, [VP, C.c_int32, C.POINTER(BlockInfo), U64P]),
+    "sb_kv_audit": (C.c_int, [VP]),
+    "sb_kv_dump": (C.c_int, [VP, C.c_char_p, C.c_int64, I64P]),
+    "sb_kv_lookup_prefix_batch": (C.c_int, [VP, VP, VP, C.c_int32, C.c_int64, VP, VP]),
+    "sb_kv_insert_batch": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int64, VP, VP, VP]),
+    "sb_kv_release_batch": (C.c_int, [VP, VP, C.c_int64, VP, VP]),
+    "sb_kv_stats": (C.c_int, [VP, U64P]),
+    "sb_continuation_attention": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                            C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_float, VP]),
+    "sb_kv_append": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, VP]),
+}
+
+
+def lib():
+    """The loaded library (raises if it was not built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(f"{LIB_PATH} missing — build it with `python -m paper_2601_12967_b200.build` "
+                                   "(no CPU fallback exists)")
+            L = C.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib
+
+
+def check(status: int, what: str = ""):
+    if status != 0:
+        msg = lib().sb_last_error().decode(errors="replace")
+        raise errors.from_status(status, f"{what}: {msg}" if what else msg)

@@ -1,0 +1,399 @@
+// attention.cu — continuation-prefill attention over the paged KV pool
+// (sm_100a: TMA + tcgen05/TMEM), plus the KV append of the suffix tokens.
+//
+// Replaces the reference engine's prefill cost model (CostModel::chunk_ms,
+// /root/reference/proj/src/engine.cpp:35-39) for Engine::extend_prefill
+// (engine.cpp:184-223): the suffix (tool-output) tokens of each sequence
+// attend to the already-cached prefix pages plus causally to themselves.
+//
+// Work item = (sequence, kv head, pair of 128-row query tiles).  A query tile
+// packs tokens x GQA heads of one kv head into the 128 MMA rows
+// (row = token * group + head), so every K/V page is read once for the whole
+// group.  One CTA per SM (192 KB smem, 512 TMEM columns):
+//   warp 0      TMA producer: Q tiles once, then K/V pages (16 tokens x 64
+//               dims boxes, SWIZZLE_128B) into a 4-stage ring
+//   warp 1      MMA issuer (one thread): S_t = Q_t K^T  (SS, K-major),
+//               O_t += P_t V (TS: P from TMEM, V MN-major)
+//   warp 2      TMEM allocator
+//   warps 4-7   softmax for tile 0, warps 8-11 softmax for tile 1: one TMEM
+//               lane (= one query row) per thread; online softmax with a
+//               lazy rescale (O is rescaled in TMEM only when the running
+//               max grows by more than 2^8)
+// TMEM columns: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P_t is
+// written as packed bf16 over the first 64 columns of S_t.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "common.h"
+#include "sm100.cuh"
+#include "tma_host.h"
+
+namespace sb {
+namespace attn {
+
+constexpr int kThreads = 384;
+constexpr int kStages = 4;
+constexpr int kTileBytes = 32768;  // 128 rows x 128 dims bf16 (two 64-col SW128 atoms)
+constexpr int kAtomBytes = 16384;
+constexpr int kSmemBytes = 2 * kTileBytes + kStages * kTileBytes + 1024;
+
+struct Params {
+  const int32_t* q_off;
+  const int32_t* kv_len;
+  const int32_t* table;
+  __nv_bfloat16* out;
+  int32_t n_seqs, max_blocks, n_q_heads, n_kv_heads, group, tpt, pairs_per_seq;
+  int32_t oob_row;  // a K/V row coordinate past the end: zero-filled loads
+  float scale_log2;
+};
+
+struct Smem {
+  uint64_t q_full;
+  uint64_t kv_full[kStages];
+  uint64_t kv_empty[kStages];
+  uint64_t s_full[2];
+  uint64_t p_full[2];
+  uint64_t o_done[2];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_continuation_attention(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                             const __grid_constant__ CUtensorMap tm_v, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = base;                    // [2 tiles][2 atoms][16 KB]
+  uint8_t* sKV = base + 2 * kTileBytes;  // [kStages][2 atoms][16 KB]
+  __shared__ Smem ss;
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  // ---- work item
+  const int item = blockIdx.x;
+  const int pair = item % p.pairs_per_seq;
+  const int kvh = (item / p.pairs_per_seq) % p.n_kv_heads;
+  const int seq = item / (p.pairs_per_seq * p.n_kv_heads);
+  const int q0 = p.q_off[seq];
+  const int q_len = p.q_off[seq + 1] - q0;
+  const int kv_len = p.kv_len[seq];
+  const int first_q = pair * 2 * p.tpt;  // query index (within sequence) of row 0 of tile 0
+  if (first_q >= q_len) return;
+  const int prefix = kv_len - q_len;
+  const int kv_limit = prefix + min(q_len, first_q + 2 * p.tpt);
+  const int n_kv = (kv_limit + 127) / 128;
+
+  if (tid == 0) {
+    mbar_init(&ss.q_full, 1);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&ss.kv_full[i], 1);
+      mbar_init(&ss.kv_empty[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&ss.s_full[t], 1);
+      mbar_init(&ss.p_full[t], 128);
+      mbar_init(&ss.o_done[t], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&ss.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = ss.tmem_base;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (elect_one()) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      mbar_arrive_expect_tx(&ss.q_full, 2 * kTileBytes);
+      for (int t = 0; t < 2; ++t)
+        for (int a = 0; a < 2; ++a)
+          tma_load_3d(sQ + t * kTileBytes + a * kAtomBytes, &tm_q, &ss.q_full, a * 64, kvh * p.group,
+                      q0 + first_q + t * p.tpt);
+      const int32_t* trow = p.table + static_cast<int64_t>(seq) * p.max_blocks;
+      for (int i = 0; i < 2 * n_kv; ++i) {
+        const int j = i >> 1, which = i & 1, stage = i % kStages;
+        mbar_wait(&ss.kv_empty[stage], ((i / kStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&ss.kv_full[stage], kTileBytes);
+        uint8_t* dst = sKV + stage * kTileBytes;
+        const void* tm = which ? static_cast<const void*>(&tm_v) : static_cast<const void*>(&tm_k);
+#pragma unroll
+        for (int pg = 0; pg < 8; ++pg) {
+          const int jb = j * 8 + pg;
+          const int row = (jb * 16 < kv_limit) ? (trow[jb] * p.n_kv_heads + kvh) * 16 : p.oob_row;
+#pragma unroll
+          for (int a = 0; a < 2; ++a) tma_load_2d(dst + a * kAtomBytes + pg * 2048, tm, &ss.kv_full[stage], a * 64, row);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (elect_one()) {
+      const uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
+      const uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
+      const uint32_t sq = smem_u32(sQ), skv = smem_u32(sKV);
+      mbar_wait(&ss.q_full, 0);
+      auto wait_stage = [&](int i) { mbar_wait(&ss.kv_full[i % kStages], (i / kStages) & 1); };
+      auto qk = [&](int t, int j) {
+        const uint32_t kb = skv + ((2 * j) % kStages) * kTileBytes;
+        const uint32_t qb = sq + t * kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
+          mma_ss(tmem + t * 128, smem_desc_sw128(qb + off, 16, 1024), smem_desc_sw128(kb + off, 16, 1024), idesc_qk,
+                 kk > 0);
+        }
+        mma_commit(&ss.s_full[t]);
+      };
+      auto pv = [&](int t, int j) {
+        mbar_wait(&ss.p_full[t], j & 1);
+        tc_fence_after();
+        const uint32_t vb = skv + ((2 * j + 1) % kStages) * kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, smem_desc_sw128(vb + kk * 2048, kAtomBytes, 1024),
+                 idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&ss.o_done[t]);
+      };
+      wait_stage(0);
+      tc_fence_after();
+      qk(0, 0);
+      qk(1, 0);
+      mma_commit(&ss.kv_empty[0]);
+      for (int j = 0; j < n_kv; ++j) {
+        wait_stage(2 * j + 1);
+        tc_fence_after();
+        pv(0, j);
+        if (j + 1 < n_kv) {
+          wait_stage(2 * j + 2);
+          tc_fence_after();
+          qk(0, j + 1);
+        }
+        pv(1, j);
+        mma_commit(&ss.kv_empty[(2 * j + 1) % kStages]);
+        if (j + 1 < n_kv) {
+          qk(1, j + 1);
+          mma_commit(&ss.kv_empty[(2 * j + 2) % kStages]);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== softmax (one query row per thread) =====================
+    const int t = (warp - 4) >> 2;  // tile of this warpgroup
+    const int r = tid - 128 - t * 128;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t s_col = tmem + lane_off + t * 128;
+    const uint32_t o_col = tmem + lane_off + 256 + t * 128;
+    const int qidx = first_q + t * p.tpt + r / p.group;
+    const int qpos = prefix + qidx;  // absolute key position of this query
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      mbar_wait(&ss.s_full[t], j & 1);
+      tc_fence_after();
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld32(s_col + c * 32, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 32; ++k) s[c * 32 + k] = __uint_as_float(v[k]) * p.scale_log2;
+      }
+      const int kbase = j * 128;
+      if (kbase + 127 > qpos) {
+#pragma unroll
+        for (int k = 0; k < 128; ++k)
+          if (kbase + k > qpos) s[k] = -INFINITY;
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int k = 1; k < 128; ++k) mx = fmaxf(mx, s[k]);
+      const float m_new = fmaxf(m_used, mx);
+      const bool need = m_new > m_used + 8.f;
+      float factor = 1.f;
+      if (need) {
+        factor = ex2(m_used - m_new);  // 0 on the first tile (m_used = -inf)
+        m_used = m_new;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+        // rescale this warp's rows of O in TMEM once PV_{j-1} has landed
+        mbar_wait(&ss.o_done[t], (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint32_t v[16];
+          tmem_ld16(o_col + c * 16, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] = __float_as_uint(__uint_as_float(v[k]) * factor);
+          tmem_st16(o_col + c * 16, v);
+        }
+      }
+      l *= factor;
+      uint32_t pk[64];
+      float sum = 0.f;
+#pragma unroll
+      for (int k = 0; k < 64; ++k) {
+        const float e0 = ex2(s[2 * k] - m_used), e1 = ex2(s[2 * k + 1] - m_used);
+        sum += e0 + e1;
+        pk[k] = pack_bf16x2(e0, e1);
+      }
+      l += sum;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t w[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) w[k] = pk[c * 32 + k];
+        tmem_st32(s_col + c * 32, w);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&ss.p_full[t]);
+    }
+    // ---- epilogue: O / l -> bf16 -> global
+    mbar_wait(&ss.o_done[t], (n_kv - 1) & 1);
+    tc_fence_after();
+    const bool valid = qidx < q_len;
+    const float inv = (valid && l > 0.f) ? 1.f / l : 0.f;
+    __nv_bfloat16* orow =
+        p.out + (static_cast<int64_t>(q0 + qidx) * p.n_q_heads + kvh * p.group + (r % p.group)) * 128;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t v[32];
+      tmem_ld32(o_col + c * 32, v);
+      tmem_wait_ld();
+      if (valid) {
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(v[8 * k + 0]) * inv, __uint_as_float(v[8 * k + 1]) * inv);
+          w.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * inv, __uint_as_float(v[8 * k + 3]) * inv);
+          w.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * inv, __uint_as_float(v[8 * k + 5]) * inv);
+          w.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * inv, __uint_as_float(v[8 * k + 7]) * inv);
+          dst[k] = w;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// KV append: write the suffix K/V rows into their pool pages.
+__global__ void k_kv_append(const __nv_bfloat16* __restrict__ k_new, const __nv_bfloat16* __restrict__ v_new,
+                            __nv_bfloat16* __restrict__ k_pool, __nv_bfloat16* __restrict__ v_pool,
+                            const int32_t* __restrict__ q_off, const int32_t* __restrict__ kv_len,
+                            const int32_t* __restrict__ table, int32_t n_seqs, int32_t max_blocks, int32_t n_kv_heads,
+                            int32_t page) {
+  // one thread per (token, kv head, 16-byte chunk): 16 chunks per 128-dim row
+  const int64_t total_tok = q_off[n_seqs];
+  const int64_t n = total_tok * n_kv_heads * 16;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int chunk = static_cast<int>(i & 15);
+    const int64_t th = i >> 4;
+    const int kvh = static_cast<int>(th % n_kv_heads);
+    const int64_t tok = th / n_kv_heads;
+    int lo = 0, hi = n_seqs;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (q_off[mid] <= tok) lo = mid; else hi = mid;
+    }
+    const int s = lo;
+    const int64_t pos = kv_len[s] - (q_off[s + 1] - q_off[s]) + (tok - q_off[s]);
+    const int64_t blk = table[static_cast<int64_t>(s) * max_blocks + pos / page];
+    const int64_t dst = ((blk * n_kv_heads + kvh) * page + pos % page) * 128 + chunk * 8;
+    const int64_t src = (tok * n_kv_heads + kvh) * 128 + chunk * 8;
+    *reinterpret_cast<uint4*>(k_pool + dst) = __ldg(reinterpret_cast<const uint4*>(k_new + src));
+    *reinterpret_cast<uint4*>(v_pool + dst) = __ldg(reinterpret_cast<const uint4*>(v_new + src));
+  }
+}
+
+}  // namespace attn
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" int sb_continuation_attention(const void* q, const void* k_pool, const void* v_pool, void* out,
+                                         const int32_t* d_q_offsets, const int32_t* d_kv_lens,
+                                         const int32_t* d_block_table, int32_t n_seqs, int32_t max_blocks_per_seq,
+                                         int32_t max_q_len, int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim,
+                                         int32_t page_size, int64_t n_pool_blocks, float softmax_scale, void* stream) {
+  return guard([&] {
+    if (head_dim != 128 || page_size != 16) throw Error(SB_ERR_UNSUPPORTED, "head_dim must be 128 and page_size 16");
+    if (n_kv_heads <= 0 || n_q_heads % n_kv_heads) throw Error(SB_ERR_INVALID, "n_q_heads % n_kv_heads != 0");
+    const int group = n_q_heads / n_kv_heads;
+    if (group > 128 || 128 % group) throw Error(SB_ERR_UNSUPPORTED, "GQA group must divide 128");
+    if (n_seqs <= 0 || max_q_len <= 0) return int(SB_OK);
+    const int64_t kv_rows = n_pool_blocks * n_kv_heads * page_size;
+    if (kv_rows + 16 >= (int64_t(1) << 31)) throw Error(SB_ERR_UNSUPPORTED, "KV pool too large for 32-bit TMA rows");
+    const int tpt = 128 / group;
+    int total_q = 0;
+    SB_CUDA(cudaMemcpyAsync(&total_q, d_q_offsets + n_seqs, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                            static_cast<cudaStream_t>(stream)));
+    SB_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    if (total_q <= 0) return int(SB_OK);
+    uint64_t qdims[3] = {128, static_cast<uint64_t>(n_q_heads), static_cast<uint64_t>(total_q)};
+    uint64_t qstr[2] = {128 * 2, static_cast<uint64_t>(n_q_heads) * 128 * 2};
+    uint32_t qbox[3] = {64, static_cast<uint32_t>(group), static_cast<uint32_t>(tpt)};
+    CUtensorMap tm_q = make_tmap_bf16(q, 3, qdims, qstr, qbox);
+    uint64_t kdims[2] = {128, static_cast<uint64_t>(kv_rows)};
+    uint64_t kstr[1] = {128 * 2};
+    uint32_t kbox[2] = {64, 16};
+    CUtensorMap tm_k = make_tmap_bf16(k_pool, 2, kdims, kstr, kbox);
+    CUtensorMap tm_v = make_tmap_bf16(v_pool, 2, kdims, kstr, kbox);
+    attn::Params prm;
+    prm.q_off = d_q_offsets;
+    prm.kv_len = d_kv_lens;
+    prm.table = d_block_table;
+    prm.out = static_cast<__nv_bfloat16*>(out);
+    prm.n_seqs = n_seqs;
+    prm.max_blocks = max_blocks_per_seq;
+    prm.n_q_heads = n_q_heads;
+    prm.n_kv_heads = n_kv_heads;
+    prm.group = group;
+    prm.tpt = tpt;
+    prm.pairs_per_seq = (max_q_len + 2 * tpt - 1) / (2 * tpt);
+    prm.oob_row = static_cast<int32_t>(kv_rows);
+    prm.scale_log2 = softmax_scale * 1.4426950408889634f;
+    static bool attr_set = false;
+    if (!attr_set) {
+      SB_CUDA(cudaFuncSetAttribute(attn::k_continuation_attention, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   attn::kSmemBytes));
+      attr_set = true;
+    }
+    const int64_t grid = static_cast<int64_t>(n_seqs) * n_kv_heads * prm.pairs_per_seq;
+    attn::k_continuation_attention<<<static_cast<unsigned>(grid), attn::kThreads, attn::kSmemBytes,
+                                     static_cast<cudaStream_t>(stream)>>>(tm_q, tm_k, tm_v, prm);
+    SB_CHECK_LAUNCH();
+    return int(SB_OK);
+  });
+}
+
+extern "C" int sb_kv_append(const void* k_new, const void* v_new, void* k_pool, void* v_pool,
+                            const int32_t* d_q_offsets, const int32_t* d_kv_lens, const int32_t* d_block_table,
+                            int32_t n_seqs, int32_t max_blocks_per_seq, int32_t n_kv_heads, int32_t head_dim,
+                            int32_t page_size, void* stream) {
+  return guard([&] {
+    if (head_dim != 128) throw Error(SB_ERR_UNSUPPORTED, "head_dim must be 128");
+    if (n_seqs <= 0) return int(SB_OK);
+    attn::k_kv_append<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const __nv_bfloat16*>(k_new), static_cast<const __nv_bfloat16*>(v_new),
+        static_cast<__nv_bfloat16*>(k_pool), static_cast<__nv_bfloat16*>(v_pool), d_q_offsets, d_kv_lens,
+        d_block_table, n_seqs, max_blocks_per_seq, n_kv_heads, page_size);
+    SB_CHECK_LAUNCH();
+    return int(SB_OK);
+  });
+}

@@ -1,0 +1,1307 @@
+// kv_pool.cu — device-resident paged-KV block pool + prefix-indexed block
+// table with hint-aware (tiered) eviction, bit-exact with the reference
+// KvCache (/root/reference/proj/src/kv_cache.cpp).
+//
+// Layout in HBM (structure of arrays, one slot per pool block id):
+//   tok[cap*bs] u64   block token contents (full-token compare on hash match)
+//   ntok[cap]   i32   tokens in block, 0 = free slot
+//   chain/parent[cap] u64  chain hash of the block / of its predecessor
+//   tag, ref, pinned [cap] i32, last[cap] i64
+//   index: open-addressed multimap chain_hash -> block id (tcap = 4*cap
+//          slots, -1 empty, -2 tombstone), slot[cap] = index slot of a block
+//
+// One insert (kv_cache.cpp:436-508) is five stream-ordered kernels, no host
+// round trip:
+//   k_probe   (all positions in parallel) find the resident block of each
+//             position in the PRE-insert state (chain hash + parent + tokens)
+//   k_select  (1 CTA) hint-aware eviction scoring: key = (tier, last_used,
+//             id) per candidate, radix-select of the K smallest, sorted
+//   k_walk    (1 thread) replays the reference's sequential decisions from
+//             the first pre-miss: hit / allocate lowest free id / evict the
+//             next victim (skipping blocks hit earlier in this insert) /
+//             CacheFull with rollback
+//   k_commit_evict, k_commit_apply  apply evictions, then hits + new blocks
+// Chain hashes are computed by k_chain_hash (one thread per sequence; the
+// hash is a sequential fold over tokens) or supplied precomputed.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "hash.cuh"
+
+namespace sb {
+
+constexpr int64_t kLastBias = int64_t(1) << 39;
+constexpr int kIdBits = 21;
+constexpr uint64_t kIdMask = (uint64_t(1) << kIdBits) - 1;
+constexpr uint64_t kNoKey = ~uint64_t(0);
+constexpr int kSelectThreads = 1024;
+constexpr int kSortSmemKeys = 8192;
+
+enum Ctr { C_NRES = 0, C_EVICTED, C_LOOKUPS, C_HIT_TOK, C_LOOK_TOK, C_INS_BLOCKS, C_EV_BLOCKS, C_FULL, C_N };
+enum Scal { S_F = 0, S_K, S_FREE, S_NEV, S_STATUS, S_FAILPOS, S_NNEW, S_NCAND, S_ERRIDX, S_N };
+
+struct Pool {
+  int64_t bs, cap, tcap;
+  int32_t policy;
+  uint64_t* tok;
+  int32_t* ntok;
+  uint64_t* chain;
+  uint64_t* parent;
+  int32_t* tag;
+  int32_t* ref;
+  int32_t* pinned;
+  int64_t* last;
+  uint64_t* tkey;
+  int32_t* tval;
+  int32_t* slot;
+  unsigned long long* ctr;
+};
+
+struct Scratch {
+  int64_t pmax = 0, kmax = 0;
+  uint64_t* hashes = nullptr;   // pmax
+  int32_t* prehit = nullptr;    // pmax
+  int32_t* chain_out = nullptr; // pmax
+  int8_t* kind = nullptr;       // pmax (0 hit, 1 new)
+  int32_t* freel = nullptr;     // pmax
+  int32_t* evicted = nullptr;   // max(pmax, cap)
+  uint64_t* victims = nullptr;  // kmax
+  uint8_t* taken = nullptr;     // kmax
+  int32_t* rank_of = nullptr;   // cap
+  uint64_t* keys = nullptr;     // cap
+  uint64_t* sortbuf = nullptr;  // kmax (global sort fallback)
+  int64_t* scal = nullptr;      // S_N
+};
+
+__device__ __forceinline__ uint64_t index_slot(uint64_t h, int64_t tcap) {
+  return (h ^ (h >> 29) ^ (h >> 47)) & static_cast<uint64_t>(tcap - 1);
+}
+
+__device__ __forceinline__ bool is_candidate(const Pool& P, int32_t id) {
+  return P.ntok[id] > 0 && P.ref[id] == 0 && P.pinned[id] == 0;
+}
+
+__device__ __forceinline__ uint64_t victim_key(const Pool& P, int32_t id) {
+  uint64_t k = (static_cast<uint64_t>(P.last[id] + kLastBias) << kIdBits) | static_cast<uint64_t>(id);
+  if (P.policy == SB_POLICY_TIERED) k |= static_cast<uint64_t>(tier_of(P.tag[id])) << 61;
+  return k;
+}
+
+// Resident block with (chain_hash, parent_hash, tokens), -1 if none
+// (find_chain_block, kv_cache.cpp:403-416).
+__device__ int32_t probe_find(const Pool& P, uint64_t h, uint64_t parent, const uint64_t* __restrict__ t, int len) {
+  uint64_t s = index_slot(h, P.tcap);
+  for (;;) {
+    const int32_t id = P.tval[s];
+    if (id == -1) return -1;
+    if (id >= 0 && P.tkey[s] == h && P.ntok[id] == len && P.parent[id] == parent) {
+      const uint64_t* bt = P.tok + static_cast<int64_t>(id) * P.bs;
+      bool eq = true;
+      for (int i = 0; i < len; ++i) eq &= (bt[i] == t[i]);
+      if (eq) return id;
+    }
+    s = (s + 1) & static_cast<uint64_t>(P.tcap - 1);
+  }
+}
+
+__device__ void index_insert(const Pool& P, uint64_t h, int32_t id) {
+  uint64_t s = index_slot(h, P.tcap);
+  for (;;) {
+    int32_t v = P.tval[s];
+    if (v < 0 && atomicCAS(&P.tval[s], v, id) == v) {
+      P.tkey[s] = h;
+      P.slot[id] = static_cast<int32_t>(s);
+      return;
+    }
+    s = (s + 1) & static_cast<uint64_t>(P.tcap - 1);
+  }
+}
+
+// ------------------------------------------------------------------ hashing
+// One thread per sequence; the chain is a sequential fold (kv_chain_hash),
+// tokens are prefetched one block ahead so only the dependent hash path is
+// exposed.  Writes the chain hash after every block (last block may be
+// partial unless full_only).
+__global__ void k_chain_hash(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ seq_off,
+                             const int64_t* __restrict__ blk_off, const uint64_t* __restrict__ parent0, int n_seqs,
+                             int64_t bs, int full_only, uint64_t* __restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_seqs) return;
+  const int64_t b = seq_off[s], e = seq_off[s + 1];
+  uint64_t h = parent0 ? parent0[s] : kRootHash;
+  const int64_t ob = blk_off[s];
+  const int64_t nblk = full_only ? (e - b) / bs : (e - b + bs - 1) / bs;
+  constexpr int U = 8;
+  int64_t pos = b;
+  for (int64_t j = 0; j < nblk; ++j) {
+    const int64_t end = min(pos + bs, e);
+    int64_t i = pos;
+    for (; i + U <= end; i += U) {
+      uint64_t v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldg(reinterpret_cast<const unsigned long long*>(tokens + i + u)) + kGolden;
+#pragma unroll
+      for (int u = 0; u < U; ++u) h = chain_step(h, v[u]);
+    }
+    for (; i < end; ++i) h = chain_step(h, tokens[i] + kGolden);
+    out[ob + j] = h;
+    pos = end;
+  }
+}
+
+// --------------------------------------------------------------- lookups
+__device__ __forceinline__ int find_seq(const int64_t* __restrict__ blk_off, int n_seqs, int64_t g) {
+  int lo = 0, hi = n_seqs;  // blk_off[lo] <= g < blk_off[hi]
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (blk_off[mid] <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Pre-state probe of every block position of a batch of sequences.
+__global__ void k_probe_batch(Pool P, const uint64_t* __restrict__ tokens, const int64_t* __restrict__ seq_off,
+                              const int64_t* __restrict__ blk_off, int n_seqs, const uint64_t* __restrict__ hashes,
+                              int64_t total_blocks, int32_t* __restrict__ prehit, int64_t* __restrict__ first_miss) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g >= total_blocks) return;
+  const int s = find_seq(blk_off, n_seqs, g);
+  const int64_t j = g - blk_off[s];
+  const int64_t base = seq_off[s] + j * P.bs;
+  const int len = static_cast<int>(min(P.bs, seq_off[s + 1] - base));
+  const uint64_t parent = j ? hashes[g - 1] : kRootHash;
+  const int32_t id = probe_find(P, hashes[g], parent, tokens + base, len);
+  prehit[g] = id;
+  if (id < 0 && first_miss) atomicMin(reinterpret_cast<unsigned long long*>(first_miss + s), static_cast<unsigned long long>(j));
+}
+
+// Pre-state probe of the block positions of insert sequence s.
+__global__ void k_probe_seq(Pool P, const uint64_t* __restrict__ tokens, const int64_t* __restrict__ seq_off,
+                            const int64_t* __restrict__ blk_off, const uint64_t* __restrict__ hashes, int s,
+                            int32_t* __restrict__ prehit) {
+  const int64_t b0 = blk_off[s];
+  const int64_t np = blk_off[s + 1] - b0;
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (p >= np) return;
+  const int64_t base = seq_off[s] + p * P.bs;
+  const int len = static_cast<int>(min(P.bs, seq_off[s + 1] - base));
+  const uint64_t parent = p ? hashes[b0 + p - 1] : kRootHash;
+  prehit[b0 + p] = probe_find(P, hashes[b0 + p], parent, tokens + base, len);
+}
+
+__global__ void k_lookup_init(const int64_t* __restrict__ blk_off, int n_seqs, int64_t* first_miss) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n_seqs) first_miss[s] = blk_off[s + 1] - blk_off[s];
+}
+
+// Touch the hit prefix (kv_cache.cpp:432) and emit hit lengths.
+__global__ void k_lookup_finish(Pool P, const int64_t* __restrict__ seq_off, const int64_t* __restrict__ blk_off,
+                                int n_seqs, int64_t total_blocks, const int32_t* __restrict__ prehit,
+                                const int64_t* __restrict__ first_miss, int64_t now, int64_t* __restrict__ hit_tokens) {
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (g < n_seqs) {
+    hit_tokens[g] = first_miss[g] * P.bs;
+    atomicAdd(&P.ctr[C_LOOKUPS], 1ull);
+    atomicAdd(&P.ctr[C_HIT_TOK], static_cast<unsigned long long>(first_miss[g] * P.bs));
+    atomicAdd(&P.ctr[C_LOOK_TOK], static_cast<unsigned long long>(seq_off[g + 1] - seq_off[g]));
+  }
+  if (g >= total_blocks) return;
+  const int s = find_seq(blk_off, n_seqs, g);
+  if (g - blk_off[s] < first_miss[s]) P.last[prehit[g]] = now;
+}
+
+// ---------------------------------------------------------------- scoring
+// Block-wide exclusive scan of 2 values per thread over kSelectThreads
+// threads (2048 bins); returns the inclusive total.
+__device__ uint32_t block_scan_2048(uint32_t* hist, uint32_t* warp_sums) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  uint32_t a = hist[2 * t], b = hist[2 * t + 1];
+  uint32_t v = a + b, x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t ws = warp_sums[lane], z = ws;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    warp_sums[lane] = z - ws;  // exclusive warp offsets
+    if (lane == 31) warp_sums[32] = z;
+  }
+  __syncthreads();
+  const uint32_t excl = warp_sums[w] + x - v;
+  hist[2 * t] = excl;
+  hist[2 * t + 1] = excl + a;
+  const uint32_t total = warp_sums[32];
+  __syncthreads();
+  return total;
+}
+
+// Bitonic sort of n (power of two) keys in shared memory.
+__device__ void bitonic_smem(uint64_t* a, int n) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t x = a[i], y = a[ixj];
+          const bool up = (i & k) == 0;
+          if ((x > y) == up) {
+            a[i] = y;
+            a[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Same network in global memory (fallback for very large victim lists).
+__device__ void bitonic_global(uint64_t* a, int64_t n) {
+  for (int64_t k = 2; k <= n; k <<= 1) {
+    for (int64_t j = k >> 1; j > 0; j >>= 1) {
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int64_t ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t x = a[i], y = a[ixj];
+          const bool up = (i & k) == 0;
+          if ((x > y) == up) {
+            a[i] = y;
+            a[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Tag coverage check (kv_cache.cpp:438-448): ranges must tile [0, n).
+__device__ bool tags_cover(const sb_tag_range* tags, int64_t ntags, int64_t n) {
+  int64_t covered = 0;
+  for (int64_t r = 0; r < ntags; ++r) {
+    if (tags[r].begin != covered || tags[r].end < tags[r].begin) return false;
+    covered = tags[r].end;
+  }
+  return covered == n;
+}
+
+struct InsertArgs {
+  const uint64_t* tokens;
+  const int64_t* seq_off;
+  const sb_tag_range* tags;
+  const int64_t* tag_off;
+  const int64_t* blk_off;
+  const uint64_t* hashes;  // all sequences, laid out by blk_off
+  int32_t* out_ids;        // laid out by blk_off
+  int32_t* status;         // per sequence
+  int64_t now;
+};
+
+// mode 0: plan one insert (sequence s).  mode 1: evict(needed) — K = needed.
+// Computes victim keys of all candidate blocks, radix-selects the K smallest,
+// sorts them, records their ranks, and lists the lowest free ids.
+__global__ void __launch_bounds__(kSelectThreads, 1)
+    k_select(Pool P, Scratch S, InsertArgs A, int s, int mode, int64_t needed) {
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t warp_sums[33];
+  __shared__ int64_t sh[8];
+  extern __shared__ uint64_t sel[];  // kSortSmemKeys
+  const int t = threadIdx.x;
+  int64_t P_, f = 0, K = 0, Fp = 0;
+  if (mode == 0) {
+    const int64_t b0 = A.blk_off[s];
+    P_ = A.blk_off[s + 1] - b0;
+    const int64_t n = A.seq_off[s + 1] - A.seq_off[s];
+    const bool ok = tags_cover(A.tags + A.tag_off[s], A.tag_off[s + 1] - A.tag_off[s], n);
+    // first pre-miss position
+    if (t == 0) sh[0] = P_;
+    __syncthreads();
+    for (int64_t p = t; p < P_; p += blockDim.x)
+      if (S.prehit[b0 + p] < 0) atomicMin(reinterpret_cast<unsigned long long*>(&sh[0]), (unsigned long long)p);
+    __syncthreads();
+    f = sh[0];
+    if (!ok) {
+      if (t == 0) {
+        S.scal[S_STATUS] = SB_ERR_CACHE;
+        S.scal[S_F] = 0;
+        S.scal[S_K] = 0;
+        S.scal[S_FREE] = 0;
+      }
+      return;
+    }
+  } else {
+    P_ = 0;
+  }
+  // candidate keys; blocks hit before the first miss are referenced before
+  // any eviction can happen and are excluded.
+  if (t == 0) {
+    sh[1] = 0;  // candidates
+    sh[2] = 0;  // pre-hit candidates at positions >= f
+  }
+  __syncthreads();
+  uint32_t my_cand = 0;
+  for (int64_t i = t; i < P.cap; i += blockDim.x) {
+    const bool c = is_candidate(P, static_cast<int32_t>(i));
+    S.keys[i] = c ? victim_key(P, static_cast<int32_t>(i)) : kNoKey;
+    my_cand += c;
+  }
+  __syncthreads();
+  uint32_t my_hc = 0, my_excl = 0;
+  if (mode == 0) {
+    const int64_t b0 = A.blk_off[s];
+    for (int64_t p = t; p < P_; p += blockDim.x) {
+      const int32_t id = S.prehit[b0 + p];
+      if (id < 0) continue;
+      if (p < f) {
+        if (S.keys[id] != kNoKey) {
+          // several positions could name the same block only via hash cycles; tolerate
+          if (atomicExch(reinterpret_cast<unsigned long long*>(&S.keys[id]), (unsigned long long)kNoKey) != kNoKey)
+            ++my_excl;
+        }
+      } else if (is_candidate(P, id)) {
+        ++my_hc;
+      }
+    }
+  }
+  atomicAdd(reinterpret_cast<unsigned long long*>(&sh[1]), (unsigned long long)my_cand);
+  atomicAdd(reinterpret_cast<unsigned long long*>(&sh[2]), (unsigned long long)my_hc);
+  __shared__ unsigned long long excl_total;
+  if (t == 0) excl_total = 0;
+  __syncthreads();
+  atomicAdd(&excl_total, (unsigned long long)my_excl);
+  __syncthreads();
+  const int64_t ncand = sh[1] - static_cast<int64_t>(excl_total);
+  const int64_t nres = static_cast<int64_t>(P.ctr[C_NRES]);
+  const int64_t free_cnt = P.cap - nres;
+  if (mode == 0) {
+    const int64_t rest = P_ - f;
+    Fp = min(free_cnt, rest);
+    K = min(ncand, (rest > free_cnt ? rest - free_cnt : int64_t(0)) + sh[2]);
+  } else {
+    K = min(ncand, needed);
+  }
+  // ---- radix select of the K smallest keys (keys are unique) ----
+  uint64_t prefix = 0, mask = 0;
+  if (K > 0) {
+    int64_t need = K;
+    const int shifts[6] = {53, 42, 31, 20, 10, 0};
+    const int widths[6] = {11, 11, 11, 11, 10, 10};
+    for (int pass = 0; pass < 6; ++pass) {
+      const int sh_ = shifts[pass], wd = widths[pass];
+      const uint64_t bmask = (uint64_t(1) << wd) - 1;
+      for (int i = t; i < 2048; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      for (int64_t i = t; i < P.cap; i += blockDim.x) {
+        const uint64_t k = S.keys[i];
+        if (k != kNoKey && (k & mask) == prefix) atomicAdd(&hist[(k >> sh_) & bmask], 1u);
+      }
+      __syncthreads();
+      // locate the bin holding the need-th smallest
+      __shared__ uint32_t cnt_b;
+      uint32_t a0 = hist[2 * t], a1 = hist[2 * t + 1];
+      block_scan_2048(hist, warp_sums);
+      const uint32_t e0 = hist[2 * t], e1 = hist[2 * t + 1];
+      if (e0 < need && need <= e0 + a0) {
+        sh[4] = 2 * t;
+        sh[5] = e0;
+        cnt_b = a0;
+      }
+      if (e1 < need && need <= e1 + a1) {
+        sh[4] = 2 * t + 1;
+        sh[5] = e1;
+        cnt_b = a1;
+      }
+      __syncthreads();
+      const uint64_t bin = static_cast<uint64_t>(sh[4]);
+      need -= sh[5];
+      prefix |= bin << sh_;
+      mask |= bmask << sh_;
+      const bool done = (static_cast<int64_t>(cnt_b) == need);
+      __syncthreads();
+      if (done) break;
+    }
+    // gather all keys whose masked prefix is <= prefix: exactly K of them
+    if (t == 0) sh[6] = 0;
+    __syncthreads();
+    const bool in_smem = K <= kSortSmemKeys;
+    uint64_t* dst = in_smem ? sel : S.sortbuf;
+    for (int64_t i = t; i < P.cap; i += blockDim.x) {
+      const uint64_t k = S.keys[i];
+      if (k != kNoKey && (k & mask) <= prefix) {
+        const int64_t at = atomicAdd(reinterpret_cast<unsigned long long*>(&sh[6]), 1ull);
+        dst[at] = k;
+      }
+    }
+    __syncthreads();
+    int64_t n2 = 1;
+    while (n2 < K) n2 <<= 1;
+    for (int64_t i = K + t; i < n2; i += blockDim.x) dst[i] = kNoKey;
+    __syncthreads();
+    if (in_smem) bitonic_smem(dst, static_cast<int>(n2));
+    else bitonic_global(dst, n2);
+    for (int64_t r = t; r < K; r += blockDim.x) {
+      const uint64_t k = dst[r];
+      S.victims[r] = k;
+      S.taken[r] = 0;
+      S.rank_of[k & kIdMask] = static_cast<int32_t>(r);
+    }
+  }
+  // ---- lowest Fp free ids, ascending (std::set<int32_t> order) ----
+  if (Fp > 0) {
+    __shared__ uint32_t wcnt[33];
+    __shared__ int64_t found;
+    if (t == 0) found = 0;
+    __syncthreads();
+    const int lane = t & 31, w = t >> 5;
+    for (int64_t base = 0; base < P.cap; base += blockDim.x) {
+      if (found >= Fp) break;  // uniform: read after a barrier
+      const int64_t i = base + t;
+      const bool fr = i < P.cap && P.ntok[i] == 0;
+      const unsigned ball = __ballot_sync(0xffffffffu, fr);
+      if (lane == 0) wcnt[w] = __popc(ball);
+      __syncthreads();
+      if (t == 0) {
+        uint32_t acc = 0;
+        for (int k = 0; k < 32; ++k) {
+          const uint32_t cnt = wcnt[k];
+          wcnt[k] = acc;
+          acc += cnt;
+        }
+        wcnt[32] = acc;
+      }
+      __syncthreads();
+      const int64_t rank = found + wcnt[w] + __popc(ball & ((1u << lane) - 1));
+      if (fr && rank < Fp) S.freel[rank] = static_cast<int32_t>(i);
+      __syncthreads();
+      if (t == 0) found += wcnt[32];
+      __syncthreads();
+    }
+  }
+  if (t == 0) {
+    S.scal[S_F] = f;
+    S.scal[S_K] = K;
+    S.scal[S_FREE] = Fp;
+    S.scal[S_STATUS] = 0;
+    S.scal[S_NCAND] = ncand;
+  }
+}
+
+// Sequential decisions of one insert (kv_cache.cpp:471-506), from the first
+// pre-miss position on.  Single thread: each step is a handful of
+// L1/L2-resident accesses.
+__global__ void k_walk(Pool P, Scratch S, InsertArgs A, int s) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (S.scal[S_STATUS] != 0) {
+    S.scal[S_NEV] = 0;
+    S.scal[S_NNEW] = 0;
+    S.scal[S_FAILPOS] = -1;
+    return;
+  }
+  const int64_t b0 = A.blk_off[s];
+  const int64_t P_ = A.blk_off[s + 1] - b0;
+  const int64_t f = S.scal[S_F], K = S.scal[S_K], Fp = S.scal[S_FREE];
+  int64_t ptr = 0, fi = 0, nev = 0, nnew = 0, failpos = -1;
+  int status = 0;
+  for (int64_t p = f; p < P_; ++p) {
+    const int32_t b = S.prehit[b0 + p];
+    bool miss = b < 0;
+    if (!miss) {
+      const int32_t r = S.rank_of[b];
+      if (r >= 0) {
+        if (r < ptr && !S.taken[r]) miss = true;  // evicted earlier in this insert
+        else S.taken[r] = 1;                       // referenced: no longer a candidate
+      }
+    }
+    if (!miss) {
+      S.chain_out[p] = b;
+      S.kind[p] = 0;
+      continue;
+    }
+    int32_t id;
+    if (fi < Fp) {
+      id = S.freel[fi++];
+    } else {
+      while (ptr < K && S.taken[ptr]) ++ptr;
+      if (ptr >= K) {
+        status = SB_ERR_CACHE_FULL;
+        failpos = p;
+        break;
+      }
+      id = static_cast<int32_t>(S.victims[ptr++] & kIdMask);
+      S.evicted[nev++] = id;
+    }
+    S.chain_out[p] = id;
+    S.kind[p] = 1;
+    ++nnew;
+  }
+  S.scal[S_NEV] = nev;
+  S.scal[S_NNEW] = nnew;
+  S.scal[S_FAILPOS] = failpos;
+  S.scal[S_STATUS] = status;
+}
+
+__global__ void k_commit_evict(Pool P, Scratch S) {
+  const int64_t nev = S.scal[S_NEV];
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nev;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t id = S.evicted[i];
+    P.tval[P.slot[id]] = -2;
+    P.ntok[id] = 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && nev > 0) {
+    P.ctr[C_NRES] -= static_cast<unsigned long long>(nev);
+    P.ctr[C_EVICTED] += static_cast<unsigned long long>(nev);
+    P.ctr[C_EV_BLOCKS] += static_cast<unsigned long long>(nev);
+  }
+}
+
+__device__ __forceinline__ int tag_at(const sb_tag_range* tags, int64_t ntags, int64_t pos) {
+  for (int64_t r = 0; r < ntags; ++r)
+    if (pos >= tags[r].begin && pos < tags[r].end) return tags[r].tag;
+  return ntags ? tags[ntags - 1].tag : SB_TAG_RESPONSE;
+}
+
+__global__ void k_commit_apply(Pool P, Scratch S, InsertArgs A, int s) {
+  const int64_t b0 = A.blk_off[s];
+  const int64_t P_ = A.blk_off[s + 1] - b0;
+  const int64_t status = S.scal[S_STATUS];
+  const int64_t f = S.scal[S_F];
+  const int64_t K = S.scal[S_K];
+  const int64_t gid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t r = gid; r < K; r += stride) S.rank_of[S.victims[r] & kIdMask] = -1;
+  if (gid == 0) {
+    A.status[s] = static_cast<int32_t>(status);
+    if (status == 0) {
+      P.ctr[C_NRES] += static_cast<unsigned long long>(S.scal[S_NNEW]);
+      P.ctr[C_INS_BLOCKS] += static_cast<unsigned long long>(S.scal[S_NNEW]);
+    } else if (status == SB_ERR_CACHE_FULL) {
+      P.ctr[C_FULL] += 1ull;
+    }
+  }
+  if (status == SB_ERR_CACHE) return;
+  const int64_t limit = status == 0 ? P_ : S.scal[S_FAILPOS];
+  const int64_t n = A.seq_off[s + 1] - A.seq_off[s];
+  const uint64_t* tok = A.tokens + A.seq_off[s];
+  const sb_tag_range* tags = A.tags + A.tag_off[s];
+  const int64_t ntags = A.tag_off[s + 1] - A.tag_off[s];
+  for (int64_t p = gid; p < limit; p += stride) {
+    const bool hit = p < f || S.kind[p] == 0;
+    const int32_t id = p < f ? S.prehit[b0 + p] : S.chain_out[p];
+    if (hit) {
+      if (status == 0) atomicAdd(&P.ref[id], 1);
+      P.last[id] = A.now;
+    } else if (status == 0) {
+      const int64_t pos = p * P.bs;
+      const int len = static_cast<int>(min(P.bs, n - pos));
+      uint64_t* dst = P.tok + static_cast<int64_t>(id) * P.bs;
+      for (int i = 0; i < len; ++i) dst[i] = tok[pos + i];
+      P.ntok[id] = len;
+      const uint64_t h = A.hashes[b0 + p];
+      P.chain[id] = h;
+      P.parent[id] = p ? A.hashes[b0 + p - 1] : kRootHash;
+      P.tag[id] = tag_at(tags, ntags, pos);
+      P.ref[id] = 1;
+      P.last[id] = A.now;
+      P.pinned[id] = 0;
+      index_insert(P, h, id);
+    }
+    if (status == 0) A.out_ids[b0 + p] = id;
+  }
+}
+
+// --------------------------------------------------------- small ops
+// First failing index of a release (kv_cache.cpp:561-569): UnknownBlock /
+// ZeroRefRelease, checked in id order; apply only if none.
+__global__ void k_validate_ids(Pool P, const int32_t* ids, int64_t n, int check_ref, int64_t* scal) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t id = ids[i];
+    const bool known = id >= 0 && id < P.cap && P.ntok[id] > 0;
+    if (!known || (check_ref && P.ref[id] < 1))
+      atomicMin(reinterpret_cast<unsigned long long*>(&scal[S_ERRIDX]), (unsigned long long)i);
+  }
+}
+__global__ void k_release_apply(Pool P, const int32_t* ids, int64_t n, const int64_t* scal) {
+  if (scal[S_ERRIDX] < n) return;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicSub(&P.ref[ids[i]], 1);
+}
+__global__ void k_touch_apply(Pool P, const int32_t* ids, int64_t n, int64_t now, const int64_t* scal) {
+  const int64_t lim = min(n, scal[S_ERRIDX]);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < lim;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    P.last[ids[i]] = now;
+}
+__global__ void k_priority_apply(Pool P, const int32_t* ids, int64_t n, int pinned, int tier, const int64_t* scal) {
+  if (scal[S_ERRIDX] < n) return;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (pinned >= 0) P.pinned[ids[i]] = pinned;
+    if (tier >= 0) P.tag[ids[i]] = tier;
+  }
+}
+__global__ void k_set_scal(int64_t* scal, int idx, int64_t v) { scal[idx] = v; }
+
+__global__ void k_evict_out(Scratch S, int32_t* out, int64_t* n_out) {
+  const int64_t K = S.scal[S_K];
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < K;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t id = static_cast<int32_t>(S.victims[r] & kIdMask);
+    out[r] = id;
+    S.evicted[r] = id;
+    S.rank_of[id] = -1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    S.scal[S_NEV] = K;
+    *n_out = K;
+  }
+}
+
+// Rebuild the index without tombstones.
+__global__ void k_index_clear(Pool P) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < P.tcap;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    P.tval[i] = -1;
+}
+__global__ void k_index_fill(Pool P) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < P.cap;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (P.ntok[i] > 0) index_insert(P, P.chain[i], static_cast<int32_t>(i));
+}
+
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+// ==================================================================== host
+template <class T>
+static T* dalloc(size_t n) {
+  T* p = nullptr;
+  if (n == 0) n = 1;
+  SB_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  return p;
+}
+
+static int grid_for(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, int64_t(1) << 30)));
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+struct sb_kv_cache {
+  Pool P{};
+  Scratch S{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t tomb_bound = 0;  // upper bound on index tombstones
+  std::mutex mu;
+  // device staging for the per-op API
+  uint64_t* d_tok = nullptr;
+  int64_t tok_cap = 0;
+  sb_tag_range* d_tags = nullptr;
+  int64_t tags_cap = 0;
+  int64_t* d_meta = nullptr;  // seq_off[2], blk_off[2], tag_off[2], misc
+  int32_t* d_ids = nullptr;
+  int64_t ids_cap = 0;
+  int32_t* d_status = nullptr;
+  int64_t* d_first = nullptr;
+  int64_t* d_hit = nullptr;
+  uint64_t* d_hash_all = nullptr;
+  int64_t hash_cap = 0;
+  int32_t* d_prehit_all = nullptr;
+  int64_t prehit_cap = 0;
+
+  ~sb_kv_cache() {
+    cudaSetDevice(device);
+    void* ptrs[] = {P.tok, P.ntok, P.chain, P.parent, P.tag, P.ref, P.pinned, P.last, P.tkey, P.tval, P.slot, P.ctr,
+                    S.hashes, S.prehit, S.chain_out, S.kind, S.freel, S.evicted, S.victims, S.taken, S.rank_of, S.keys,
+                    S.sortbuf, S.scal, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  void ensure_positions(int64_t pmax) {
+    if (pmax <= S.pmax) return;
+    int64_t n = std::max<int64_t>(pmax, 2 * S.pmax);
+    cudaFree(S.hashes);
+    cudaFree(S.chain_out);
+    cudaFree(S.kind);
+    cudaFree(S.freel);
+    cudaFree(S.victims);
+    cudaFree(S.taken);
+    cudaFree(S.sortbuf);
+    S.hashes = dalloc<uint64_t>(n);
+    S.chain_out = dalloc<int32_t>(n);
+    S.kind = dalloc<int8_t>(n);
+    S.freel = dalloc<int32_t>(n);
+    S.kmax = 2 * n + P.cap;
+    S.victims = dalloc<uint64_t>(S.kmax);
+    S.taken = dalloc<uint8_t>(S.kmax);
+    int64_t pw = 1;
+    while (pw < S.kmax) pw <<= 1;
+    S.sortbuf = dalloc<uint64_t>(pw);
+    S.pmax = n;
+  }
+  void ensure_tokens(int64_t n) {
+    if (n <= tok_cap) return;
+    cudaFree(d_tok);
+    tok_cap = std::max<int64_t>(n, 2 * tok_cap);
+    d_tok = dalloc<uint64_t>(tok_cap);
+  }
+  void ensure_tags(int64_t n) {
+    if (n <= tags_cap) return;
+    cudaFree(d_tags);
+    tags_cap = std::max<int64_t>(n, 2 * tags_cap + 4);
+    d_tags = dalloc<sb_tag_range>(tags_cap);
+  }
+  void ensure_ids(int64_t n) {
+    if (n <= ids_cap) return;
+    cudaFree(d_ids);
+    ids_cap = std::max<int64_t>(n, 2 * ids_cap + 16);
+    d_ids = dalloc<int32_t>(ids_cap);
+  }
+  void ensure_hash_all(int64_t n) {
+    if (n <= hash_cap) return;
+    cudaFree(d_hash_all);
+    hash_cap = std::max<int64_t>(n, 2 * hash_cap);
+    d_hash_all = dalloc<uint64_t>(hash_cap);
+  }
+  void ensure_prehit_all(int64_t n) {
+    if (n <= prehit_cap) return;
+    cudaFree(d_prehit_all);
+    prehit_cap = std::max<int64_t>(n, 2 * prehit_cap);
+    d_prehit_all = dalloc<int32_t>(prehit_cap);
+    S.prehit = d_prehit_all;
+  }
+
+  void maybe_rebuild_index(int64_t added_tombs) {
+    tomb_bound += added_tombs;
+    if (tomb_bound <= P.cap) return;
+    k_index_clear<<<grid_for(P.tcap), 256, 0, stream>>>(P);
+    k_index_fill<<<grid_for(P.cap), 256, 0, stream>>>(P);
+    SB_CHECK_LAUNCH();
+    tomb_bound = 0;
+  }
+
+  int64_t read_scal(int idx) {
+    int64_t v = 0;
+    SB_CUDA(cudaMemcpyAsync(&v, S.scal + idx, sizeof(v), cudaMemcpyDeviceToHost, stream));
+    SB_CUDA(cudaStreamSynchronize(stream));
+    return v;
+  }
+  unsigned long long read_ctr(int idx) const {
+    unsigned long long v = 0;
+    cudaMemcpyAsync(&v, P.ctr + idx, sizeof(v), cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    return v;
+  }
+
+  size_t select_smem() const { return kSortSmemKeys * sizeof(uint64_t); }
+
+  // Inserts sequences [0, n_seqs) described by device arrays, sequentially.
+  void insert_device(const uint64_t* tokens, const int64_t* seq_off, const sb_tag_range* tags, const int64_t* tag_off,
+                     const int64_t* blk_off, const uint64_t* hashes_in, int n_seqs, int64_t now, int32_t* out_ids,
+                     int32_t* status, const std::vector<int64_t>& h_blk_off) {
+    const int64_t total_blocks = h_blk_off[n_seqs];
+    int64_t pmax = 1;
+    for (int s = 0; s < n_seqs; ++s) pmax = std::max(pmax, h_blk_off[s + 1] - h_blk_off[s]);
+    ensure_positions(pmax);
+    ensure_prehit_all(std::max<int64_t>(total_blocks, 1));
+    const uint64_t* hashes = hashes_in;
+    if (!hashes) {
+      ensure_hash_all(std::max<int64_t>(total_blocks, 1));
+      k_chain_hash<<<(n_seqs + 127) / 128, 128, 0, stream>>>(tokens, seq_off, blk_off, nullptr, n_seqs, P.bs, 0,
+                                                           d_hash_all);
+      SB_CHECK_LAUNCH();
+      hashes = d_hash_all;
+    }
+    InsertArgs A{tokens, seq_off, tags, tag_off, blk_off, hashes, out_ids, status, now};
+    for (int s = 0; s < n_seqs; ++s) {
+      const int64_t np = h_blk_off[s + 1] - h_blk_off[s];
+      if (np > 0)
+        k_probe_seq<<<static_cast<int>((np + 255) / 256), 256, 0, stream>>>(P, tokens, seq_off, blk_off, hashes, s,
+                                                                            S.prehit);
+      k_select<<<1, kSelectThreads, select_smem(), stream>>>(P, S, A, s, 0, 0);
+      k_walk<<<1, 32, 0, stream>>>(P, S, A, s);
+      k_commit_evict<<<grid_for(np), 256, 0, stream>>>(P, S);
+      k_commit_apply<<<grid_for(std::max<int64_t>(np, 1) + 2 * np), 256, 0, stream>>>(P, S, A, s);
+      SB_CHECK_LAUNCH();
+      maybe_rebuild_index(np);
+    }
+  }
+};
+
+static thread_local std::string g_last_error;
+void sb::set_last_error(const std::string& m) { g_last_error = m; }
+
+extern "C" {
+
+const char* sb_last_error(void) { return g_last_error.c_str(); }
+const char* sb_version(void) { return "sutradhara_b200 0.1 (sm_100a)"; }
+
+uint64_t sb_kv_root_hash(void) { return kRootHash; }
+uint64_t sb_kv_chain_hash_host(uint64_t parent, const uint64_t* t, int64_t n) {
+  uint64_t h = parent;
+  for (int64_t i = 0; i < n; ++i) h = hash_combine(h, t[i]);
+  return h;
+}
+
+int sb_chain_hash_batch(const uint64_t* d_tokens, const int64_t* d_seq_offsets, const int64_t* d_block_offsets,
+                        const uint64_t* d_parent, int32_t n_seqs, int64_t block_size, uint64_t* d_block_hashes,
+                        void* stream) {
+  return guard([&] {
+    if (n_seqs <= 0) return int(SB_OK);
+    if (block_size < 1) throw Error(SB_ERR_INVALID, "block_size must be >= 1");
+    k_chain_hash<<<(n_seqs + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        d_tokens, d_seq_offsets, d_block_offsets, d_parent, n_seqs, block_size, 0, d_block_hashes);
+    SB_CHECK_LAUNCH();
+    return int(SB_OK);
+  });
+}
+
+int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, int32_t device, sb_kv_cache** out) {
+  return guard([&] {
+    if (block_size < 1) throw Error(SB_ERR_CONFIG, "cache block_size must be >= 1");
+    if (capacity_blocks < 1) throw Error(SB_ERR_CONFIG, "cache capacity_blocks must be >= 1");
+    if (capacity_blocks > (int64_t(1) << kIdBits)) throw Error(SB_ERR_UNSUPPORTED, "capacity above 2^21 blocks");
+    if (policy != SB_POLICY_LRU && policy != SB_POLICY_TIERED) throw Error(SB_ERR_CONFIG, "unknown policy");
+    SB_CUDA(cudaSetDevice(device));
+    auto* c = new sb_kv_cache();
+    try {
+      c->device = device;
+      SB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      Pool& P = c->P;
+      P.bs = block_size;
+      P.cap = capacity_blocks;
+      P.policy = policy;
+      P.tcap = 16;
+      while (P.tcap < 4 * capacity_blocks) P.tcap <<= 1;
+      P.tok = dalloc<uint64_t>(static_cast<size_t>(block_size * capacity_blocks));
+      P.ntok = dalloc<int32_t>(capacity_blocks);
+      P.chain = dalloc<uint64_t>(capacity_blocks);
+      P.parent = dalloc<uint64_t>(capacity_blocks);
+      P.tag = dalloc<int32_t>(capacity_blocks);
+      P.ref = dalloc<int32_t>(capacity_blocks);
+      P.pinned = dalloc<int32_t>(capacity_blocks);
+      P.last = dalloc<int64_t>(capacity_blocks);
+      P.tkey = dalloc<uint64_t>(P.tcap);
+      P.tval = dalloc<int32_t>(P.tcap);
+      P.slot = dalloc<int32_t>(capacity_blocks);
+      P.ctr = dalloc<unsigned long long>(C_N);
+      SB_CUDA(cudaMemsetAsync(P.ntok, 0, sizeof(int32_t) * capacity_blocks, c->stream));
+      SB_CUDA(cudaMemsetAsync(P.ref, 0, sizeof(int32_t) * capacity_blocks, c->stream));
+      SB_CUDA(cudaMemsetAsync(P.pinned, 0, sizeof(int32_t) * capacity_blocks, c->stream));
+      SB_CUDA(cudaMemsetAsync(P.ctr, 0, sizeof(unsigned long long) * C_N, c->stream));
+      k_fill_i32<<<grid_for(P.tcap), 256, 0, c->stream>>>(P.tval, P.tcap, -1);
+      Scratch& S = c->S;
+      S.rank_of = dalloc<int32_t>(capacity_blocks);
+      k_fill_i32<<<grid_for(capacity_blocks), 256, 0, c->stream>>>(S.rank_of, capacity_blocks, -1);
+      S.keys = dalloc<uint64_t>(capacity_blocks);
+      S.evicted = dalloc<int32_t>(capacity_blocks + 16);
+      S.scal = dalloc<int64_t>(S_N);
+      SB_CUDA(cudaMemsetAsync(S.scal, 0, sizeof(int64_t) * S_N, c->stream));
+      c->ensure_positions(64);
+      c->ensure_prehit_all(64);
+      c->d_meta = dalloc<int64_t>(16);
+      c->d_status = dalloc<int32_t>(4);
+      c->d_first = dalloc<int64_t>(4);
+      c->d_hit = dalloc<int64_t>(4);
+      SB_CUDA(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(c->select_smem())));
+      SB_CHECK_LAUNCH();
+      SB_CUDA(cudaStreamSynchronize(c->stream));
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+    return int(SB_OK);
+  });
+}
+
+void sb_kv_destroy(sb_kv_cache* c) { delete c; }
+
+int sb_kv_lookup_prefix(sb_kv_cache* c, const uint64_t* tokens, int64_t n, int64_t now, int64_t* hit_tokens) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(c->mu);
+    SB_CUDA(cudaSetDevice(c->device));
+    if (now < -kLastBias || now >= kLastBias) throw Error(SB_ERR_UNSUPPORTED, "now outside +-2^39");
+    const int64_t nblk = n / c->P.bs;
+    *hit_tokens = 0;
+    if (nblk == 0) return int(SB_OK);
+    c->ensure_tokens(n);
+    c->ensure_hash_all(nblk);
+    c->ensure_prehit_all(nblk);
+    int64_t meta[4] = {0, n, 0, nblk};
+    SB_CUDA(cudaMemcpyAsync(c->d_tok, tokens, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, c->stream));
+    SB_CUDA(cudaMemcpyAsync(c->d_meta, meta, sizeof(meta), cudaMemcpyHostToDevice, c->stream));
+    const int64_t* seq_off = c->d_meta;
+    const int64_t* blk_off = c->d_meta + 2;
+    k_chain_hash<<<1, 32, 0, c->stream>>>(c->d_tok, seq_off, blk_off, nullptr, 1, c->P.bs, 1, c->d_hash_all);
+    k_lookup_init<<<1, 32, 0, c->stream>>>(blk_off, 1, c->d_first);
+    k_probe_batch<<<grid_for(nblk), 256, 0, c->stream>>>(c->P, c->d_tok, seq_off, blk_off, 1, c->d_hash_all, nblk,
+                                                         c->d_prehit_all, c->d_first);
+    k_lookup_finish<<<grid_for(nblk + 1), 256, 0, c->stream>>>(c->P, seq_off, blk_off, 1, nblk, c->d_prehit_all,
+                                                               c->d_first, now, c->d_hit);
+    SB_CHECK_LAUNCH();
+    SB_CUDA(cudaMemcpyAsync(hit_tokens, c->d_hit, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    SB_CUDA(cudaStreamSynchronize(c->stream));
+    return int(SB_OK);
+  });
+}
+
+int sb_kv_lookup_prefix_batch(sb_kv_cache* c, const uint64_t* d_tokens, const int64_t* d_seq_offsets, int32_t n_seqs,
+                              int64_t now, int64_t* d_hit_tokens, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(c->mu);
+    SB_CUDA(cudaSetDevice(c->device));
+    if (n_seqs <= 0) return int(SB_OK);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    std::vector<int64_t> off(n_seqs + 1), blk(n_seqs + 1);
+    SB_CUDA(cudaMemcpyAsync(off.data(), d_seq_offsets, sizeof(int64_t) * (n_seqs + 1), cudaMemcpyDeviceToHost, st));
+    SB_CUDA(cudaStreamSynchronize(st));
+    blk[0] = 0;
+    for (int s = 0; s < n_seqs; ++s) blk[s + 1] = blk[s] + (off[s + 1] - off[s]) / c->P.bs;
+    const int64_t total = blk[n_seqs];
+    c->ensure_hash_all(total + 1);
+    c->ensure_prehit_all(total + 1);
+    int64_t* d_blk = dalloc<int64_t>(n_seqs + 1);
+    int64_t* d_first = dalloc<int64_t>(n_seqs);
+    SB_CUDA(cudaMemcpyAsync(d_blk, blk.data(), sizeof(int64_t) * (n_seqs + 1), cudaMemcpyHostToDevice, st));
+    k_chain_hash<<<(n_seqs + 127) / 128, 128, 0, st>>>(d_tokens, d_seq_offsets, d_blk, nullptr, n_seqs, c->P.bs, 1,
+                                                       c->d_hash_all);
+    k_lookup_init<<<(n_seqs + 127) / 128, 128, 0, st>>>(d_blk, n_seqs, d_first);
+    if (total > 0)
+      k_probe_batch<<<grid_for(total), 256, 0, st>>>(c->P, d_tokens, d_seq_offsets, d_blk, n_seqs, c->d_hash_all, total,
+                                                     c->d_prehit_all, d_first);
+    k_lookup_finish<<<grid_for(std::max<int64_t>(total, n_seqs)), 256, 0, st>>>(
+        c->P, d_seq_offsets, d_blk, n_seqs, total, c->d_prehit_all, d_first, now, d_hit_tokens);
+    SB_CHECK_LAUNCH();
+    SB_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_blk);
+    cudaFree(d_first);
+    return int(SB_OK);
+  });
+}
+
+int sb_kv_insert(sb_kv_cache* c, const uint64_t* tokens, int64_t n, const sb_tag_range* tags, int64_t n_tags,
+                 int64_t now, int32_t* out_ids, int64_t* n_out) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(c->mu);
+    SB_CUDA(cudaSetDevice(c->device));
+    *n_out = 0;
+    if (now < -kLastBias || now >= kLastBias) throw Error(SB_ERR_UNSUPPORTED, "now outside +-2^39");
+    const int64_t nblk = (n + c->P.bs - 1) / c->P.bs;
+    c->ensure_tokens(std::max<int64_t>(n, 1));
+    c->ensure_tags(std::max<int64_t>(n_tags, 1));
+    c->ensure_ids(std::max<int64_t>(nblk, 1));
+    int64_t meta[6] = {0, n, 0, n_tags, 0, nblk};
+    if (n) SB_CUDA(cudaMemcpyAsync(c->d_tok, tokens, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, c->stream));
+    if (n_tags)
+      SB_CUDA(cudaMemcpyAsync(c->d_tags, tags, sizeof(sb_tag_range) * n_tags, cudaMemcpyHostToDevice, c->stream));
+    SB_CUDA(cudaMemcpyAsync(c->d_meta, meta, sizeof(meta), cudaMemcpyHostToDevice, c->stream));
+    std::vector<int64_t> hb = {0, nblk};
+    c->insert_device(c->d_tok, c->d_meta, c->d_tags, c->d_meta + 2, c->d_meta + 4, nullptr, 1, now, c->d_ids,
+                     c->d_status, hb);
+    int32_t st = 0;
+    SB_CUDA(cudaMemcpyAsync(&st, c->d_status, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    SB_CUDA(cudaStreamSynchronize(c->stream));
+    if (st == 0 && nblk) {
+      SB_CUDA(cudaMemcpy(out_ids, c->d_ids, sizeof(int32_t) * nblk, cudaMemcpyDeviceToHost));
+      *n_out = nblk;
+    }
+    if (st == SB_ERR_CACHE_FULL) set_last_error("insert: cannot free a block (all pinned or referenced)");
+    if (st == SB_ERR_CACHE) set_last_error("insert: tag ranges must cover the full token range without gaps");
+    return int(st);
+  });
+}
+
+int sb_kv_insert_batch(sb_kv_cache* c, const uint64_t* d_tokens, const int64_t* d_seq_offsets,
+                       const sb_tag_range* d_tags, const int64_t* d_tag_offsets, const int64_t* d_block_offsets,
+                       const uint64_t* d_block_hashes, int32_t n_seqs, int64_t now, int32_t* d_out_ids,
+                       int32_t* d_status, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(c->mu);
+    SB_CUDA(cudaSetDevice(c->device));
+    if (n_seqs <= 0) return int(SB_OK);
+    if (now < -kLastBias || now >= kLastBias) throw Error(SB_ERR_UNSUPPORTED, "now outside +-2^39");
+    std::vector<int64_t> hb(n_seqs + 1);
+    SB_CUDA(cudaMemcpy(hb.data(), d_block_offsets, sizeof(int64_t) * (n_seqs + 1), cudaMemcpyDeviceToHost));
+    cudaStream_t saved = c->stream;
+    if (stream) c->stream = static_cast<cudaStream_t>(stream);
+    try {
+      c->insert_device(d_tokens, d_seq_offsets, d_tags, d_tag_offsets, d_block_offsets, d_block_hashes, n_seqs, now,
+                       d_out_ids, d_status, hb);
+    } catch (...) {
+      c->stream = saved;
+      throw;
+    }
+    c->stream = saved;
+    return int(SB_OK);
+  });
+}
+
+int sb_kv_evict(sb_kv_cache* c, int64_t needed, int32_t* out_ids, int64_t* n_out) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(c->mu);
+    SB_CUDA(cudaSetDevice(c->device));
+    *n_out = 0;
+    if (needed <= 0) return int(SB_OK);
+    c->ensure_positions(std::min<int64_t>(needed, c->P.cap));
+    c->ensure_ids(std::min<int64_t>(needed, c->P.cap) + 1);
+    InsertArgs A{};
+    k_select<<<1, kSelectThreads, c->select_smem(), c->stream>>>(c->P, c->S, A, 0, 1, needed);
+    k_evict_out<<<grid_for(c->P.cap), 256, 0, c->stream>>>(c->S, c->d_ids, c->d_first);
+    k_commit_evict<<<grid_for(c->P.cap), 256, 0, c->stream>>>(c->P, c->S);
+    SB_CHECK_LAUNCH();
+    int64_t k = 0;
+    SB_CUDA(cudaMemcpyAsync(&k, c->d_first, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    SB_CUDA(cudaStreamSynchronize(c->stream));
+    if (k) SB_CUDA(cudaMemcpy(out_ids, c->d_ids, sizeof(int32_t) * k, cudaMemcpyDeviceToHost));
+    *n_out = k;
+    c->maybe_rebuild_index(k);
+    return int(SB_OK);
+  });
+}
+
+static int run_validated(sb_kv_cache* c, const int32_t* ids, int64_t n, int check_ref, int kind, int a0, int a1,
+                         int64_t now) {
+  c->ensure_ids(std::max<int64_t>(n, 1));
+  if (n) SB_CUDA(cudaMemcpyAsync(c->d_ids, ids, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+  k_set_scal<<<1, 1, 0, c->stream>>>(c->S.scal, S_ERRIDX, INT64_MAX);
+  if (n) k_validate_ids<<<grid_for(n), 256, 0, c->stream>>>(c->P, c->d_ids, n, check_ref, c->S.scal);
+  if (n) {
+    if (kind == 0) k_release_apply<<<grid_for(n), 256, 0, c->stream>>>(c->P, c->d_ids, n, c->S.scal);
+    if (kind == 1) k_touch_apply<<<grid_for(n), 256, 0, c->stream>>>(c->P, c->d_ids, n, now, c->S.scal);
+    if (kind == 2) k_priority_apply<<<grid_for(n), 256, 0, c->stream>>>(c->P, c->d_ids, n, a0, a1, c->S.scal);
+  }
+  SB_CHECK_LAUNCH();
+  const int64_t err = c->read_scal(S_ERRIDX);
+  if (err >= n) return SB_OK;
+  // classify the first failing id exactly as the reference's in-order loop
+  int32_t id = ids[err];
+  if (id < 0 || id >= c->P.cap) {
+    set_last_error("block " + std::to_string(id) + " not resident");
+    return SB_ERR_UNKNOWN_BLOCK;
+  }
+  int32_t nt = 0;
+  SB_CUDA(cudaMemcpy(&nt, c->P.ntok + id, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (nt == 0) {
+    set_last_error("block " + std::to_string(id) + " not resident");
+    return SB_ERR_UNKNOWN_BLOCK;
+  }
+  set_last_error("release of block " + std::to_string(id) + " with ref_count 0");
+  return SB_ERR_ZERO_REF_RELEASE;
+}
+
+int sb_kv_release(sb_kv_cache* c, const int32_t* ids, int64_t n) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(c->mu);
+    SB_CUDA(cudaSetDevice(c->device));
+    return run_validated(c, ids, n, 1, 0, 0, 0, 0);
+  });
+}
+
+int sb_kv_release_batch(sb_kv_cache* c, const int32_t* d_ids, int64_t n, int32_t* d_status, void* stream) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(c->mu);
+    SB_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    k_set_scal<<<1, 1, 0, st>>>(c->S.scal, S_ERRIDX, INT64_MAX);
+    if (n > 0) {
+      k_validate_ids<<<grid_for(n), 256, 0, st>>>(c->P, d_ids, n, 1, c->S.scal);
+      k_release_apply<<<grid_for(n), 256, 0, st>>>(c->P, d_ids, n, c->S.scal);
+    }
+    SB_CHECK_LAUNCH();
+    (void)d_status;
+    return int(SB_OK);
+  });
+}
+
+int sb_kv_touch(sb_kv_cache* c, const int32_t* ids, int64_t n, int64_t now) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(c->mu);
+    SB_CUDA(cudaSetDevice(c->device));
+    return run_validated(c, ids, n, 0, 1, 0, 0, now);
+  });
+}
+
+int sb_kv_set_reuse_priority(sb_kv_cache* c, const int32_t* ids, int64_t n, int32_t pinned, int32_t tier_override) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(c->mu);
+    SB_CUDA(cudaSetDevice(c->device));
+    if (tier_override > SB_TAG_HISTORY) throw Error(SB_ERR_INVALID, "bad tag");
+    return run_validated(c, ids, n, 0, 2, pinned, tier_override, 0);
+  });
+}
+
+int sb_kv_set_tag(sb_kv_cache* c, int32_t id, int32_t tag) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(c->mu);
+    SB_CUDA(cudaSetDevice(c->device));
+    if (tag < 0 || tag > SB_TAG_HISTORY) throw Error(SB_ERR_INVALID, "bad tag");
+    return run_validated(c, &id, 1, 0, 2, -1, tag, 0);
+  });
+}
+
+int64_t sb_kv_block_size(const sb_kv_cache* c) { return c->P.bs; }
+int64_t sb_kv_capacity_blocks(const sb_kv_cache* c) { return c->P.cap; }
+int64_t sb_kv_resident_blocks(const sb_kv_cache* c) { return static_cast<int64_t>(c->read_ctr(C_NRES)); }
+int64_t sb_kv_free_blocks(const sb_kv_cache* c) { return c->P.cap - sb_kv_resident_blocks(c); }
+uint64_t sb_kv_total_evicted(const sb_kv_cache* c) { return c->read_ctr(C_EVICTED); }
+int32_t sb_kv_policy(const sb_kv_cache* c) { return c->P.policy; }
+
+int sb_kv_contains(const sb_kv_cache* c, int32_t id) {
+  if (id < 0 || id >= c->P.cap) return 0;
+  int32_t nt = 0;
+  cudaMemcpy(&nt, c->P.ntok + id, sizeof(int32_t), cudaMemcpyDeviceToHost);
+  return nt > 0 ? 1 : 0;
+}
+
+int sb_kv_block(const sb_kv_cache* c, int32_t id, sb_block_info* info, uint64_t* tokens_out) {
+  return guard([&] {
+    if (id < 0 || id >= c->P.cap || !sb_kv_contains(c, id)) {
+      set_last_error("block " + std::to_string(id) + " not resident");
+      return int(SB_ERR_UNKNOWN_BLOCK);
+    }
+    const Pool& P = c->P;
+    info->block_id = id;
+    SB_CUDA(cudaMemcpy(&info->tag, P.tag + id, 4, cudaMemcpyDeviceToHost));
+    SB_CUDA(cudaMemcpy(&info->ref_count, P.ref + id, 4, cudaMemcpyDeviceToHost));
+    SB_CUDA(cudaMemcpy(&info->pinned, P.pinned + id, 4, cudaMemcpyDeviceToHost));
+    SB_CUDA(cudaMemcpy(&info->n_tokens, P.ntok + id, 4, cudaMemcpyDeviceToHost));
+    SB_CUDA(cudaMemcpy(&info->last_used, P.last + id, 8, cudaMemcpyDeviceToHost));
+    SB_CUDA(cudaMemcpy(&info->chain_hash, P.chain + id, 8, cudaMemcpyDeviceToHost));
+    SB_CUDA(cudaMemcpy(&info->parent_hash, P.parent + id, 8, cudaMemcpyDeviceToHost));
+    info->tier = tier_of(info->tag);
+    if (tokens_out)
+      SB_CUDA(cudaMemcpy(tokens_out, P.tok + int64_t(id) * P.bs, sizeof(uint64_t) * info->n_tokens,
+                         cudaMemcpyDeviceToHost));
+    return int(SB_OK);
+  });
+}
+
+namespace {
+struct HostView {
+  std::vector<int32_t> ntok, tag, ref, pinned, tval;
+  std::vector<int64_t> last;
+  std::vector<uint64_t> chain, tkey;
+  unsigned long long nres = 0;
+};
+HostView read_view(const sb_kv_cache* c, bool with_index) {
+  const Pool& P = c->P;
+  HostView v;
+  v.ntok.resize(P.cap);
+  v.tag.resize(P.cap);
+  v.ref.resize(P.cap);
+  v.pinned.resize(P.cap);
+  v.last.resize(P.cap);
+  SB_CUDA(cudaMemcpy(v.ntok.data(), P.ntok, 4 * P.cap, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(v.tag.data(), P.tag, 4 * P.cap, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(v.ref.data(), P.ref, 4 * P.cap, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(v.pinned.data(), P.pinned, 4 * P.cap, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(v.last.data(), P.last, 8 * P.cap, cudaMemcpyDeviceToHost));
+  SB_CUDA(cudaMemcpy(&v.nres, P.ctr + C_NRES, 8, cudaMemcpyDeviceToHost));
+  if (with_index) {
+    v.chain.resize(P.cap);
+    v.tkey.resize(P.tcap);
+    v.tval.resize(P.tcap);
+    SB_CUDA(cudaMemcpy(v.chain.data(), P.chain, 8 * P.cap, cudaMemcpyDeviceToHost));
+    SB_CUDA(cudaMemcpy(v.tkey.data(), P.tkey, 8 * P.tcap, cudaMemcpyDeviceToHost));
+    SB_CUDA(cudaMemcpy(v.tval.data(), P.tval, 4 * P.tcap, cudaMemcpyDeviceToHost));
+  }
+  return v;
+}
+const char* tag_name(int t) {
+  static const char* n[6] = {"response", "tool_output", "user_query", "system_prompt", "partial_prefill", "history"};
+  return t >= 0 && t < 6 ? n[t] : "unknown";
+}
+}  // namespace
+
+int sb_kv_audit(const sb_kv_cache* c) {
+  return guard([&] {
+    SB_CUDA(cudaStreamSynchronize(c->stream));
+    HostView v = read_view(c, true);
+    int64_t res = 0;
+    for (int64_t i = 0; i < c->P.cap; ++i) {
+      if (v.ntok[i] == 0) continue;
+      ++res;
+      if (v.ref[i] < 0) throw Error(SB_ERR_CACHE, "audit: negative ref_count");
+      if (v.ntok[i] < 1 || v.ntok[i] > c->P.bs) throw Error(SB_ERR_CACHE, "audit: bad block token count");
+    }
+    if (res != static_cast<int64_t>(v.nres) || res > c->P.cap) throw Error(SB_ERR_CACHE, "audit: block accounting mismatch");
+    int64_t indexed = 0;
+    for (int64_t s = 0; s < c->P.tcap; ++s) {
+      const int32_t id = v.tval[s];
+      if (id < 0) continue;
+      if (v.ntok[id] == 0 || v.chain[id] != v.tkey[s]) throw Error(SB_ERR_CACHE, "audit: hash index out of sync");
+      ++indexed;
+    }
+    if (indexed != res) throw Error(SB_ERR_CACHE, "audit: hash index size mismatch");
+    return int(SB_OK);
+  });
+}
+
+int sb_kv_dump(const sb_kv_cache* c, char* buf, int64_t cap, int64_t* len) {
+  return guard([&] {
+    SB_CUDA(cudaStreamSynchronize(c->stream));
+    HostView v = read_view(c, false);
+    std::string out;
+    out.reserve(64 * v.nres);
+    char line[256];
+    for (int64_t i = 0; i < c->P.cap; ++i) {
+      if (v.ntok[i] == 0) continue;
+      int m = snprintf(line, sizeof line, "block=%lld tag=%s tier=%d ref=%d pinned=%d last_used=%lld tokens=%d\n",
+                       (long long)i, tag_name(v.tag[i]), tier_of(v.tag[i]), v.ref[i], v.pinned[i] ? 1 : 0,
+                       (long long)v.last[i], v.ntok[i]);
+      out.append(line, m);
+    }
+    *len = static_cast<int64_t>(out.size());
+    if (buf && cap > 0) {
+      int64_t m = std::min<int64_t>(cap - 1, *len);
+      std::memcpy(buf, out.data(), m);
+      buf[m] = 0;
+    }
+    return int(SB_OK);
+  });
+}
+
+int sb_kv_stats(const sb_kv_cache* c, uint64_t out[6]) {
+  return guard([&] {
+    unsigned long long v[C_N];
+    SB_CUDA(cudaMemcpy(v, c->P.ctr, sizeof(v), cudaMemcpyDeviceToHost));
+    out[0] = v[C_LOOKUPS];
+    out[1] = v[C_HIT_TOK];
+    out[2] = v[C_LOOK_TOK];
+    out[3] = v[C_INS_BLOCKS];
+    out[4] = v[C_EV_BLOCKS];
+    out[5] = v[C_FULL];
+    return int(SB_OK);
+  });
+}
+
+}  // extern "C"

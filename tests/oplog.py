@@ -113,3 +113,65 @@ def replay(ops: List[dict], factory: Callable, check_dump: bool = True, max_erro
     if cache is not None and hasattr(cache, "close"):
         cache.close()
     return errs
+
+
+class StatusAdapter:
+    """Wraps the product's exception-raising KvCache into the status-code call
+    surface the op-log replayer uses."""
+
+    def __init__(self, cache):
+        self.c = cache
+
+    def _st(self, fn, *a):
+        from paper_2601_12967_b200 import errors
+
+        try:
+            return 0, fn(*a)
+        except Exception as e:  # map back to the C-ABI status codes
+            for cls, code in errors.STATUS_OF.items():
+                if type(e) is cls:
+                    return code, None
+            raise
+
+    def lookup_prefix(self, t, now):
+        return self.c.lookup_prefix(t, now)
+
+    def insert(self, t, tags, now):
+        st, ids = self._st(self.c.insert, t, tags, now)
+        return st, ids or []
+
+    def evict(self, needed):
+        st, ids = self._st(self.c.evict, needed)
+        return st, ids or []
+
+    def set_reuse_priority(self, ids, pinned, tier):
+        return self._st(self.c.set_reuse_priority, ids, None if pinned < 0 else bool(pinned),
+                        None if tier < 0 else tier)[0]
+
+    def set_tag(self, bid, tag):
+        return self._st(self.c.set_tag, bid, tag)[0]
+
+    def release(self, ids):
+        return self._st(self.c.release, ids)[0]
+
+    def touch(self, ids, now):
+        return self._st(self.c.touch, ids, now)[0]
+
+    def block(self, bid):
+        st, b = self._st(self.c.block, bid)
+        if st:
+            return st, None
+        return 0, dict(tag=b.tag, tier=b.tier, ref=b.ref_count, pinned=int(b.pinned), ntok=len(b.tokens),
+                       last=b.last_used, chain=b.chain_hash, parent=b.parent_hash, tokens=b.tokens)
+
+    def dump(self):
+        return self.c.dump()
+
+    def audit(self):
+        return self._st(self.c.audit)[0]
+
+    def total_evicted(self):
+        return self.c.total_evicted()
+
+    def close(self):
+        self.c.close()

@@ -1,0 +1,114 @@
+"""GPU numerics of the continuation-prefill attention kernel (csrc/attention.cu)
+against a plain PyTorch fp32 reference of the same op.  Tolerance (north
+star): bf16 outputs within 1e-2 relative (max-norm) of the fp32 reference."""
+import math
+
+import numpy as np
+import pytest
+
+REL_TOL_BF16 = 1e-2
+
+
+def ref_attention(q, k_pool, v_pool, q_off, kv_lens, table, scale):
+    """fp32 reference: gather pages, causal over the suffix, full over the prefix."""
+    import torch
+
+    out = torch.zeros_like(q, dtype=torch.float32)
+    n_kv = k_pool.shape[1]
+    group = q.shape[1] // n_kv
+    for s in range(len(kv_lens)):
+        a, b = int(q_off[s]), int(q_off[s + 1])
+        ql, kl = b - a, int(kv_lens[s])
+        if ql == 0:
+            continue
+        pages = table[s, : (kl + 15) // 16].long()
+        k = k_pool[pages].float().permute(1, 0, 2, 3).reshape(n_kv, -1, 128)[:, :kl]  # [kvh, kl, d]
+        v = v_pool[pages].float().permute(1, 0, 2, 3).reshape(n_kv, -1, 128)[:, :kl]
+        qs = q[a:b].float().permute(1, 0, 2)  # [hq, ql, d]
+        k = k.repeat_interleave(group, 0)
+        v = v.repeat_interleave(group, 0)
+        sc = qs @ k.transpose(1, 2) * scale  # [hq, ql, kl]
+        qpos = torch.arange(kl - ql, kl, device=q.device)[:, None]
+        kpos = torch.arange(kl, device=q.device)[None, :]
+        sc = sc.masked_fill(kpos > qpos, float("-inf"))
+        out[a:b] = (torch.softmax(sc, -1) @ v).permute(1, 0, 2)
+    return out
+
+
+def make_case(q_lens, prefix_lens, n_q_heads, n_kv_heads, seed=0, pool_extra=7):
+    import torch
+
+    g = torch.Generator().manual_seed(seed)
+    kv_lens = [p + q for p, q in zip(prefix_lens, q_lens)]
+    max_blocks = max((k + 15) // 16 for k in kv_lens)
+    n_blocks = sum((k + 15) // 16 for k in kv_lens) + pool_extra
+    perm = torch.randperm(n_blocks, generator=g)
+    table = torch.zeros(len(q_lens), max_blocks, dtype=torch.int32)
+    c = 0
+    for s, k in enumerate(kv_lens):
+        nb = (k + 15) // 16
+        table[s, :nb] = perm[c:c + nb].int()
+        c += nb
+    k_pool = (torch.randn(n_blocks, n_kv_heads, 16, 128, generator=g)).to(torch.bfloat16)
+    v_pool = (torch.randn(n_blocks, n_kv_heads, 16, 128, generator=g)).to(torch.bfloat16)
+    q = (torch.randn(sum(q_lens), n_q_heads, 128, generator=g) * 1.5).to(torch.bfloat16)
+    q_off = torch.tensor(np.cumsum([0] + list(q_lens)), dtype=torch.int32)
+    return q, k_pool, v_pool, q_off, torch.tensor(kv_lens, dtype=torch.int32), table
+
+
+CASES = [
+    # (q_lens, prefix_lens, n_q_heads, n_kv_heads)
+    ([64], [0], 4, 1),                        # single tile, no prefix
+    ([32], [128], 4, 1),                      # exactly one prefix tile
+    ([100, 37, 1], [300, 0, 1000], 8, 2),     # ragged, non-multiples of 16/128
+    ([257, 64], [2048, 4095], 32, 8),         # Llama-3-8B heads, multi-tile
+    ([130], [70], 2, 2),                      # MHA (group 1): 128 tokens per tile
+    ([96, 200], [500, 33], 16, 8),            # group 2
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES)
+def test_continuation_attention_matches_fp32(case):
+    import torch
+    from paper_2601_12967_b200.attention import continuation_attention
+
+    q_lens, prefix, hq, hkv = case
+    q, kp, vp, qo, kl, tb = make_case(q_lens, prefix, hq, hkv)
+    dev = torch.device("cuda")
+    q, kp, vp, qo, kl, tb = (x.to(dev) for x in (q, kp, vp, qo, kl, tb))
+    scale = 1.0 / math.sqrt(128)
+    out = continuation_attention(q, kp, vp, qo, kl, tb, max(q_lens), scale)
+    torch.cuda.synchronize()
+    ref = ref_attention(q, kp, vp, qo.cpu(), kl.cpu(), tb, scale)
+    err = (out.float() - ref).abs().max().item()
+    assert torch.isfinite(out.float()).all()
+    assert err <= REL_TOL_BF16 * ref.abs().max().item() + 1e-3, err
+
+
+@pytest.mark.gpu
+def test_kv_append_then_attend():
+    """extend_prefill semantics: write the suffix K/V into pool pages, then the
+    suffix queries attend over prefix + suffix."""
+    import torch
+    from paper_2601_12967_b200.attention import continuation_attention, kv_append
+
+    dev = torch.device("cuda")
+    q_lens, prefix = [48, 130], [200, 16]
+    q, kp, vp, qo, kl, tb = (x.to(dev) for x in make_case(q_lens, prefix, 8, 2, seed=3))
+    g = torch.Generator(device="cpu").manual_seed(4)
+    k_new = torch.randn(sum(q_lens), 2, 128, generator=g).to(torch.bfloat16).to(dev)
+    v_new = torch.randn(sum(q_lens), 2, 128, generator=g).to(torch.bfloat16).to(dev)
+    kv_append(k_new, v_new, kp, vp, qo, kl, tb)
+    torch.cuda.synchronize()
+    # the appended rows are where the table says
+    for s, (ql, pl) in enumerate(zip(q_lens, prefix)):
+        for i in (0, ql - 1):
+            pos = pl + i
+            page = int(tb[s, pos // 16])
+            tok = int(qo[s]) + i
+            assert torch.equal(kp[page, :, pos % 16], k_new[tok])
+            assert torch.equal(vp[page, :, pos % 16], v_new[tok])
+    out = continuation_attention(q, kp, vp, qo, kl, tb, max(q_lens))
+    ref = ref_attention(q, kp, vp, qo.cpu(), kl.cpu(), tb, 1 / math.sqrt(128))
+    assert (out.float() - ref).abs().max().item() <= REL_TOL_BF16 * ref.abs().max().item() + 1e-3

@@ -1,0 +1,167 @@
+"""GPU parity of the device block pool (csrc/kv_pool.cu) with the reference:
+golden op logs recorded from the reference engine + randomized large-scale
+comparisons against the C oracle.  Bit-exact: hit lengths, block ids,
+eviction order, statuses and the full audit dump after every op."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests import oplog
+
+
+def product(bs, cap, pol):
+    from paper_2601_12967_b200.kv_cache import CacheConfig, KvCache
+
+    return oplog.StatusAdapter(KvCache(CacheConfig(bs, cap, pol)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", oplog.golden_logs())
+def test_product_replays_reference_oplog(name):
+    errs = oplog.replay(oplog.load(name), product)
+    assert not errs, "\n".join(errs)
+
+
+def _random_workload(seed, n_ops, bs, cap, pol, long=False):
+    """Engine-like traffic: shared system prompts, growing conversations,
+    partial-prefill pins, releases, explicit evictions."""
+    rng = np.random.default_rng(seed)
+    sys_prompts = [O.materialize(0, int(rng.integers(200, 2500 if long else 600)), 100 + k) for k in range(5)]
+    ops = []
+    live = []
+    now = 0
+    for _ in range(n_ops):
+        now += int(rng.integers(0, 20))
+        r = rng.random()
+        sp = sys_prompts[int(rng.integers(len(sys_prompts)))]
+        tail = O.materialize(int(rng.integers(4)), int(rng.integers(0, 3000 if long else 400)), int(rng.integers(50)),
+                             int(rng.integers(-1, 3)))
+        toks = np.concatenate([sp, tail])
+        if r < 0.35:
+            ops.append(("lookup", toks, now))
+        elif r < 0.75:
+            n = len(toks)
+            cut = int(rng.integers(1, n)) if n > 1 else n
+            tags = [(0, cut, int(rng.integers(6))), (cut, n, int(rng.integers(6)))] if cut < n else [(0, n, 3)]
+            ops.append(("insert", toks, tags, now))
+        elif r < 0.9:
+            ops.append(("release_one",))
+        elif r < 0.95:
+            ops.append(("evict", int(rng.integers(1, max(2, cap // 8)))))
+        else:
+            ops.append(("pin_some", int(rng.integers(0, 2))))
+    return ops
+
+
+def _run(cache, ops, bs):
+    out = []
+    live = []
+    rng = np.random.default_rng(7)
+    for op in ops:
+        if op[0] == "lookup":
+            out.append(("L", cache.lookup_prefix(op[1], op[2])))
+        elif op[0] == "insert":
+            st, ids = cache.insert(op[1], op[2], op[3])
+            out.append(("I", st, tuple(ids)))
+            if st == 0:
+                live.append(ids)
+        elif op[0] == "release_one":
+            if live:
+                ids = live.pop(int(rng.integers(len(live))))
+                out.append(("R", cache.release(ids)))
+        elif op[0] == "evict":
+            out.append(("E", tuple(cache.evict(op[1])[1])))
+        elif op[0] == "pin_some":
+            if live:
+                out.append(("P", cache.set_reuse_priority(live[-1][:3], op[1], -1)))
+    out.append(("D", cache.dump()))
+    out.append(("T", cache.total_evicted()))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pol", [0, 1])
+def test_product_matches_oracle_engine_like(pol):
+    bs, cap = 16, 700
+    ops = _random_workload(3 + pol, 400, bs, cap, pol)
+    ref = _run(O.OracleCache(bs, cap, pol), ops, bs)
+    got = _run(product(bs, cap, pol), ops, bs)
+    for i, (a, b) in enumerate(zip(ref, got)):
+        assert a == b, f"op {i}: oracle {str(a)[:200]} vs product {str(b)[:200]}"
+
+
+@pytest.mark.gpu
+def test_product_matches_oracle_large_pool_long_prompts():
+    """8192-block pool (the reference's default capacity), multi-K-token prompts:
+    victim lists longer than the shared-memory sort exercise the global path."""
+    bs, cap = 16, 8192
+    ops = _random_workload(11, 160, bs, cap, 1, long=True)
+    ref = _run(O.OracleCache(bs, cap, 1), ops, bs)
+    got = _run(product(bs, cap, 1), ops, bs)
+    for i, (a, b) in enumerate(zip(ref, got)):
+        assert a == b, f"op {i}: oracle {str(a)[:200]} vs product {str(b)[:200]}"
+
+
+@pytest.mark.gpu
+def test_evict_everything_sorted_order():
+    bs, cap = 4, 9000  # > shared-memory sort size when evicting all
+    c = product(bs, cap, 1)
+    o = O.OracleCache(bs, cap, 1)
+    rng = np.random.default_rng(5)
+    for k in range(40):
+        t = O.materialize(int(rng.integers(4)), int(rng.integers(1, 900)), k)
+        tags = [(0, len(t), int(rng.integers(6)))]
+        a = o.insert(t, tags, k)
+        b = c.insert(t, tags, k)
+        assert a == b
+        if a[0] == 0:
+            assert o.release(a[1]) == c.release(b[1]) == 0
+    assert o.evict(cap) == c.evict(cap)
+    assert o.dump() == c.dump()
+
+
+@pytest.mark.gpu
+def test_batch_apis_match_sequential_oracle():
+    import torch
+    import ctypes as C
+    from paper_2601_12967_b200 import _lib
+    from paper_2601_12967_b200.kv_cache import CacheConfig, KvCache
+
+    bs, cap = 16, 600
+    rng = np.random.default_rng(9)
+    base = O.materialize(0, 700, 1)
+    seqs = [np.concatenate([base[: int(rng.integers(0, 700))], O.materialize(2, int(rng.integers(1, 300)), k, 0)])
+            for k in range(24)]
+    tags = [[(0, len(s), int(rng.integers(6)))] for s in seqs]
+    o = O.OracleCache(bs, cap, 1)
+    exp = [o.insert(s, t, 5) for s, t in zip(seqs, tags)]
+    exp_hits = [o.lookup_prefix(s, 9) for s in seqs]
+    c = KvCache(CacheConfig(bs, cap, 1))
+    dev = torch.device("cuda")
+    tok = torch.from_numpy(np.concatenate(seqs).view(np.int64)).to(dev)
+    off = torch.tensor(np.cumsum([0] + [len(s) for s in seqs]), dtype=torch.int64, device=dev)
+    blk = torch.tensor(np.cumsum([0] + [(len(s) + bs - 1) // bs for s in seqs]), dtype=torch.int64, device=dev)
+    tag_arr = (_lib.TagRange * len(seqs))()
+    for i, t in enumerate(tags):
+        tag_arr[i].begin, tag_arr[i].end, tag_arr[i].tag = t[0]
+    tag_dev = torch.empty(len(seqs) * 24, dtype=torch.uint8, device=dev)
+    tag_dev.copy_(torch.frombuffer(bytearray(tag_arr), dtype=torch.uint8))
+    tag_off = torch.arange(len(seqs) + 1, dtype=torch.int64, device=dev)
+    out_ids = torch.full((int(blk[-1]),), -1, dtype=torch.int32, device=dev)
+    status = torch.zeros(len(seqs), dtype=torch.int32, device=dev)
+    p = lambda t: C.c_void_p(t.data_ptr())
+    _lib.check(_lib.lib().sb_kv_insert_batch(c.handle, p(tok), p(off), p(tag_dev), p(tag_off), p(blk), None,
+                                             len(seqs), 5, p(out_ids), p(status), None))
+    torch.cuda.synchronize()
+    st = status.cpu().tolist()
+    ids = out_ids.cpu().tolist()
+    b = blk.cpu().tolist()
+    for i, (est, eids) in enumerate(exp):
+        assert st[i] == est, i
+        if est == 0:
+            assert ids[b[i]:b[i + 1]] == eids, i
+    hits = torch.zeros(len(seqs), dtype=torch.int64, device=dev)
+    _lib.check(_lib.lib().sb_kv_lookup_prefix_batch(c.handle, p(tok), p(off), len(seqs), 9, p(hits), None))
+    torch.cuda.synchronize()
+    assert hits.cpu().tolist() == exp_hits
+    assert c.dump() == o.dump()
