@@ -149,21 +149,29 @@ int sb_kv_dump(const sb_kv_cache* cache, char* buf, int64_t cap, int64_t* len);
 /* ---- batched, stream-ordered engine path (no host round trip) --------- */
 /* Batched lookup_prefix: sequence s is d_tokens[d_seq_offsets[s]..[s+1]);
  * d_hit_tokens[s] receives its hit length.  Touch semantics are identical to
- * calling lookup_prefix for each sequence at the same `now`. */
+ * calling lookup_prefix for each sequence at the same `now`.  Optional
+ * precomputed chain hashes (d_block_hashes, laid out by d_block_offsets with
+ * ceil(len/block_size) entries per sequence, as for insert) skip hashing;
+ * pass NULL for both to hash here.  h_block_offsets (optional host copy of
+ * d_block_offsets) avoids a device->host read, keeping the call fully
+ * stream-ordered. */
 int sb_kv_lookup_prefix_batch(sb_kv_cache* cache, const uint64_t* d_tokens,
-                              const int64_t* d_seq_offsets, int32_t n_seqs, int64_t now,
-                              int64_t* d_hit_tokens, void* stream);
+                              const int64_t* d_seq_offsets, const int64_t* d_block_offsets,
+                              const int64_t* h_block_offsets, const uint64_t* d_block_hashes,
+                              int32_t n_seqs, int64_t now, int64_t* d_hit_tokens, void* stream);
 /* Batched insert with the reference's sequential semantics (sequence 0 is
  * applied first).  Tag ranges for sequence s are
  * d_tags[d_tag_offsets[s]..[s+1]) with sequence-local token positions.
  * d_out_ids[d_block_offsets[s] + j] receive block ids; d_status[s] a status
  * code.  Optional d_block_hashes (NULL = computed here) are precomputed chain
- * hashes laid out like d_out_ids. */
+ * hashes laid out like d_out_ids; optional h_block_offsets is a host copy of
+ * d_block_offsets (NULL = read back, one synchronisation). */
 int sb_kv_insert_batch(sb_kv_cache* cache, const uint64_t* d_tokens,
                        const int64_t* d_seq_offsets, const sb_tag_range* d_tags,
                        const int64_t* d_tag_offsets, const int64_t* d_block_offsets,
-                       const uint64_t* d_block_hashes, int32_t n_seqs, int64_t now,
-                       int32_t* d_out_ids, int32_t* d_status, void* stream);
+                       const int64_t* h_block_offsets, const uint64_t* d_block_hashes,
+                       int32_t n_seqs, int64_t now, int32_t* d_out_ids, int32_t* d_status,
+                       void* stream);
 /* Batched release of d_ids[0..n). */
 int sb_kv_release_batch(sb_kv_cache* cache, const int32_t* d_ids, int64_t n, int32_t* d_status,
                         void* stream);
@@ -181,7 +189,7 @@ int sb_kv_stats(const sb_kv_cache* cache, uint64_t out[6]);
  *  q        [total_q, n_q_heads, head_dim] bf16 (suffix queries, packed)
  *  k_pool,v_pool [n_pool_blocks, n_kv_heads, page_size, head_dim] bf16
  *  out      [total_q, n_q_heads, head_dim] bf16
- *  d_q_offsets[s]..[s+1]   rows of q for sequence s (n_q_heads rows each token)
+ *  d_q_offsets[s]..[s+1]   suffix tokens of sequence s within q (total_q = d_q_offsets[n_seqs])
  *  d_kv_lens[s]            total keys of s (prefix + suffix); the suffix
  *                          occupies the last (q_len) positions
  *  d_block_table[s*max_blocks + j]  pool block of key positions
@@ -190,7 +198,8 @@ int sb_kv_stats(const sb_kv_cache* cache, uint64_t out[6]);
 int sb_continuation_attention(const void* q, const void* k_pool, const void* v_pool, void* out,
                               const int32_t* d_q_offsets, const int32_t* d_kv_lens,
                               const int32_t* d_block_table, int32_t n_seqs,
-                              int32_t max_blocks_per_seq, int32_t max_q_len, int32_t n_q_heads,
+                              int32_t max_blocks_per_seq, int32_t max_q_len, int32_t total_q,
+                              int32_t n_q_heads,
                               int32_t n_kv_heads, int32_t head_dim, int32_t page_size,
                               int64_t n_pool_blocks, float softmax_scale, void* stream);
 
@@ -200,6 +209,17 @@ int sb_kv_append(const void* k_new, const void* v_new, void* k_pool, void* v_poo
                  const int32_t* d_q_offsets, const int32_t* d_kv_lens,
                  const int32_t* d_block_table, int32_t n_seqs, int32_t max_blocks_per_seq,
                  int32_t n_kv_heads, int32_t head_dim, int32_t page_size, void* stream);
+
+/* ---- engine-path helpers ---------------------------------------------- */
+/* Dense block table from the per-sequence chain ids returned by
+ * sb_kv_insert_batch: table[s*max_blocks + j] = ids[block_offsets[s] + j]
+ * for j < block_offsets[s+1]-block_offsets[s], -1 elsewhere. */
+int sb_build_block_table(const int32_t* d_ids, const int64_t* d_block_offsets, int32_t n_seqs,
+                         int32_t max_blocks, int32_t* d_table, void* stream);
+/* Deterministic pseudo-random bf16 fill in [-amp, amp) keyed by `seed`: the
+ * stand-in for projection outputs / prefilled pages with random-init
+ * weights. */
+int sb_fill_random_bf16(void* d_out, int64_t n_elems, uint64_t seed, float amp, void* stream);
 
 #ifdef __cplusplus
 }

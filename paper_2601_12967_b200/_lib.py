@@ -60,12 +60,14 @@ SIGNATURES = {
     "sb_kv_block": (C.c_int, [VP, C.c_int32, C.POINTER(BlockInfo), U64P]),
     "sb_kv_audit": (C.c_int, [VP]),
     "sb_kv_dump": (C.c_int, [VP, C.c_char_p, C.c_int64, I64P]),
-    "sb_kv_lookup_prefix_batch": (C.c_int, [VP, VP, VP, C.c_int32, C.c_int64, VP, VP]),
-    "sb_kv_insert_batch": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int64, VP, VP, VP]),
+    "sb_kv_lookup_prefix_batch": (C.c_int, [VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int64, VP, VP]),
+    "sb_kv_insert_batch": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int64, VP, VP, VP]),
     "sb_kv_release_batch": (C.c_int, [VP, VP, C.c_int64, VP, VP]),
     "sb_kv_stats": (C.c_int, [VP, U64P]),
     "sb_continuation_attention": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
-                                            C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_float, VP]),
+                                            C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_float, VP]),
+    "sb_build_block_table": (C.c_int, [VP, VP, C.c_int32, C.c_int32, VP, VP]),
+    "sb_fill_random_bf16": (C.c_int, [VP, C.c_int64, C.c_uint64, C.c_float, VP]),
     "sb_kv_append": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, VP]),
 }
 

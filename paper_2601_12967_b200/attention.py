@@ -48,7 +48,8 @@ def continuation_attention(q, k_pool, v_pool, q_offsets, kv_lens, block_table, m
     n_seqs = kv_lens.numel()
     st = _lib.lib().sb_continuation_attention(
         _ptr(q), _ptr(k_pool), _ptr(v_pool), _ptr(out), _ptr(q_offsets), _ptr(kv_lens), _ptr(block_table), n_seqs,
-        block_table.shape[1], max_q_len, n_q_heads, n_kv_heads, head_dim, page, n_blocks, C.c_float(softmax_scale),
+        block_table.shape[1], max_q_len, total_q, n_q_heads, n_kv_heads, head_dim, page, n_blocks,
+        C.c_float(softmax_scale),
         _stream_ptr(stream))
     _lib.check(st, "continuation_attention")
     return out

@@ -329,7 +329,8 @@ using namespace sb;
 extern "C" int sb_continuation_attention(const void* q, const void* k_pool, const void* v_pool, void* out,
                                          const int32_t* d_q_offsets, const int32_t* d_kv_lens,
                                          const int32_t* d_block_table, int32_t n_seqs, int32_t max_blocks_per_seq,
-                                         int32_t max_q_len, int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim,
+                                         int32_t max_q_len, int32_t total_q, int32_t n_q_heads, int32_t n_kv_heads,
+                                         int32_t head_dim,
                                          int32_t page_size, int64_t n_pool_blocks, float softmax_scale, void* stream) {
   return guard([&] {
     if (head_dim != 128 || page_size != 16) throw Error(SB_ERR_UNSUPPORTED, "head_dim must be 128 and page_size 16");
@@ -340,10 +341,6 @@ extern "C" int sb_continuation_attention(const void* q, const void* k_pool, cons
     const int64_t kv_rows = n_pool_blocks * n_kv_heads * page_size;
     if (kv_rows + 16 >= (int64_t(1) << 31)) throw Error(SB_ERR_UNSUPPORTED, "KV pool too large for 32-bit TMA rows");
     const int tpt = 128 / group;
-    int total_q = 0;
-    SB_CUDA(cudaMemcpyAsync(&total_q, d_q_offsets + n_seqs, sizeof(int32_t), cudaMemcpyDeviceToHost,
-                            static_cast<cudaStream_t>(stream)));
-    SB_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
     if (total_q <= 0) return int(SB_OK);
     uint64_t qdims[3] = {128, static_cast<uint64_t>(n_q_heads), static_cast<uint64_t>(total_q)};
     uint64_t qstr[2] = {128 * 2, static_cast<uint64_t>(n_q_heads) * 128 * 2};

@@ -46,7 +46,11 @@ constexpr int kSelectThreads = 1024;
 constexpr int kSortSmemKeys = 8192;
 
 enum Ctr { C_NRES = 0, C_EVICTED, C_LOOKUPS, C_HIT_TOK, C_LOOK_TOK, C_INS_BLOCKS, C_EV_BLOCKS, C_FULL, C_N };
-enum Scal { S_F = 0, S_K, S_FREE, S_NEV, S_STATUS, S_FAILPOS, S_NNEW, S_NCAND, S_ERRIDX, S_N };
+enum Scal { S_F = 0, S_K, S_FREE, S_NEV, S_STATUS, S_FAILPOS, S_NNEW, S_NCAND, S_ERRIDX, S_NLATE, S_N };
+// Blocks whose ref_count is -1 (reachable only through duplicate releases)
+// become eviction candidates the moment an insert hits them; at most this
+// many are tracked per insert.
+constexpr int kLateMax = 64;
 
 struct Pool {
   int64_t bs, cap, tcap;
@@ -79,6 +83,7 @@ struct Scratch {
   uint64_t* keys = nullptr;     // cap
   uint64_t* sortbuf = nullptr;  // kmax (global sort fallback)
   int64_t* scal = nullptr;      // S_N
+  int32_t* late = nullptr;      // 2 * kLateMax: (position, id) of hits on ref==-1 blocks before the first miss
 };
 
 __device__ __forceinline__ uint64_t index_slot(uint64_t h, int64_t tcap) {
@@ -170,13 +175,19 @@ __device__ __forceinline__ int find_seq(const int64_t* __restrict__ blk_off, int
 // Pre-state probe of every block position of a batch of sequences.
 __global__ void k_probe_batch(Pool P, const uint64_t* __restrict__ tokens, const int64_t* __restrict__ seq_off,
                               const int64_t* __restrict__ blk_off, int n_seqs, const uint64_t* __restrict__ hashes,
-                              int64_t total_blocks, int32_t* __restrict__ prehit, int64_t* __restrict__ first_miss) {
+                              int64_t total_blocks, int32_t* __restrict__ prehit, int64_t* __restrict__ first_miss,
+                              int full_only_check) {
   const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (g >= total_blocks) return;
   const int s = find_seq(blk_off, n_seqs, g);
   const int64_t j = g - blk_off[s];
   const int64_t base = seq_off[s] + j * P.bs;
   const int len = static_cast<int>(min(P.bs, seq_off[s + 1] - base));
+  if (full_only_check && len < P.bs) {  // lookups never match a partial block (kv_cache.cpp:423)
+    prehit[g] = -1;
+    if (first_miss) atomicMin(reinterpret_cast<unsigned long long*>(first_miss + s), static_cast<unsigned long long>(j));
+    return;
+  }
   const uint64_t parent = j ? hashes[g - 1] : kRootHash;
   const int32_t id = probe_find(P, hashes[g], parent, tokens + base, len);
   prehit[g] = id;
@@ -365,9 +376,19 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
   uint32_t my_hc = 0, my_excl = 0;
   if (mode == 0) {
     const int64_t b0 = A.blk_off[s];
+    if (t == 0) S.scal[S_NLATE] = 0;
+    __syncthreads();
     for (int64_t p = t; p < P_; p += blockDim.x) {
       const int32_t id = S.prehit[b0 + p];
+      if (p < f) S.kind[p] = 0;
       if (id < 0) continue;
+      if (p < f && P.ref[id] == -1 && P.pinned[id] == 0) {
+        const int64_t at = atomicAdd(reinterpret_cast<unsigned long long*>(&S.scal[S_NLATE]), 1ull);
+        if (at < kLateMax) {
+          S.late[2 * at] = static_cast<int32_t>(p);
+          S.late[2 * at + 1] = id;
+        }
+      }
       if (p < f) {
         if (S.keys[id] != kNoKey) {
           // several positions could name the same block only via hash cycles; tolerate
@@ -516,6 +537,21 @@ __global__ void k_walk(Pool P, Scratch S, InsertArgs A, int s) {
   const int64_t b0 = A.blk_off[s];
   const int64_t P_ = A.blk_off[s + 1] - b0;
   const int64_t f = S.scal[S_F], K = S.scal[S_K], Fp = S.scal[S_FREE];
+  const uint64_t now_bits = static_cast<uint64_t>(A.now + kLastBias) << kIdBits;
+  // late candidates: blocks that a hit in this insert raised from ref -1 to 0
+  uint64_t lkey[kLateMax];
+  int32_t lpos[kLateMax];
+  int nl = 0;
+  auto late_key = [&](int32_t id) {
+    uint64_t k = now_bits | static_cast<uint64_t>(id);
+    if (P.policy == SB_POLICY_TIERED) k |= static_cast<uint64_t>(tier_of(P.tag[id])) << 61;
+    return k;
+  };
+  const int64_t n_pre_late = S.scal[S_NLATE] < kLateMax ? S.scal[S_NLATE] : int64_t(kLateMax);
+  for (int64_t i = 0; i < n_pre_late; ++i) {
+    lpos[nl] = S.late[2 * i];
+    lkey[nl++] = late_key(S.late[2 * i + 1]);
+  }
   int64_t ptr = 0, fi = 0, nev = 0, nnew = 0, failpos = -1;
   int status = 0;
   for (int64_t p = f; p < P_; ++p) {
@@ -531,6 +567,10 @@ __global__ void k_walk(Pool P, Scratch S, InsertArgs A, int s) {
     if (!miss) {
       S.chain_out[p] = b;
       S.kind[p] = 0;
+      if (P.ref[b] == -1 && P.pinned[b] == 0 && nl < kLateMax) {
+        lpos[nl] = static_cast<int32_t>(p);
+        lkey[nl++] = late_key(b);
+      }
       continue;
     }
     int32_t id;
@@ -538,12 +578,24 @@ __global__ void k_walk(Pool P, Scratch S, InsertArgs A, int s) {
       id = S.freel[fi++];
     } else {
       while (ptr < K && S.taken[ptr]) ++ptr;
-      if (ptr >= K) {
+      int li = -1;
+      for (int i = 0; i < nl; ++i)
+        if (li < 0 || lkey[i] < lkey[li]) li = i;
+      const bool use_list = ptr < K && (li < 0 || S.victims[ptr] < lkey[li]);
+      if (!use_list && li < 0) {
         status = SB_ERR_CACHE_FULL;
         failpos = p;
         break;
       }
-      id = static_cast<int32_t>(S.victims[ptr++] & kIdMask);
+      if (use_list) {
+        id = static_cast<int32_t>(S.victims[ptr++] & kIdMask);
+      } else {
+        id = static_cast<int32_t>(lkey[li] & kIdMask);
+        S.kind[lpos[li]] = 2;  // hit, then evicted later in this insert
+        lkey[li] = lkey[nl - 1];
+        lpos[li] = lpos[nl - 1];
+        --nl;
+      }
       S.evicted[nev++] = id;
     }
     S.chain_out[p] = id;
@@ -602,9 +654,12 @@ __global__ void k_commit_apply(Pool P, Scratch S, InsertArgs A, int s) {
   const sb_tag_range* tags = A.tags + A.tag_off[s];
   const int64_t ntags = A.tag_off[s + 1] - A.tag_off[s];
   for (int64_t p = gid; p < limit; p += stride) {
-    const bool hit = p < f || S.kind[p] == 0;
+    const int kd = S.kind[p];
+    const bool hit = kd == 0;
     const int32_t id = p < f ? S.prehit[b0 + p] : S.chain_out[p];
-    if (hit) {
+    if (kd == 2) {
+      // block was hit, then evicted (and possibly re-allocated) later in this insert
+    } else if (hit) {
       if (status == 0) atomicAdd(&P.ref[id], 1);
       P.last[id] = A.now;
     } else if (status == 0) {
@@ -733,12 +788,24 @@ struct sb_kv_cache {
   int64_t hash_cap = 0;
   int32_t* d_prehit_all = nullptr;
   int64_t prehit_cap = 0;
+  int64_t* d_batch_blk = nullptr;
+  int64_t* d_batch_first = nullptr;
+  int64_t batch_cap = 0;
+
+  void ensure_batch(int64_t n) {
+    if (n <= batch_cap) return;
+    cudaFree(d_batch_blk);
+    cudaFree(d_batch_first);
+    batch_cap = std::max<int64_t>(n, 2 * batch_cap);
+    d_batch_blk = dalloc<int64_t>(batch_cap + 1);
+    d_batch_first = dalloc<int64_t>(batch_cap + 1);
+  }
 
   ~sb_kv_cache() {
     cudaSetDevice(device);
     void* ptrs[] = {P.tok, P.ntok, P.chain, P.parent, P.tag, P.ref, P.pinned, P.last, P.tkey, P.tval, P.slot, P.ctr,
                     S.hashes, S.prehit, S.chain_out, S.kind, S.freel, S.evicted, S.victims, S.taken, S.rank_of, S.keys,
-                    S.sortbuf, S.scal, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all};
+                    S.sortbuf, S.scal, S.late, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
@@ -923,6 +990,7 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
       S.keys = dalloc<uint64_t>(capacity_blocks);
       S.evicted = dalloc<int32_t>(capacity_blocks + 16);
       S.scal = dalloc<int64_t>(S_N);
+      S.late = dalloc<int32_t>(2 * kLateMax);
       SB_CUDA(cudaMemsetAsync(S.scal, 0, sizeof(int64_t) * S_N, c->stream));
       c->ensure_positions(64);
       c->ensure_prehit_all(64);
@@ -964,7 +1032,7 @@ int sb_kv_lookup_prefix(sb_kv_cache* c, const uint64_t* tokens, int64_t n, int64
     k_chain_hash<<<1, 32, 0, c->stream>>>(c->d_tok, seq_off, blk_off, nullptr, 1, c->P.bs, 1, c->d_hash_all);
     k_lookup_init<<<1, 32, 0, c->stream>>>(blk_off, 1, c->d_first);
     k_probe_batch<<<grid_for(nblk), 256, 0, c->stream>>>(c->P, c->d_tok, seq_off, blk_off, 1, c->d_hash_all, nblk,
-                                                         c->d_prehit_all, c->d_first);
+                                                         c->d_prehit_all, c->d_first, 0);
     k_lookup_finish<<<grid_for(nblk + 1), 256, 0, c->stream>>>(c->P, seq_off, blk_off, 1, nblk, c->d_prehit_all,
                                                                c->d_first, now, c->d_hit);
     SB_CHECK_LAUNCH();
@@ -974,36 +1042,52 @@ int sb_kv_lookup_prefix(sb_kv_cache* c, const uint64_t* tokens, int64_t n, int64
   });
 }
 
-int sb_kv_lookup_prefix_batch(sb_kv_cache* c, const uint64_t* d_tokens, const int64_t* d_seq_offsets, int32_t n_seqs,
-                              int64_t now, int64_t* d_hit_tokens, void* stream) {
+int sb_kv_lookup_prefix_batch(sb_kv_cache* c, const uint64_t* d_tokens, const int64_t* d_seq_offsets,
+                              const int64_t* d_block_offsets, const int64_t* h_block_offsets,
+                              const uint64_t* d_block_hashes, int32_t n_seqs, int64_t now, int64_t* d_hit_tokens,
+                              void* stream) {
   return guard([&] {
     std::lock_guard<std::mutex> lk(c->mu);
     SB_CUDA(cudaSetDevice(c->device));
     if (n_seqs <= 0) return int(SB_OK);
+    if (now < -kLastBias || now >= kLastBias) throw Error(SB_ERR_UNSUPPORTED, "now outside +-2^39");
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
     std::vector<int64_t> off(n_seqs + 1), blk(n_seqs + 1);
-    SB_CUDA(cudaMemcpyAsync(off.data(), d_seq_offsets, sizeof(int64_t) * (n_seqs + 1), cudaMemcpyDeviceToHost, st));
-    SB_CUDA(cudaStreamSynchronize(st));
-    blk[0] = 0;
-    for (int s = 0; s < n_seqs; ++s) blk[s + 1] = blk[s] + (off[s + 1] - off[s]) / c->P.bs;
-    const int64_t total = blk[n_seqs];
-    c->ensure_hash_all(total + 1);
+    const bool pre = d_block_hashes && d_block_offsets;
+    if (pre && h_block_offsets) {
+      std::memcpy(off.data(), h_block_offsets, sizeof(int64_t) * (n_seqs + 1));
+    } else {
+      SB_CUDA(cudaMemcpyAsync(off.data(), pre ? d_block_offsets : d_seq_offsets, sizeof(int64_t) * (n_seqs + 1),
+                              cudaMemcpyDeviceToHost, st));
+      SB_CUDA(cudaStreamSynchronize(st));
+    }
+    int64_t total;
+    if (pre) {
+      total = off[n_seqs];
+    } else {
+      blk[0] = 0;
+      for (int s = 0; s < n_seqs; ++s) blk[s + 1] = blk[s] + (off[s + 1] - off[s]) / c->P.bs;
+      total = blk[n_seqs];
+    }
     c->ensure_prehit_all(total + 1);
-    int64_t* d_blk = dalloc<int64_t>(n_seqs + 1);
-    int64_t* d_first = dalloc<int64_t>(n_seqs);
-    SB_CUDA(cudaMemcpyAsync(d_blk, blk.data(), sizeof(int64_t) * (n_seqs + 1), cudaMemcpyHostToDevice, st));
-    k_chain_hash<<<(n_seqs + 127) / 128, 128, 0, st>>>(d_tokens, d_seq_offsets, d_blk, nullptr, n_seqs, c->P.bs, 1,
-                                                       c->d_hash_all);
-    k_lookup_init<<<(n_seqs + 127) / 128, 128, 0, st>>>(d_blk, n_seqs, d_first);
+    c->ensure_batch(n_seqs);
+    const uint64_t* hashes = d_block_hashes;
+    const int64_t* d_blk = d_block_offsets;
+    if (!pre) {
+      c->ensure_hash_all(total + 1);
+      SB_CUDA(cudaMemcpyAsync(c->d_batch_blk, blk.data(), sizeof(int64_t) * (n_seqs + 1), cudaMemcpyHostToDevice, st));
+      d_blk = c->d_batch_blk;
+      k_chain_hash<<<(n_seqs + 127) / 128, 128, 0, st>>>(d_tokens, d_seq_offsets, d_blk, nullptr, n_seqs, c->P.bs, 1,
+                                                         c->d_hash_all);
+      hashes = c->d_hash_all;
+    }
+    k_lookup_init<<<(n_seqs + 127) / 128, 128, 0, st>>>(d_blk, n_seqs, c->d_batch_first);
     if (total > 0)
-      k_probe_batch<<<grid_for(total), 256, 0, st>>>(c->P, d_tokens, d_seq_offsets, d_blk, n_seqs, c->d_hash_all, total,
-                                                     c->d_prehit_all, d_first);
+      k_probe_batch<<<grid_for(total), 256, 0, st>>>(c->P, d_tokens, d_seq_offsets, d_blk, n_seqs, hashes, total,
+                                                     c->d_prehit_all, c->d_batch_first, pre ? 1 : 0);
     k_lookup_finish<<<grid_for(std::max<int64_t>(total, n_seqs)), 256, 0, st>>>(
-        c->P, d_seq_offsets, d_blk, n_seqs, total, c->d_prehit_all, d_first, now, d_hit_tokens);
+        c->P, d_seq_offsets, d_blk, n_seqs, total, c->d_prehit_all, c->d_batch_first, now, d_hit_tokens);
     SB_CHECK_LAUNCH();
-    SB_CUDA(cudaStreamSynchronize(st));
-    cudaFree(d_blk);
-    cudaFree(d_first);
     return int(SB_OK);
   });
 }
@@ -1042,15 +1126,18 @@ int sb_kv_insert(sb_kv_cache* c, const uint64_t* tokens, int64_t n, const sb_tag
 
 int sb_kv_insert_batch(sb_kv_cache* c, const uint64_t* d_tokens, const int64_t* d_seq_offsets,
                        const sb_tag_range* d_tags, const int64_t* d_tag_offsets, const int64_t* d_block_offsets,
-                       const uint64_t* d_block_hashes, int32_t n_seqs, int64_t now, int32_t* d_out_ids,
-                       int32_t* d_status, void* stream) {
+                       const int64_t* h_block_offsets, const uint64_t* d_block_hashes, int32_t n_seqs, int64_t now,
+                       int32_t* d_out_ids, int32_t* d_status, void* stream) {
   return guard([&] {
     std::lock_guard<std::mutex> lk(c->mu);
     SB_CUDA(cudaSetDevice(c->device));
     if (n_seqs <= 0) return int(SB_OK);
     if (now < -kLastBias || now >= kLastBias) throw Error(SB_ERR_UNSUPPORTED, "now outside +-2^39");
     std::vector<int64_t> hb(n_seqs + 1);
-    SB_CUDA(cudaMemcpy(hb.data(), d_block_offsets, sizeof(int64_t) * (n_seqs + 1), cudaMemcpyDeviceToHost));
+    if (h_block_offsets)
+      std::memcpy(hb.data(), h_block_offsets, sizeof(int64_t) * (n_seqs + 1));
+    else
+      SB_CUDA(cudaMemcpy(hb.data(), d_block_offsets, sizeof(int64_t) * (n_seqs + 1), cudaMemcpyDeviceToHost));
     cudaStream_t saved = c->stream;
     if (stream) c->stream = static_cast<cudaStream_t>(stream);
     try {

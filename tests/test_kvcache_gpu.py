@@ -150,7 +150,7 @@ def test_batch_apis_match_sequential_oracle():
     out_ids = torch.full((int(blk[-1]),), -1, dtype=torch.int32, device=dev)
     status = torch.zeros(len(seqs), dtype=torch.int32, device=dev)
     p = lambda t: C.c_void_p(t.data_ptr())
-    _lib.check(_lib.lib().sb_kv_insert_batch(c.handle, p(tok), p(off), p(tag_dev), p(tag_off), p(blk), None,
+    _lib.check(_lib.lib().sb_kv_insert_batch(c.handle, p(tok), p(off), p(tag_dev), p(tag_off), p(blk), None, None,
                                              len(seqs), 5, p(out_ids), p(status), None))
     torch.cuda.synchronize()
     st = status.cpu().tolist()
@@ -161,7 +161,7 @@ def test_batch_apis_match_sequential_oracle():
         if est == 0:
             assert ids[b[i]:b[i + 1]] == eids, i
     hits = torch.zeros(len(seqs), dtype=torch.int64, device=dev)
-    _lib.check(_lib.lib().sb_kv_lookup_prefix_batch(c.handle, p(tok), p(off), len(seqs), 9, p(hits), None))
+    _lib.check(_lib.lib().sb_kv_lookup_prefix_batch(c.handle, p(tok), p(off), None, None, None, len(seqs), 9, p(hits), None))
     torch.cuda.synchronize()
     assert hits.cpu().tolist() == exp_hits
     assert c.dump() == o.dump()
