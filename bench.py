@@ -117,6 +117,21 @@ def capacity_for(reqs, bs=16, slack=1.25):
     return prefix_blocks, suffix_blocks, prefix_blocks + int(slack * suffix_blocks) + 1
 
 
+def reduce_over_ranks(values, device=None):
+    """Cross-rank reduction of per-rank step statistics: element-wise MAX
+    (times) and SUM (counters).  The only collective of the multi-GPU run
+    (NCCL on GPUs; gloo in tests/test_multirank_stats.py)."""
+    import torch
+    import torch.distributed as dist
+
+    v = torch.tensor(values, dtype=torch.float64, device=device)
+    mx, sm = v.clone(), v.clone()
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    return mx.cpu().tolist(), sm.cpu().tolist()
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local_rank):
     import torch
@@ -140,7 +155,7 @@ def run_ours(args, rank, world, local_rank):
         suffix_host.append(torch.from_numpy(arr).pin_memory())
     suffix_dev = [t.to(dev) for t in suffix_host]
     tokens_per_step = batch.total_q
-    flops_attn = batch.attention_flops() / LLAMA3_8B.n_layers  # per launch (one layer)
+    flops_attn = batch.attention_flops()  # per launch = one layer
     now = 10
     stream = torch.cuda.current_stream()
 
@@ -202,15 +217,10 @@ def run_ours(args, rank, world, local_rank):
     assert (batch.status.cpu().numpy() == 0).all()
 
     # max over ranks; NCCL only for the cross-GPU statistics reduction
-    vec = torch.tensor([ms, ms_e2e, float(hits.sum()), float(sum(batch.full_lens)), float(stats["evicted_blocks"]),
-                        attn_avg_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        mx = vec.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = vec.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms, ms_e2e, attn_avg_ms = float(mx[0]), float(mx[1]), float(mx[5])
-        hit_rate = float(sm[2] / sm[3])
+    mx, sm = reduce_over_ranks([ms, ms_e2e, float(hits.sum()), float(sum(batch.full_lens)),
+                                float(stats["evicted_blocks"]), attn_avg_ms], dev)
+    ms, ms_e2e, attn_avg_ms = mx[0], mx[1], mx[5]
+    hit_rate = sm[2] / sm[3]
     if rank != 0:
         return None
 

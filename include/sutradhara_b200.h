@@ -138,6 +138,9 @@ uint64_t sb_kv_total_evicted(const sb_kv_cache* cache);  /* kv_cache.hpp:303 */
 int32_t sb_kv_policy(const sb_kv_cache* cache);
 /* KvCache::contains(id) — 1 resident, 0 not      kv_cache.hpp:305 */
 int sb_kv_contains(const sb_kv_cache* cache, int32_t id);
+/* Resident block ids in ascending order (the key set of KvCache::blocks_,
+ * kv_cache.hpp:323); out holds capacity entries. */
+int sb_kv_resident_ids(const sb_kv_cache* cache, int32_t* out, int64_t* n_out);
 /* KvCache::block(id); tokens_out may be NULL, else holds block_size u64. */
 int sb_kv_block(const sb_kv_cache* cache, int32_t id, sb_block_info* info, uint64_t* tokens_out);
 /* KvCache::audit()                                kv_cache.cpp:575 */

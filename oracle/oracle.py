@@ -50,6 +50,8 @@ def build_ref() -> bool:
     if not os.path.isdir("/root/reference/proj/src"):
         return os.path.exists(os.path.join(REF_DIR, "libagentsim_ref.so"))
     subprocess.run(["make", "-C", HERE, "-j8", "ref"], check=True, capture_output=True)
+    if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_2601_12967_b200", "_build", "libsutradhara_b200.so")):
+        subprocess.run(["make", "-C", HERE, "-j8", "b200"], check=True, capture_output=True)
     return True
 
 
@@ -288,6 +290,25 @@ def ref():
     return _ref
 
 
+_b200 = None
+
+
+def b200_lib():
+    """Reference engine/orchestrator linked against the B200 block pool."""
+    global _b200
+    with _lock:
+        if _b200 is None:
+            L = _load_ref("libagentsim_b200.so")
+            L.refrun_generate_and_run.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.c_int32, C.c_uint64,
+                                                  C.c_int32, C.c_int64, C.c_int64, I64P, I64P, I64P, I64P,
+                                                  U64P, C.POINTER(C.c_double)]
+            L.refrun_scenarios.argtypes = [C.c_char_p, C.c_int64]
+            L.refrun_thrashing.argtypes = [C.c_int32, I64P]
+            L.refrun_last_error.restype = C.c_char_p
+            _b200 = L
+    return _b200
+
+
 def kvlog_lib():
     global _kvlog
     with _lock:
@@ -383,12 +404,14 @@ class RefCache:
 
 
 def ref_run_trace(n_requests: int, seed: int, preset: int, capacity: int, block_size: int = 16,
-                  workload: Optional[str] = None, gen: Optional[Sequence[float]] = None, kvlog: bool = False):
-    """Generate + replay a trace in the reference simulator.
+                  workload: Optional[str] = None, gen: Optional[Sequence[float]] = None, kvlog: bool = False,
+                  b200: bool = False):
+    """Generate + replay a trace in the reference simulator (b200=True: with
+    its KvCache served by the B200 block pool through the C-ABI).
 
     Returns (ftr, e2e, hit_tokens, prompt_tokens, evictions, wall_s[, oplog]).
     """
-    L = kvlog_lib() if kvlog else ref()
+    L = kvlog_lib() if kvlog else (b200_lib() if b200 else ref())
     g = (C.c_double * 8)(*(list(gen) + [0.0] * (8 - len(gen)))) if gen is not None else None
     ftr = np.zeros(n_requests, np.int64)
     e2e = np.zeros(n_requests, np.int64)

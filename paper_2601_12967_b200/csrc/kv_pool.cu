@@ -1269,6 +1269,19 @@ int sb_kv_contains(const sb_kv_cache* c, int32_t id) {
   return nt > 0 ? 1 : 0;
 }
 
+int sb_kv_resident_ids(const sb_kv_cache* c, int32_t* out, int64_t* n_out) {
+  return guard([&] {
+    SB_CUDA(cudaStreamSynchronize(c->stream));
+    std::vector<int32_t> nt(c->P.cap);
+    SB_CUDA(cudaMemcpy(nt.data(), c->P.ntok, 4 * c->P.cap, cudaMemcpyDeviceToHost));
+    int64_t n = 0;
+    for (int64_t i = 0; i < c->P.cap; ++i)
+      if (nt[i] > 0) out[n++] = static_cast<int32_t>(i);
+    *n_out = n;
+    return int(SB_OK);
+  });
+}
+
 int sb_kv_block(const sb_kv_cache* c, int32_t id, sb_block_info* info, uint64_t* tokens_out) {
   return guard([&] {
     if (id < 0 || id >= c->P.cap || !sb_kv_contains(c, id)) {
