@@ -204,7 +204,17 @@ int sb_continuation_attention(const void* q, const void* k_pool, const void* v_p
                               int32_t max_blocks_per_seq, int32_t max_q_len, int32_t total_q,
                               int32_t n_q_heads,
                               int32_t n_kv_heads, int32_t head_dim, int32_t page_size,
-                              int64_t n_pool_blocks, float softmax_scale, void* stream);
+                              int64_t n_pool_blocks, float softmax_scale, const int32_t* d_work,
+                              int32_t n_work, void* stream);
+
+/* Work list for sb_continuation_attention (host): one item per (sequence, kv
+ * head, pair of 128-row query tiles) that has queries, longest first (LPT),
+ * as int32 pairs {seq, kv_head << 16 | pair}.  out holds 2*cap ints; returns
+ * the item count in *n_out.  With d_work = NULL the kernel walks a dense
+ * (n_seqs x n_kv_heads x pairs(max_q_len)) grid instead. */
+int sb_attention_work_list(const int32_t* h_q_offsets, const int32_t* h_kv_lens, int32_t n_seqs,
+                           int32_t n_q_heads, int32_t n_kv_heads, int32_t* out, int32_t cap,
+                           int32_t* n_out);
 
 /* Scatter the suffix K/V rows into their pool pages (the KV write of
  * extend_prefill).  k_new/v_new [total_q, n_kv_heads, head_dim]. */

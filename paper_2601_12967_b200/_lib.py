@@ -66,7 +66,9 @@ SIGNATURES = {
     "sb_kv_release_batch": (C.c_int, [VP, VP, C.c_int64, VP, VP]),
     "sb_kv_stats": (C.c_int, [VP, U64P]),
     "sb_continuation_attention": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
-                                            C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_float, VP]),
+                                            C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_float, VP,
+                                            C.c_int32, VP]),
+    "sb_attention_work_list": (C.c_int, [I32P, I32P, C.c_int32, C.c_int32, C.c_int32, I32P, C.c_int32, I32P]),
     "sb_build_block_table": (C.c_int, [VP, VP, C.c_int32, C.c_int32, VP, VP]),
     "sb_fill_random_bf16": (C.c_int, [VP, C.c_int64, C.c_uint64, C.c_float, VP]),
     "sb_kv_append": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, VP]),

@@ -32,8 +32,25 @@ def _stream_ptr(stream):
     return C.c_void_p(s.cuda_stream)
 
 
+def attention_work_list(q_lens, kv_lens, n_q_heads: int, n_kv_heads: int):
+    """LPT-ordered work items (host int32 array [n, 2]) for continuation_attention."""
+    import numpy as np
+
+    qo = np.cumsum([0] + list(q_lens)).astype(np.int32)
+    kl = np.asarray(kv_lens, dtype=np.int32)
+    tpt = 128 // (n_q_heads // n_kv_heads)
+    cap = int(sum(-(-q // (2 * tpt)) for q in q_lens)) * n_kv_heads + 1
+    out = np.zeros(2 * cap, dtype=np.int32)
+    n = C.c_int32(0)
+    _lib.check(_lib.lib().sb_attention_work_list(qo.ctypes.data_as(_lib.I32P), kl.ctypes.data_as(_lib.I32P), len(q_lens),
+                                                 n_q_heads, n_kv_heads, out.ctypes.data_as(_lib.I32P), cap, C.byref(n)),
+               "attention_work_list")
+    return out[: 2 * n.value].reshape(-1, 2)
+
+
 def continuation_attention(q, k_pool, v_pool, q_offsets, kv_lens, block_table, max_q_len: int,
-                           softmax_scale: Optional[float] = None, out=None, stream=None):
+                           softmax_scale: Optional[float] = None, out=None, stream=None, work=None):
+    """work: optional device int32 tensor from attention_work_list (LPT order)."""
     import torch
 
     assert q.dtype == torch.bfloat16 and k_pool.dtype == torch.bfloat16 and v_pool.dtype == torch.bfloat16
@@ -49,8 +66,8 @@ def continuation_attention(q, k_pool, v_pool, q_offsets, kv_lens, block_table, m
     st = _lib.lib().sb_continuation_attention(
         _ptr(q), _ptr(k_pool), _ptr(v_pool), _ptr(out), _ptr(q_offsets), _ptr(kv_lens), _ptr(block_table), n_seqs,
         block_table.shape[1], max_q_len, total_q, n_q_heads, n_kv_heads, head_dim, page, n_blocks,
-        C.c_float(softmax_scale),
-        _stream_ptr(stream))
+        C.c_float(softmax_scale), _ptr(work) if work is not None else None,
+        int(work.shape[0]) if work is not None else 0, _stream_ptr(stream))
     _lib.check(st, "continuation_attention")
     return out
 

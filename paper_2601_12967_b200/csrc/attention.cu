@@ -25,7 +25,9 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstdint>
+#include <vector>
 
 #include "common.h"
 #include "sm100.cuh"
@@ -48,6 +50,7 @@ struct Params {
   int32_t n_seqs, max_blocks, n_q_heads, n_kv_heads, group, tpt, pairs_per_seq;
   int32_t oob_row;  // a K/V row coordinate past the end: zero-filled loads
   float scale_log2;
+  const int32_t* work;  // optional {seq, kvh << 16 | pair} items
 };
 
 struct Smem {
@@ -65,6 +68,27 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// packed pair helpers (FFMA2 / FADD2 on sm_100a)
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b, float c) {
+  uint64_t r, pa, pb, pc;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pa) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(pb) : "f"(b));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(pc) : "f"(c));
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pa), "l"(pb), "l"(pc));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(r));
+}
+__device__ __forceinline__ void fadd2(float& a0, float& a1, float b0, float b1) {
+  uint64_t r, pa, pb;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pa) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(pb) : "f"(b0), "f"(b1));
+  asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pa), "l"(pb));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(r));
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
     k_continuation_attention(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -77,10 +101,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5;
   // ---- work item
-  const int item = blockIdx.x;
-  const int pair = item % p.pairs_per_seq;
-  const int kvh = (item / p.pairs_per_seq) % p.n_kv_heads;
-  const int seq = item / (p.pairs_per_seq * p.n_kv_heads);
+  int pair, kvh, seq;
+  if (p.work) {
+    seq = p.work[2 * blockIdx.x];
+    kvh = p.work[2 * blockIdx.x + 1] >> 16;
+    pair = p.work[2 * blockIdx.x + 1] & 0xFFFF;
+  } else {
+    const int item = blockIdx.x;
+    pair = item % p.pairs_per_seq;
+    kvh = (item / p.pairs_per_seq) % p.n_kv_heads;
+    seq = item / (p.pairs_per_seq * p.n_kv_heads);
+  }
   const int q0 = p.q_off[seq];
   const int q_len = p.q_off[seq + 1] - q0;
   const int kv_len = p.kv_len[seq];
@@ -200,24 +231,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < n_kv; ++j) {
       mbar_wait(&ss.s_full[t], j & 1);
       tc_fence_after();
-      float s[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld32(s_col + c * 32, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int k = 0; k < 32; ++k) s[c * 32 + k] = __uint_as_float(v[k]) * p.scale_log2;
-      }
+      // raw scores: four TMEM loads in flight, one wait
+      uint32_t sv[128];
+      tmem_ld32(s_col + 0, *reinterpret_cast<uint32_t(*)[32]>(sv + 0));
+      tmem_ld32(s_col + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+      tmem_ld32(s_col + 64, *reinterpret_cast<uint32_t(*)[32]>(sv + 64));
+      tmem_ld32(s_col + 96, *reinterpret_cast<uint32_t(*)[32]>(sv + 96));
+      tmem_wait_ld();
+      float* s = reinterpret_cast<float*>(sv);
       const int kbase = j * 128;
       if (kbase + 127 > qpos) {
 #pragma unroll
         for (int k = 0; k < 128; ++k)
           if (kbase + k > qpos) s[k] = -INFINITY;
       }
-      float mx = s[0];
+      // row max: 8 independent 3-input max chains, then a short tree
+      float mk[8];
 #pragma unroll
-      for (int k = 1; k < 128; ++k) mx = fmaxf(mx, s[k]);
+      for (int i = 0; i < 8; ++i) mk[i] = fmax3(s[i], s[8 + i], s[16 + i]);
+#pragma unroll
+      for (int k = 24; k + 16 <= 120; k += 16)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mk[i] = fmax3(mk[i], s[k + i], s[k + 8 + i]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mk[i] = fmaxf(mk[i], s[120 + i]);
+      const float mx = fmaxf(fmax3(mk[0], mk[1], mk[2]), fmax3(fmax3(mk[3], mk[4], mk[5]), mk[6], mk[7])) *
+                       p.scale_log2;
       const float m_new = fmaxf(m_used, mx);
       const bool need = m_new > m_used + 8.f;
       float factor = 1.f;
@@ -240,22 +279,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       l *= factor;
-      uint32_t pk[64];
-      float sum = 0.f;
+      // p = 2^(s*scale - m): one FFMA2 per pair, MUFU ex2, 4 packed partial sums
+      const float neg_m = -m_used;
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int k = 0; k < 64; ++k) {
-        const float e0 = ex2(s[2 * k] - m_used), e1 = ex2(s[2 * k + 1] - m_used);
-        sum += e0 + e1;
-        pk[k] = pack_bf16x2(e0, e1);
+      for (int c = 0; c < 4; ++c) {
+        uint32_t w[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          float a0, a1;
+          ffma2(a0, a1, s[32 * c + 2 * k], s[32 * c + 2 * k + 1], p.scale_log2, neg_m);
+          const float e0 = ex2(a0), e1 = ex2(a1);
+          fadd2(acc[2 * (k & 3)], acc[2 * (k & 3) + 1], e0, e1);
+          w[k] = pack_bf16x2(e0, e1);
+        }
+        tmem_st16(s_col + c * 16, w);
       }
-      l += sum;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t w[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) w[k] = pk[c * 32 + k];
-        tmem_st32(s_col + c * 32, w);
-      }
+      fadd2(acc[0], acc[1], acc[2], acc[3]);
+      fadd2(acc[4], acc[5], acc[6], acc[7]);
+      fadd2(acc[0], acc[1], acc[4], acc[5]);
+      l += acc[0] + acc[1];
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&ss.p_full[t]);
@@ -331,7 +374,8 @@ extern "C" int sb_continuation_attention(const void* q, const void* k_pool, cons
                                          const int32_t* d_block_table, int32_t n_seqs, int32_t max_blocks_per_seq,
                                          int32_t max_q_len, int32_t total_q, int32_t n_q_heads, int32_t n_kv_heads,
                                          int32_t head_dim,
-                                         int32_t page_size, int64_t n_pool_blocks, float softmax_scale, void* stream) {
+                                         int32_t page_size, int64_t n_pool_blocks, float softmax_scale,
+                                         const int32_t* d_work, int32_t n_work, void* stream) {
   return guard([&] {
     if (head_dim != 128 || page_size != 16) throw Error(SB_ERR_UNSUPPORTED, "head_dim must be 128 and page_size 16");
     if (n_kv_heads <= 0 || n_q_heads % n_kv_heads) throw Error(SB_ERR_INVALID, "n_q_heads % n_kv_heads != 0");
@@ -365,16 +409,44 @@ extern "C" int sb_continuation_attention(const void* q, const void* k_pool, cons
     prm.pairs_per_seq = (max_q_len + 2 * tpt - 1) / (2 * tpt);
     prm.oob_row = static_cast<int32_t>(kv_rows);
     prm.scale_log2 = softmax_scale * 1.4426950408889634f;
+    prm.work = d_work;
     static bool attr_set = false;
     if (!attr_set) {
       SB_CUDA(cudaFuncSetAttribute(attn::k_continuation_attention, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    attn::kSmemBytes));
       attr_set = true;
     }
-    const int64_t grid = static_cast<int64_t>(n_seqs) * n_kv_heads * prm.pairs_per_seq;
+    const int64_t grid = d_work ? static_cast<int64_t>(n_work) : static_cast<int64_t>(n_seqs) * n_kv_heads * prm.pairs_per_seq;
+    if (grid <= 0) return int(SB_OK);
     attn::k_continuation_attention<<<static_cast<unsigned>(grid), attn::kThreads, attn::kSmemBytes,
                                      static_cast<cudaStream_t>(stream)>>>(tm_q, tm_k, tm_v, prm);
     SB_CHECK_LAUNCH();
+    return int(SB_OK);
+  });
+}
+
+extern "C" int sb_attention_work_list(const int32_t* h_q_offsets, const int32_t* h_kv_lens, int32_t n_seqs,
+                                      int32_t n_q_heads, int32_t n_kv_heads, int32_t* out, int32_t cap, int32_t* n_out) {
+  return guard([&] {
+    if (n_kv_heads <= 0 || n_q_heads % n_kv_heads) throw Error(SB_ERR_INVALID, "n_q_heads % n_kv_heads != 0");
+    const int tpt = 128 / (n_q_heads / n_kv_heads);
+    struct It { int64_t work; int32_t seq, kvh, pair; };
+    std::vector<It> items;
+    for (int s = 0; s < n_seqs; ++s) {
+      const int q_len = h_q_offsets[s + 1] - h_q_offsets[s];
+      const int prefix = h_kv_lens[s] - q_len;
+      for (int pr = 0; pr * 2 * tpt < q_len; ++pr) {
+        const int64_t kv_limit = prefix + std::min(q_len, (pr + 1) * 2 * tpt);
+        for (int h = 0; h < n_kv_heads; ++h) items.push_back({kv_limit, s, h, pr});
+      }
+    }
+    std::stable_sort(items.begin(), items.end(), [](const It& a, const It& b) { return a.work > b.work; });
+    if (static_cast<int64_t>(items.size()) > cap) throw Error(SB_ERR_INVALID, "work list capacity too small");
+    for (size_t i = 0; i < items.size(); ++i) {
+      out[2 * i] = items[i].seq;
+      out[2 * i + 1] = (items[i].kvh << 16) | items[i].pair;
+    }
+    *n_out = static_cast<int32_t>(items.size());
     return int(SB_OK);
   });
 }

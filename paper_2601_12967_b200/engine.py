@@ -167,6 +167,11 @@ class ContinuationBatch:
                       for i in range(self.n)]
         self.suffix_dev = torch.empty(self.total_q, dtype=torch.int64, device=dev)
         self.scale = 1.0 / math.sqrt(sh.head_dim)
+        from .attention import attention_work_list
+
+        w = attention_work_list(self.suffix_lens, self.full_lens, sh.n_q_heads, sh.n_kv_heads)
+        self.work = torch.from_numpy(w.copy()).to(dev)
+        self.n_work = int(w.shape[0])
         self.launches_per_step = None
 
     def stage_suffix_host(self, host_suffix) -> int:
@@ -228,7 +233,8 @@ class ContinuationBatch:
                                                    _p(self.q_off), _p(self.kv_lens), _p(self.table), self.n,
                                                    self.max_blocks, self.max_q, self.total_q, sh.n_q_heads,
                                                    sh.n_kv_heads, sh.head_dim, eng.bs, eng.capacity,
-                                                   C.c_float(self.scale), st), "attention")
+                                                   C.c_float(self.scale), _p(self.work), self.n_work, st),
+                       "attention")
             if ev is not None:
                 ev[1].record()
                 attn_events.append(ev)

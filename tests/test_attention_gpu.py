@@ -69,16 +69,21 @@ CASES = [
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("case", CASES)
-def test_continuation_attention_matches_fp32(case):
+@pytest.mark.parametrize("use_work_list", [False, True])
+def test_continuation_attention_matches_fp32(case, use_work_list):
     import torch
-    from paper_2601_12967_b200.attention import continuation_attention
+    from paper_2601_12967_b200.attention import attention_work_list, continuation_attention
 
     q_lens, prefix, hq, hkv = case
     q, kp, vp, qo, kl, tb = make_case(q_lens, prefix, hq, hkv)
     dev = torch.device("cuda")
     q, kp, vp, qo, kl, tb = (x.to(dev) for x in (q, kp, vp, qo, kl, tb))
     scale = 1.0 / math.sqrt(128)
-    out = continuation_attention(q, kp, vp, qo, kl, tb, max(q_lens), scale)
+    work = None
+    if use_work_list:
+        w = attention_work_list(q_lens, [p + ql for p, ql in zip(prefix, q_lens)], hq, hkv)
+        work = torch.from_numpy(w.copy()).to(dev)
+    out = continuation_attention(q, kp, vp, qo, kl, tb, max(q_lens), scale, work=work)
     torch.cuda.synchronize()
     ref = ref_attention(q, kp, vp, qo.cpu(), kl.cpu(), tb, scale)
     err = (out.float() - ref).abs().max().item()
