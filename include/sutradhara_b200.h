@@ -175,7 +175,8 @@ int sb_kv_insert_batch(sb_kv_cache* cache, const uint64_t* d_tokens,
                        const int64_t* h_block_offsets, const uint64_t* d_block_hashes,
                        int32_t n_seqs, int64_t now, int32_t* d_out_ids, int32_t* d_status,
                        void* stream);
-/* Batched release of d_ids[0..n). */
+/* Batched release of d_ids[0..n) (all-or-nothing like release(); negative
+ * ids — the outputs of failed inserts — are skipped). */
 int sb_kv_release_batch(sb_kv_cache* cache, const int32_t* d_ids, int64_t n, int32_t* d_status,
                         void* stream);
 /* Counters for the cross-GPU statistics reduction: [lookups, hit_tokens,

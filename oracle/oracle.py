@@ -317,6 +317,7 @@ def kvlog_lib():
             L.kvlog_take.restype = C.c_int64
             L.kvlog_take.argtypes = [C.c_char_p, C.c_int64]
             L.kvlog_enable.argtypes = [C.c_int]
+            L.refrun_last_error.restype = C.c_char_p
             L.refrun_generate_and_run.argtypes = [C.c_char_p, C.POINTER(C.c_double), C.c_int32, C.c_uint64,
                                                   C.c_int32, C.c_int64, C.c_int64, I64P, I64P, I64P, I64P,
                                                   U64P, C.POINTER(C.c_double)]
@@ -426,7 +427,7 @@ def ref_run_trace(n_requests: int, seed: int, preset: int, capacity: int, block_
                                    capacity, block_size, _i64(ftr), _i64(e2e), _i64(hit), _i64(prm),
                                    C.byref(ev), C.byref(wall))
     if st:
-        raise RuntimeError("reference run failed")
+        raise RuntimeError("reference run failed: " + L.refrun_last_error().decode(errors="replace"))
     res = (ftr, e2e, hit, prm, int(ev.value), float(wall.value))
     if kvlog:
         res = res + (_drain_kvlog(L),)

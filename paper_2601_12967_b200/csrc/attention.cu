@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int pg = 0; pg < 8; ++pg) {
           const int jb = j * 8 + pg;
-          const int row = (jb * 16 < kv_limit) ? (trow[jb] * p.n_kv_heads + kvh) * 16 : p.oob_row;
+          const int page = (jb * 16 < kv_limit) ? trow[jb] : -1;  // -1: no page (failed insert)
+          const int row = page >= 0 ? (page * p.n_kv_heads + kvh) * 16 : p.oob_row;
 #pragma unroll
           for (int a = 0; a < 2; ++a) tma_load_2d(dst + a * kAtomBytes + pg * 2048, tm, &ss.kv_full[stage], a * 64, row);
         }
@@ -357,6 +358,7 @@ __global__ void k_kv_append(const __nv_bfloat16* __restrict__ k_new, const __nv_
     const int s = lo;
     const int64_t pos = kv_len[s] - (q_off[s + 1] - q_off[s]) + (tok - q_off[s]);
     const int64_t blk = table[static_cast<int64_t>(s) * max_blocks + pos / page];
+    if (blk < 0) continue;  // sequence without pages (its insert failed)
     const int64_t dst = ((blk * n_kv_heads + kvh) * page + pos % page) * 128 + chunk * 8;
     const int64_t src = (tok * n_kv_heads + kvh) * 128 + chunk * 8;
     *reinterpret_cast<uint4*>(k_pool + dst) = __ldg(reinterpret_cast<const uint4*>(k_new + src));

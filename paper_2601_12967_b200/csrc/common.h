@@ -29,6 +29,9 @@ void set_last_error(const std::string& msg);
 // Wraps a C-ABI body: converts exceptions into status codes + last error.
 template <class F>
 int guard(F&& f) {
+  // errors recorded by earlier runtime calls of other components are not ours
+  // to report (a sticky device fault still resurfaces on our own calls)
+  (void)cudaGetLastError();
   try {
     return f();
   } catch (const Error& e) {

@@ -647,6 +647,8 @@ __global__ void k_commit_apply(Pool P, Scratch S, InsertArgs A, int s) {
       P.ctr[C_FULL] += 1ull;
     }
   }
+  if (status != 0)
+    for (int64_t p = gid; p < P_; p += stride) A.out_ids[b0 + p] = -1;
   if (status == SB_ERR_CACHE) return;
   const int64_t limit = status == 0 ? P_ : S.scal[S_FAILPOS];
   const int64_t n = A.seq_off[s + 1] - A.seq_off[s];
@@ -684,10 +686,12 @@ __global__ void k_commit_apply(Pool P, Scratch S, InsertArgs A, int s) {
 // --------------------------------------------------------- small ops
 // First failing index of a release (kv_cache.cpp:561-569): UnknownBlock /
 // ZeroRefRelease, checked in id order; apply only if none.
-__global__ void k_validate_ids(Pool P, const int32_t* ids, int64_t n, int check_ref, int64_t* scal) {
+__global__ void k_validate_ids(Pool P, const int32_t* ids, int64_t n, int check_ref, int64_t* scal,
+                               int skip_negative = 0) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int32_t id = ids[i];
+    if (skip_negative && id < 0) continue;
     const bool known = id >= 0 && id < P.cap && P.ntok[id] > 0;
     if (!known || (check_ref && P.ref[id] < 1))
       atomicMin(reinterpret_cast<unsigned long long*>(&scal[S_ERRIDX]), (unsigned long long)i);
@@ -697,7 +701,7 @@ __global__ void k_release_apply(Pool P, const int32_t* ids, int64_t n, const int
   if (scal[S_ERRIDX] < n) return;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    atomicSub(&P.ref[ids[i]], 1);
+    if (ids[i] >= 0) atomicSub(&P.ref[ids[i]], 1);
 }
 __global__ void k_touch_apply(Pool P, const int32_t* ids, int64_t n, int64_t now, const int64_t* scal) {
   const int64_t lim = min(n, scal[S_ERRIDX]);
@@ -803,8 +807,9 @@ struct sb_kv_cache {
 
   ~sb_kv_cache() {
     cudaSetDevice(device);
+    // S.prehit aliases d_prehit_all: freed once below
     void* ptrs[] = {P.tok, P.ntok, P.chain, P.parent, P.tag, P.ref, P.pinned, P.last, P.tkey, P.tval, P.slot, P.ctr,
-                    S.hashes, S.prehit, S.chain_out, S.kind, S.freel, S.evicted, S.victims, S.taken, S.rank_of, S.keys,
+                    S.hashes, S.chain_out, S.kind, S.freel, S.evicted, S.victims, S.taken, S.rank_of, S.keys,
                     S.sortbuf, S.scal, S.late, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first};
     for (void* p : ptrs)
       if (p) cudaFree(p);
@@ -1220,7 +1225,7 @@ int sb_kv_release_batch(sb_kv_cache* c, const int32_t* d_ids, int64_t n, int32_t
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
     k_set_scal<<<1, 1, 0, st>>>(c->S.scal, S_ERRIDX, INT64_MAX);
     if (n > 0) {
-      k_validate_ids<<<grid_for(n), 256, 0, st>>>(c->P, d_ids, n, 1, c->S.scal);
+      k_validate_ids<<<grid_for(n), 256, 0, st>>>(c->P, d_ids, n, 1, c->S.scal, 1);
       k_release_apply<<<grid_for(n), 256, 0, st>>>(c->P, d_ids, n, c->S.scal);
     }
     SB_CHECK_LAUNCH();
