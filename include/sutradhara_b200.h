@@ -150,6 +150,9 @@ int sb_kv_audit(const sb_kv_cache* cache);
 int sb_kv_dump(const sb_kv_cache* cache, char* buf, int64_t cap, int64_t* len);
 
 /* ---- batched, stream-ordered engine path (no host round trip) --------- */
+/* `stream` is used literally (NULL = the legacy default stream); the per-op
+ * calls above run on the pool's own stream and synchronise before
+ * returning. */
 /* Batched lookup_prefix: sequence s is d_tokens[d_seq_offsets[s]..[s+1]);
  * d_hit_tokens[s] receives its hit length.  Touch semantics are identical to
  * calling lookup_prefix for each sequence at the same `now`.  Optional

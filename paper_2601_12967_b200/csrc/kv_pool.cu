@@ -965,7 +965,8 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
     auto* c = new sb_kv_cache();
     try {
       c->device = device;
-      SB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      // blocking stream: per-op calls order after outstanding work on the legacy stream
+      SB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamDefault));
       Pool& P = c->P;
       P.bs = block_size;
       P.cap = capacity_blocks;
@@ -1056,7 +1057,7 @@ int sb_kv_lookup_prefix_batch(sb_kv_cache* c, const uint64_t* d_tokens, const in
     SB_CUDA(cudaSetDevice(c->device));
     if (n_seqs <= 0) return int(SB_OK);
     if (now < -kLastBias || now >= kLastBias) throw Error(SB_ERR_UNSUPPORTED, "now outside +-2^39");
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
     std::vector<int64_t> off(n_seqs + 1), blk(n_seqs + 1);
     const bool pre = d_block_hashes && d_block_offsets;
     if (pre && h_block_offsets) {
@@ -1143,8 +1144,9 @@ int sb_kv_insert_batch(sb_kv_cache* c, const uint64_t* d_tokens, const int64_t* 
       std::memcpy(hb.data(), h_block_offsets, sizeof(int64_t) * (n_seqs + 1));
     else
       SB_CUDA(cudaMemcpy(hb.data(), d_block_offsets, sizeof(int64_t) * (n_seqs + 1), cudaMemcpyDeviceToHost));
+    // the caller's stream, taken literally (NULL = legacy default stream)
     cudaStream_t saved = c->stream;
-    if (stream) c->stream = static_cast<cudaStream_t>(stream);
+    c->stream = static_cast<cudaStream_t>(stream);
     try {
       c->insert_device(d_tokens, d_seq_offsets, d_tags, d_tag_offsets, d_block_offsets, d_block_hashes, n_seqs, now,
                        d_out_ids, d_status, hb);
@@ -1222,7 +1224,7 @@ int sb_kv_release_batch(sb_kv_cache* c, const int32_t* d_ids, int64_t n, int32_t
   return guard([&] {
     std::lock_guard<std::mutex> lk(c->mu);
     SB_CUDA(cudaSetDevice(c->device));
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
     k_set_scal<<<1, 1, 0, st>>>(c->S.scal, S_ERRIDX, INT64_MAX);
     if (n > 0) {
       k_validate_ids<<<grid_for(n), 256, 0, st>>>(c->P, d_ids, n, 1, c->S.scal, 1);

@@ -30,6 +30,8 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
+import os
+
 from . import _lib
 from .kv_cache import PARTIAL_PREFILL, TIERED, TOOL_OUTPUT, CacheConfig, KvCache
 
@@ -45,6 +47,8 @@ class ModelShape:
     def kv_bytes_per_token(self) -> int:  # K + V, all layers, bf16
         return 2 * self.n_layers * self.n_kv_heads * self.head_dim * 2
 
+
+_DEBUG = os.environ.get("SB_DEBUG", "0") == "1"
 
 LLAMA3_8B = ModelShape(32, 32, 8, 128)
 TOY_2L_256 = ModelShape(2, 2, 1, 128)  # configs[0]: 2 layers, d_model = 2 x 128
@@ -215,6 +219,16 @@ class ContinuationBatch:
         launches += 5 * self.n
         _lib.check(L.sb_build_block_table(_p(self.ids), _p(self.blk_off), self.n, self.max_blocks, _p(self.table), st))
         launches += 1
+        if _DEBUG:
+            torch.cuda.synchronize()
+            tb = self.table.cpu().numpy()
+            bad = np.argwhere((tb < -1) | (tb >= eng.capacity))
+            assert len(bad) == 0, f"block table out of range at {bad[:5].tolist()}: {tb[tuple(bad[0])]}"
+            stt = self.status.cpu().numpy()
+            for i in range(self.n):
+                nb = int(self.blk_off_h[i + 1] - self.blk_off_h[i])
+                row = tb[i, :nb]
+                assert (row >= 0).all() if stt[i] == 0 else (row == -1).all(), (i, stt[i], row[:8])
         # 4. per layer: projections (random-init stand-in), KV append, attention
         sh = eng.shape
         for li in range(sh.n_layers):
