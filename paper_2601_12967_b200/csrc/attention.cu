@@ -82,6 +82,36 @@ __device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, 
   asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pa), "l"(pb), "l"(pc));
   asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(r));
 }
+// 2^x for a pair on the FMA/ALU pipes (offloads MUFU): x = r + f with
+// r = rint(x) (magic-number rounding), 2^f by a degree-3 minimax polynomial on
+// [-0.5, 0.5] (max rel. error 7.5e-5, below bf16 rounding of P), and r added
+// to the exponent field.  x is clamped to >= -120 (masked -inf -> ~1e-36).
+__device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& y1) {
+  constexpr float kMagic = 12582912.f;  // 1.5 * 2^23
+  x0 = fmaxf(x0, -120.f);  // keeps the result's exponent field normal
+  x1 = fmaxf(x1, -120.f);
+  uint64_t px, pm, pt, pr, pf, pc, pp;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(px) : "f"(x0), "f"(x1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(pm) : "f"(kMagic));
+  asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(pt) : "l"(px), "l"(pm));  // t = x + M
+  asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(pr) : "l"(pt), "l"(pm));  // r = t - M
+  asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(pf) : "l"(px), "l"(pr));  // f = x - r
+  asm("mov.b64 %0, {%1, %1};" : "=l"(pc) : "f"(0.055170975625514984f));
+  uint64_t c2, c1, c0;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(c2) : "f"(0.24260970950126648f));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(c1) : "f"(0.6932609677314758f));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(c0) : "f"(0.9999281764030457f));
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pc), "l"(pf), "l"(c2));
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(pf), "l"(c1));
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(pp) : "l"(pp), "l"(pf), "l"(c0));
+  float q0, q1, t0, t1;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(q0), "=f"(q1) : "l"(pp));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(t0), "=f"(t1) : "l"(pt));
+  // exponent add: the integer r sits in the low mantissa bits of t
+  y0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23));
+  y1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
+}
+
 __device__ __forceinline__ void fadd2(float& a0, float& a1, float b0, float b1) {
   uint64_t r, pa, pb;
   asm("mov.b64 %0, {%1, %2};" : "=l"(pa) : "f"(a0), "f"(a1));
@@ -290,7 +320,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < 16; ++k) {
           float a0, a1;
           ffma2(a0, a1, s[32 * c + 2 * k], s[32 * c + 2 * k + 1], p.scale_log2, neg_m);
-          const float e0 = ex2(a0), e1 = ex2(a1);
+          float e0, e1;
+          if ((k & 3) == 3) {  // a quarter of the pairs on the FMA pipes
+            ex2_poly2(a0, a1, e0, e1);
+          } else {
+            e0 = ex2(a0);
+            e1 = ex2(a1);
+          }
           fadd2(acc[2 * (k & 3)], acc[2 * (k & 3) + 1], e0, e1);
           w[k] = pack_bf16x2(e0, e1);
         }
