@@ -44,6 +44,7 @@ constexpr uint64_t kIdMask = (uint64_t(1) << kIdBits) - 1;
 constexpr uint64_t kNoKey = ~uint64_t(0);
 constexpr int kSelectThreads = 1024;
 constexpr int kSortSmemKeys = 8192;
+constexpr int kCandSmem = 16384;  // candidate keys staged in shared memory (128 KB)
 
 enum Ctr { C_NRES = 0, C_EVICTED, C_LOOKUPS, C_HIT_TOK, C_LOOK_TOK, C_INS_BLOCKS, C_EV_BLOCKS, C_FULL, C_N };
 enum Scal { S_F = 0, S_K, S_FREE, S_NEV, S_STATUS, S_FAILPOS, S_NNEW, S_NCAND, S_ERRIDX, S_NLATE, S_N };
@@ -325,22 +326,30 @@ struct InsertArgs {
 };
 
 // mode 0: plan one insert (sequence s).  mode 1: evict(needed) — K = needed.
-// Computes victim keys of all candidate blocks, radix-selects the K smallest,
-// sorts them, records their ranks, and lists the lowest free ids.
+// Hint-aware eviction scoring: the key (tier, last_used, id) of every
+// candidate block (resident, unpinned, ref 0, not referenced before the first
+// miss of this insert) is compacted into shared memory, the K smallest are
+// radix-selected there (11-bit digits from the top, early exit once the
+// boundary bin is exactly consumed), sorted, and published with their ranks.
+// The lowest free ids are listed as well.  Pools whose candidate set exceeds
+// the shared-memory budget run the same passes over global memory.
 __global__ void __launch_bounds__(kSelectThreads, 1)
     k_select(Pool P, Scratch S, InsertArgs A, int s, int mode, int64_t needed) {
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t warp_sums[33];
   __shared__ int64_t sh[8];
-  extern __shared__ uint64_t sel[];  // kSortSmemKeys
+  __shared__ uint32_t cnt_b;
+  __shared__ unsigned long long n_cand, n_hc;
+  extern __shared__ uint64_t dyn[];  // [kCandSmem] candidates | [kSortSmemKeys] selection
+  uint64_t* cand_s = dyn;
+  uint64_t* sel_s = dyn + kCandSmem;
   const int t = threadIdx.x;
-  int64_t P_, f = 0, K = 0, Fp = 0;
+  int64_t P_ = 0, f = 0, b0 = 0;
   if (mode == 0) {
-    const int64_t b0 = A.blk_off[s];
+    b0 = A.blk_off[s];
     P_ = A.blk_off[s + 1] - b0;
     const int64_t n = A.seq_off[s + 1] - A.seq_off[s];
     const bool ok = tags_cover(A.tags + A.tag_off[s], A.tag_off[s + 1] - A.tag_off[s], n);
-    // first pre-miss position
     if (t == 0) sh[0] = P_;
     __syncthreads();
     for (int64_t p = t; p < P_; p += blockDim.x)
@@ -356,31 +365,22 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
       }
       return;
     }
-  } else {
-    P_ = 0;
-  }
-  // candidate keys; blocks hit before the first miss are referenced before
-  // any eviction can happen and are excluded.
-  if (t == 0) {
-    sh[1] = 0;  // candidates
-    sh[2] = 0;  // pre-hit candidates at positions >= f
-  }
-  __syncthreads();
-  uint32_t my_cand = 0;
-  for (int64_t i = t; i < P.cap; i += blockDim.x) {
-    const bool c = is_candidate(P, static_cast<int32_t>(i));
-    S.keys[i] = c ? victim_key(P, static_cast<int32_t>(i)) : kNoKey;
-    my_cand += c;
-  }
-  __syncthreads();
-  uint32_t my_hc = 0, my_excl = 0;
-  if (mode == 0) {
-    const int64_t b0 = A.blk_off[s];
     if (t == 0) S.scal[S_NLATE] = 0;
-    __syncthreads();
+    // blocks referenced before the first miss cannot be evicted by this insert
+    for (int64_t p = t; p < f; p += blockDim.x) {
+      const int32_t id = S.prehit[b0 + p];
+      S.kind[p] = 0;
+      S.rank_of[id] = -2;  // temporary exclusion mark (rank_of is -1 elsewhere)
+    }
+  }
+  if (t == 0) {
+    n_cand = 0;
+    n_hc = 0;
+  }
+  __syncthreads();
+  if (mode == 0) {
     for (int64_t p = t; p < P_; p += blockDim.x) {
       const int32_t id = S.prehit[b0 + p];
-      if (p < f) S.kind[p] = 0;
       if (id < 0) continue;
       if (p < f && P.ref[id] == -1 && P.pinned[id] == 0) {
         const int64_t at = atomicAdd(reinterpret_cast<unsigned long long*>(&S.scal[S_NLATE]), 1ull);
@@ -388,83 +388,83 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
           S.late[2 * at] = static_cast<int32_t>(p);
           S.late[2 * at + 1] = id;
         }
-      }
-      if (p < f) {
-        if (S.keys[id] != kNoKey) {
-          // several positions could name the same block only via hash cycles; tolerate
-          if (atomicExch(reinterpret_cast<unsigned long long*>(&S.keys[id]), (unsigned long long)kNoKey) != kNoKey)
-            ++my_excl;
-        }
-      } else if (is_candidate(P, id)) {
-        ++my_hc;
+      } else if (p >= f && is_candidate(P, id)) {
+        atomicAdd(&n_hc, 1ull);
       }
     }
   }
-  atomicAdd(reinterpret_cast<unsigned long long*>(&sh[1]), (unsigned long long)my_cand);
-  atomicAdd(reinterpret_cast<unsigned long long*>(&sh[2]), (unsigned long long)my_hc);
-  __shared__ unsigned long long excl_total;
-  if (t == 0) excl_total = 0;
+  // ---- score every block, compact the candidates
+  // (first into shared memory; overflow keeps going into global S.keys)
+  for (int64_t i = t; i < P.cap; i += blockDim.x) {
+    const int32_t id = static_cast<int32_t>(i);
+    if (!is_candidate(P, id) || S.rank_of[id] == -2) continue;
+    const unsigned long long at = atomicAdd(&n_cand, 1ull);
+    const uint64_t k = victim_key(P, id);
+    if (at < kCandSmem) cand_s[at] = k; else S.keys[at - kCandSmem] = k;
+  }
   __syncthreads();
-  atomicAdd(&excl_total, (unsigned long long)my_excl);
-  __syncthreads();
-  const int64_t ncand = sh[1] - static_cast<int64_t>(excl_total);
+  if (mode == 0)
+    for (int64_t p = t; p < f; p += blockDim.x) S.rank_of[S.prehit[b0 + p]] = -1;
+  const int64_t ncand = static_cast<int64_t>(n_cand);
   const int64_t nres = static_cast<int64_t>(P.ctr[C_NRES]);
   const int64_t free_cnt = P.cap - nres;
+  int64_t K, Fp = 0;
   if (mode == 0) {
     const int64_t rest = P_ - f;
     Fp = min(free_cnt, rest);
-    K = min(ncand, (rest > free_cnt ? rest - free_cnt : int64_t(0)) + sh[2]);
+    K = min(ncand, (rest > free_cnt ? rest - free_cnt : int64_t(0)) + static_cast<int64_t>(n_hc));
   } else {
     K = min(ncand, needed);
   }
-  // ---- radix select of the K smallest keys (keys are unique) ----
-  uint64_t prefix = 0, mask = 0;
+  auto key_at = [&](int64_t i) -> uint64_t { return i < kCandSmem ? cand_s[i] : S.keys[i - kCandSmem]; };
+  // ---- radix select of the K smallest keys (keys are unique)
   if (K > 0) {
-    int64_t need = K;
-    const int shifts[6] = {53, 42, 31, 20, 10, 0};
-    const int widths[6] = {11, 11, 11, 11, 10, 10};
-    for (int pass = 0; pass < 6; ++pass) {
-      const int sh_ = shifts[pass], wd = widths[pass];
-      const uint64_t bmask = (uint64_t(1) << wd) - 1;
-      for (int i = t; i < 2048; i += blockDim.x) hist[i] = 0;
-      __syncthreads();
-      for (int64_t i = t; i < P.cap; i += blockDim.x) {
-        const uint64_t k = S.keys[i];
-        if (k != kNoKey && (k & mask) == prefix) atomicAdd(&hist[(k >> sh_) & bmask], 1u);
+    uint64_t prefix = 0, mask = 0;
+    if (K < ncand) {
+      int64_t need = K;
+      const int shifts[6] = {53, 42, 31, 20, 10, 0};
+      const int widths[6] = {11, 11, 11, 11, 10, 10};
+      for (int pass = 0; pass < 6; ++pass) {
+        const int sh_ = shifts[pass], wd = widths[pass];
+        const uint64_t bmask = (uint64_t(1) << wd) - 1;
+        hist[2 * t] = 0;
+        hist[2 * t + 1] = 0;
+        __syncthreads();
+        for (int64_t i = t; i < ncand; i += blockDim.x) {
+          const uint64_t k = key_at(i);
+          if ((k & mask) == prefix) atomicAdd(&hist[(k >> sh_) & bmask], 1u);
+        }
+        __syncthreads();
+        const uint32_t a0 = hist[2 * t], a1 = hist[2 * t + 1];
+        block_scan_2048(hist, warp_sums);
+        const uint32_t e0 = hist[2 * t], e1 = hist[2 * t + 1];
+        if (e0 < need && need <= e0 + a0) {
+          sh[4] = 2 * t;
+          sh[5] = e0;
+          cnt_b = a0;
+        }
+        if (e1 < need && need <= e1 + a1) {
+          sh[4] = 2 * t + 1;
+          sh[5] = e1;
+          cnt_b = a1;
+        }
+        __syncthreads();
+        need -= sh[5];
+        prefix |= static_cast<uint64_t>(sh[4]) << sh_;
+        mask |= bmask << sh_;
+        const bool done = (static_cast<int64_t>(cnt_b) == need);
+        __syncthreads();
+        if (done) break;
       }
-      __syncthreads();
-      // locate the bin holding the need-th smallest
-      __shared__ uint32_t cnt_b;
-      uint32_t a0 = hist[2 * t], a1 = hist[2 * t + 1];
-      block_scan_2048(hist, warp_sums);
-      const uint32_t e0 = hist[2 * t], e1 = hist[2 * t + 1];
-      if (e0 < need && need <= e0 + a0) {
-        sh[4] = 2 * t;
-        sh[5] = e0;
-        cnt_b = a0;
-      }
-      if (e1 < need && need <= e1 + a1) {
-        sh[4] = 2 * t + 1;
-        sh[5] = e1;
-        cnt_b = a1;
-      }
-      __syncthreads();
-      const uint64_t bin = static_cast<uint64_t>(sh[4]);
-      need -= sh[5];
-      prefix |= bin << sh_;
-      mask |= bmask << sh_;
-      const bool done = (static_cast<int64_t>(cnt_b) == need);
-      __syncthreads();
-      if (done) break;
     }
-    // gather all keys whose masked prefix is <= prefix: exactly K of them
+    // gather the selected keys: exactly K of them
     if (t == 0) sh[6] = 0;
     __syncthreads();
     const bool in_smem = K <= kSortSmemKeys;
-    uint64_t* dst = in_smem ? sel : S.sortbuf;
-    for (int64_t i = t; i < P.cap; i += blockDim.x) {
-      const uint64_t k = S.keys[i];
-      if (k != kNoKey && (k & mask) <= prefix) {
+    uint64_t* dst = in_smem ? sel_s : S.sortbuf;
+    for (int64_t i = t; i < ncand; i += blockDim.x) {
+      const uint64_t k = key_at(i);
+      if (K == ncand || (k & mask) <= prefix) {
         const int64_t at = atomicAdd(reinterpret_cast<unsigned long long*>(&sh[6]), 1ull);
         dst[at] = k;
       }
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
       S.rank_of[k & kIdMask] = static_cast<int32_t>(r);
     }
   }
-  // ---- lowest Fp free ids, ascending (std::set<int32_t> order) ----
+  // ---- lowest Fp free ids, ascending (std::set<int32_t> order)
   if (Fp > 0) {
     __shared__ uint32_t wcnt[33];
     __shared__ int64_t found;
@@ -526,17 +526,32 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
 // Sequential decisions of one insert (kv_cache.cpp:471-506), from the first
 // pre-miss position on.  Single thread: each step is a handful of
 // L1/L2-resident accesses.
-__global__ void k_walk(Pool P, Scratch S, InsertArgs A, int s) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+constexpr int kWalkSmemVictims = 4096;
+
+__global__ void __launch_bounds__(32, 1) k_walk(Pool P, Scratch S, InsertArgs A, int s) {
+  __shared__ uint64_t vic_s[kWalkSmemVictims];
+  __shared__ uint8_t taken_s[kWalkSmemVictims];
+  __shared__ int32_t pb[32], pr[32];
+  __shared__ uint8_t pl[32];
+  const int lane = threadIdx.x;
   if (S.scal[S_STATUS] != 0) {
-    S.scal[S_NEV] = 0;
-    S.scal[S_NNEW] = 0;
-    S.scal[S_FAILPOS] = -1;
+    if (lane == 0) {
+      S.scal[S_NEV] = 0;
+      S.scal[S_NNEW] = 0;
+      S.scal[S_FAILPOS] = -1;
+    }
     return;
   }
   const int64_t b0 = A.blk_off[s];
   const int64_t P_ = A.blk_off[s + 1] - b0;
   const int64_t f = S.scal[S_F], K = S.scal[S_K], Fp = S.scal[S_FREE];
+  const bool vs = K <= kWalkSmemVictims;
+  if (vs)
+    for (int64_t r = lane; r < K; r += 32) {
+      vic_s[r] = S.victims[r];
+      taken_s[r] = 0;
+    }
+  uint8_t* taken = vs ? taken_s : S.taken;
   const uint64_t now_bits = static_cast<uint64_t>(A.now + kLastBias) << kIdBits;
   // late candidates: blocks that a hit in this insert raised from ref -1 to 0
   uint64_t lkey[kLateMax];
@@ -547,65 +562,92 @@ __global__ void k_walk(Pool P, Scratch S, InsertArgs A, int s) {
     if (P.policy == SB_POLICY_TIERED) k |= static_cast<uint64_t>(tier_of(P.tag[id])) << 61;
     return k;
   };
-  const int64_t n_pre_late = S.scal[S_NLATE] < kLateMax ? S.scal[S_NLATE] : int64_t(kLateMax);
-  for (int64_t i = 0; i < n_pre_late; ++i) {
-    lpos[nl] = S.late[2 * i];
-    lkey[nl++] = late_key(S.late[2 * i + 1]);
+  if (lane == 0) {
+    const int64_t n_pre_late = S.scal[S_NLATE] < kLateMax ? S.scal[S_NLATE] : int64_t(kLateMax);
+    for (int64_t i = 0; i < n_pre_late; ++i) {
+      lpos[nl] = S.late[2 * i];
+      lkey[nl++] = late_key(S.late[2 * i + 1]);
+    }
   }
+  __syncwarp();
   int64_t ptr = 0, fi = 0, nev = 0, nnew = 0, failpos = -1;
   int status = 0;
-  for (int64_t p = f; p < P_; ++p) {
-    const int32_t b = S.prehit[b0 + p];
-    bool miss = b < 0;
-    if (!miss) {
-      const int32_t r = S.rank_of[b];
-      if (r >= 0) {
-        if (r < ptr && !S.taken[r]) miss = true;  // evicted earlier in this insert
-        else S.taken[r] = 1;                       // referenced: no longer a candidate
+  for (int64_t p0 = f; p0 < P_ && status == 0; p0 += 32) {
+    // the warp prefetches 32 positions' pre-state probe results
+    const int64_t p = p0 + lane;
+    int32_t b = -1, r = -1;
+    uint8_t late = 0;
+    if (p < P_) {
+      b = S.prehit[b0 + p];
+      if (b >= 0) {
+        r = S.rank_of[b];
+        late = P.ref[b] == -1 && P.pinned[b] == 0;
       }
     }
-    if (!miss) {
-      S.chain_out[p] = b;
-      S.kind[p] = 0;
-      if (P.ref[b] == -1 && P.pinned[b] == 0 && nl < kLateMax) {
-        lpos[nl] = static_cast<int32_t>(p);
-        lkey[nl++] = late_key(b);
+    pb[lane] = b;
+    pr[lane] = r;
+    pl[lane] = late;
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t n = (P_ - p0) < 32 ? (P_ - p0) : int64_t(32);
+      for (int64_t i = 0; i < n; ++i) {
+        const int64_t q = p0 + i;
+        const int32_t bb = pb[i], rr = pr[i];
+        bool miss = bb < 0;
+        if (!miss && rr >= 0) {
+          if (rr < ptr && !taken[rr]) miss = true;  // evicted earlier in this insert
+          else taken[rr] = 1;                        // referenced: no longer a candidate
+        }
+        if (!miss) {
+          S.chain_out[q] = bb;
+          S.kind[q] = 0;
+          if (pl[i] && nl < kLateMax) {
+            lpos[nl] = static_cast<int32_t>(q);
+            lkey[nl++] = late_key(bb);
+          }
+          continue;
+        }
+        int32_t id;
+        if (fi < Fp) {
+          id = S.freel[fi++];
+        } else {
+          while (ptr < K && taken[ptr]) ++ptr;
+          int li = -1;
+          for (int k = 0; k < nl; ++k)
+            if (li < 0 || lkey[k] < lkey[li]) li = k;
+          const uint64_t vk = ptr < K ? (vs ? vic_s[ptr] : S.victims[ptr]) : kNoKey;
+          const bool use_list = ptr < K && (li < 0 || vk < lkey[li]);
+          if (!use_list && li < 0) {
+            status = SB_ERR_CACHE_FULL;
+            failpos = q;
+            break;
+          }
+          if (use_list) {
+            id = static_cast<int32_t>(vk & kIdMask);
+            ++ptr;
+          } else {
+            id = static_cast<int32_t>(lkey[li] & kIdMask);
+            S.kind[lpos[li]] = 2;  // hit, then evicted later in this insert
+            lkey[li] = lkey[nl - 1];
+            lpos[li] = lpos[nl - 1];
+            --nl;
+          }
+          S.evicted[nev++] = id;
+        }
+        S.chain_out[q] = id;
+        S.kind[q] = 1;
+        ++nnew;
       }
-      continue;
     }
-    int32_t id;
-    if (fi < Fp) {
-      id = S.freel[fi++];
-    } else {
-      while (ptr < K && S.taken[ptr]) ++ptr;
-      int li = -1;
-      for (int i = 0; i < nl; ++i)
-        if (li < 0 || lkey[i] < lkey[li]) li = i;
-      const bool use_list = ptr < K && (li < 0 || S.victims[ptr] < lkey[li]);
-      if (!use_list && li < 0) {
-        status = SB_ERR_CACHE_FULL;
-        failpos = p;
-        break;
-      }
-      if (use_list) {
-        id = static_cast<int32_t>(S.victims[ptr++] & kIdMask);
-      } else {
-        id = static_cast<int32_t>(lkey[li] & kIdMask);
-        S.kind[lpos[li]] = 2;  // hit, then evicted later in this insert
-        lkey[li] = lkey[nl - 1];
-        lpos[li] = lpos[nl - 1];
-        --nl;
-      }
-      S.evicted[nev++] = id;
-    }
-    S.chain_out[p] = id;
-    S.kind[p] = 1;
-    ++nnew;
+    status = __shfl_sync(0xffffffffu, status, 0);
+    __syncwarp();
   }
-  S.scal[S_NEV] = nev;
-  S.scal[S_NNEW] = nnew;
-  S.scal[S_FAILPOS] = failpos;
-  S.scal[S_STATUS] = status;
+  if (lane == 0) {
+    S.scal[S_NEV] = nev;
+    S.scal[S_NNEW] = nnew;
+    S.scal[S_FAILPOS] = failpos;
+    S.scal[S_STATUS] = status;
+  }
 }
 
 __global__ void k_commit_evict(Pool P, Scratch S) {
@@ -892,7 +934,7 @@ struct sb_kv_cache {
     return v;
   }
 
-  size_t select_smem() const { return kSortSmemKeys * sizeof(uint64_t); }
+  size_t select_smem() const { return (kCandSmem + kSortSmemKeys) * sizeof(uint64_t); }
 
   // Inserts sequences [0, n_seqs) described by device arrays, sequentially.
   void insert_device(const uint64_t* tokens, const int64_t* seq_off, const sb_tag_range* tags, const int64_t* tag_off,
