@@ -1,0 +1,131 @@
+"""Roofline micro-benchmarks of the block-pool kernels (HBM side of the hot
+path): chain hashing, batched prefix lookup, hint-aware eviction scoring and
+the KV append, each timed with CUDA events on its stream and reported as
+algorithmic GB/s against the measured HBM copy bandwidth.
+
+    python bench_kv.py            # one JSON line per kernel/config
+
+Algorithmic bytes per unit:
+  chain hash     8 B read per token + 8 B written per block
+  lookup         per full block position: 128 B query tokens + 128 B stored
+                 tokens + 20 B block metadata + 12 B index slot
+  evict scoring  per pool block: ntok/ref/pinned/tag (16 B) + last (8 B)
+  kv append      per token and layer: 2 x H_kv x 128 x 2 B read + same written
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return json.load(open(p)) if os.path.exists(p) else {"hbm_gbs": 6650.0}
+
+
+def timed(fn, reps=10, warm=3):
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
+        a.record()
+        fn()
+        b.record()
+    torch.cuda.synchronize()
+    return float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e-3
+
+
+def emit(kernel, config, bytes_, sec, hbm):
+    gbs = bytes_ / sec / 1e9
+    print(json.dumps({"kernel": kernel, "config": config, "seconds": sec, "algorithmic_bytes": bytes_,
+                      "achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm}), flush=True)
+
+
+def main():
+    import torch
+    from paper_2601_12967_b200 import _lib
+    from paper_2601_12967_b200.kv_cache import CacheConfig, KvCache
+
+    L = _lib.lib()
+    hbm = float(peaks()["hbm_gbs"])
+    dev = torch.device("cuda")
+    p = lambda t: C.c_void_p(t.data_ptr())
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    # ---- chain hashing: latency-bound per sequence, throughput over sequences
+    for n_seqs, toks in ((64, 8192), (4096, 1024), (65536, 512)):
+        n = n_seqs * toks
+        tokens = torch.randint(0, 2**62, (n,), dtype=torch.int64, device=dev)
+        seq_off = torch.arange(0, n + 1, toks, dtype=torch.int64, device=dev)
+        blk_off = torch.arange(0, n // 16 + 1, toks // 16, dtype=torch.int64, device=dev)
+        out = torch.empty(n // 16, dtype=torch.int64, device=dev)
+        sec = timed(lambda: L.sb_chain_hash_batch(p(tokens), p(seq_off), p(blk_off), None, n_seqs, 16, p(out), st))
+        emit("k_chain_hash", f"{n_seqs} seqs x {toks} tokens", 8 * n + 8 * (n // 16), sec, hbm)
+
+    # ---- batched lookup over a populated pool (all-hit prefixes)
+    cap = 1 << 20
+    cache = KvCache(CacheConfig(16, cap, 1))
+    n_seqs, toks = 1024, 8192
+    n = n_seqs * toks
+    host = np.random.default_rng(0).integers(0, 2**62, n, dtype=np.int64)
+    tokens = torch.from_numpy(host).to(dev)
+    seq_off = torch.arange(0, n + 1, toks, dtype=torch.int64, device=dev)
+    blk_off = torch.arange(0, n // 16 + 1, toks // 16, dtype=torch.int64, device=dev)
+    blk_off_h = np.arange(0, n // 16 + 1, toks // 16, dtype=np.int64)
+    tags = (_lib.TagRange * n_seqs)()
+    for i in range(n_seqs):
+        tags[i].begin, tags[i].end, tags[i].tag = 0, toks, 3
+    tag_dev = torch.frombuffer(bytearray(tags), dtype=torch.uint8).to(dev)
+    tag_off = torch.arange(n_seqs + 1, dtype=torch.int64, device=dev)
+    ids = torch.empty(n // 16, dtype=torch.int32, device=dev)
+    status = torch.empty(n_seqs, dtype=torch.int32, device=dev)
+    hashes = torch.empty(n // 16, dtype=torch.int64, device=dev)
+    L.sb_chain_hash_batch(p(tokens), p(seq_off), p(blk_off), None, n_seqs, 16, p(hashes), st)
+    _lib.check(L.sb_kv_insert_batch(cache.handle, p(tokens), p(seq_off), p(tag_dev), p(tag_off), p(blk_off),
+                                    blk_off_h.ctypes.data_as(_lib.I64P), p(hashes), n_seqs, 1, p(ids), p(status), st))
+    _lib.check(L.sb_kv_release_batch(cache.handle, p(ids), n // 16, None, st))
+    torch.cuda.synchronize()
+    hits = torch.empty(n_seqs, dtype=torch.int64, device=dev)
+    sec = timed(lambda: L.sb_kv_lookup_prefix_batch(cache.handle, p(tokens), p(seq_off), p(blk_off),
+                                                    blk_off_h.ctypes.data_as(_lib.I64P), p(hashes), n_seqs, 2,
+                                                    p(hits), st))
+    assert int(hits.sum()) == n
+    emit("k_probe_batch (+init/finish)", f"{n_seqs} seqs x {toks} tokens, pool {cap} blocks, all hit",
+         (n // 16) * (128 + 128 + 20 + 12), sec, hbm)
+
+    # ---- eviction scoring at pool scale: evict() = score + select + sort
+    for needed in (64, 4096):
+        def ev():
+            out = np.zeros(needed, dtype=np.int32)
+            k = C.c_int64(0)
+            L.sb_kv_evict(cache.handle, needed, out.ctypes.data_as(_lib.I32P), C.byref(k))
+        sec = timed(ev, reps=5, warm=1)
+        emit("k_select (evict)", f"pool {cap} blocks, {cache.resident_blocks()} resident, evict {needed}",
+             cap * 24, sec, hbm)
+
+    # ---- KV append (Llama-3-8B kv heads), one layer
+    tok_n, hkv, pages = 98896, 8, 27281
+    kp = torch.empty(pages, hkv, 16, 128, dtype=torch.bfloat16, device=dev)
+    vp = torch.empty_like(kp)
+    k_new = torch.randn(tok_n, hkv, 128, device=dev).to(torch.bfloat16)
+    v_new = torch.randn_like(k_new)
+    q_off = torch.tensor([0, tok_n], dtype=torch.int32, device=dev)
+    kv_len = torch.tensor([tok_n], dtype=torch.int32, device=dev)
+    table = torch.randperm(pages, device=dev)[: (tok_n + 15) // 16].to(torch.int32).reshape(1, -1).contiguous()
+    sec = timed(lambda: L.sb_kv_append(p(k_new), p(v_new), p(kp), p(vp), p(q_off), p(kv_len), p(table), 1,
+                                       table.shape[1], hkv, 128, 16, st))
+    emit("k_kv_append", f"{tok_n} tokens x {hkv} kv heads", 2 * 2 * tok_n * hkv * 128 * 2, sec, hbm)
+
+
+if __name__ == "__main__":
+    main()

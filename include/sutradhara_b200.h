@@ -238,6 +238,53 @@ int sb_build_block_table(const int32_t* d_ids, const int64_t* d_block_offsets, i
  * weights. */
 int sb_fill_random_bf16(void* d_out, int64_t n_elems, uint64_t seed, float amp, void* stream);
 
+/* ---- continuation engine (host C++): Engine prompt-splitting path ------ */
+typedef struct sb_engine sb_engine; /* pool + per-layer K/V page pools */
+typedef struct sb_batch sb_batch;   /* static layout of a batch of continuations */
+
+/* Model shape of the paged KV (head_dim 128), pool of capacity_blocks 16-token
+ * pages per layer; pages are filled with seeded random-init KV. */
+int sb_engine_create(int32_t n_layers, int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim,
+                     int64_t capacity_blocks, int32_t policy, int32_t device, uint64_t seed,
+                     sb_engine** out);
+void sb_engine_destroy(sb_engine* engine);
+sb_kv_cache* sb_engine_cache(sb_engine* engine);
+void* sb_engine_k_pool(sb_engine* engine, int32_t layer);
+void* sb_engine_v_pool(sb_engine* engine, int32_t layer);
+/* Engine::submit_partial_prefill + pin_partial (engine.cpp:153-182, 250-286):
+ * insert the tool-independent prefix and pin it at PARTIAL_PREFILL. */
+int sb_engine_submit_partial(sb_engine* engine, const uint64_t* tokens, int64_t n,
+                             const sb_tag_range* tags, int64_t n_tags, int64_t now,
+                             int32_t* handle);
+/* Engine::abandon_partial (engine.cpp:234-248): unpin and drop the refs. */
+int sb_engine_abandon_partial(sb_engine* engine, int32_t handle);
+int sb_engine_partial_blocks(sb_engine* engine, int32_t handle, int32_t* out, int64_t cap,
+                             int64_t* n_out);
+/* A batch of extend_prefill continuations (engine.cpp:184-223) with fixed
+ * suffix (tool-output) lengths. */
+int sb_batch_create(sb_engine* engine, const int32_t* handles, const int64_t* suffix_lens,
+                    int32_t n, sb_batch** out);
+void sb_batch_destroy(sb_batch* batch);
+/* This step's suffix tokens, packed in batch order (host or device array). */
+int sb_batch_stage_suffix(sb_batch* batch, const uint64_t* tokens, int32_t on_device,
+                          void* stream);
+/* One continuation-prefill step: chain hashes, admission lookup, insert with
+ * hint-aware eviction (Engine::complete_prefill, engine.cpp:305-322), page
+ * table, then per layer {projection stand-in, KV append, attention}, and the
+ * release of the call's block references (engine.cpp:343-346). */
+int sb_batch_run(sb_batch* batch, int64_t now, uint64_t seed, int32_t time_attention,
+                 void* stream, int32_t* launches);
+/* Per-layer attention times of the last timed run (ms, n_layers floats). */
+int sb_batch_attention_ms(sb_batch* batch, float* out);
+int sb_batch_results(sb_batch* batch, int64_t* hits, int32_t* status, int32_t* block_ids,
+                     void* stream);
+/* Async D2H of query rows [first_row, first_row+n_rows) of the last layer's
+ * attention output (bf16) into host_dst. */
+int sb_batch_copy_output(sb_batch* batch, int64_t first_row, int64_t n_rows, void* host_dst,
+                         void* stream);
+int sb_batch_info(const sb_batch* batch, int64_t* total_q, int64_t* total_blocks,
+                  int64_t* prompt_tokens, double* attention_flops, void** out);
+
 #ifdef __cplusplus
 }
 #endif

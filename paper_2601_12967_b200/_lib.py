@@ -71,6 +71,23 @@ SIGNATURES = {
     "sb_attention_work_list": (C.c_int, [I32P, I32P, C.c_int32, C.c_int32, C.c_int32, I32P, C.c_int32, I32P]),
     "sb_build_block_table": (C.c_int, [VP, VP, C.c_int32, C.c_int32, VP, VP]),
     "sb_fill_random_bf16": (C.c_int, [VP, C.c_int64, C.c_uint64, C.c_float, VP]),
+    "sb_engine_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                   C.c_uint64, C.POINTER(VP)]),
+    "sb_engine_destroy": (None, [VP]),
+    "sb_engine_cache": (VP, [VP]),
+    "sb_engine_k_pool": (VP, [VP, C.c_int32]),
+    "sb_engine_v_pool": (VP, [VP, C.c_int32]),
+    "sb_engine_submit_partial": (C.c_int, [VP, U64P, C.c_int64, C.POINTER(TagRange), C.c_int64, C.c_int64, I32P]),
+    "sb_engine_abandon_partial": (C.c_int, [VP, C.c_int32]),
+    "sb_engine_partial_blocks": (C.c_int, [VP, C.c_int32, I32P, C.c_int64, I64P]),
+    "sb_batch_create": (C.c_int, [VP, I32P, I64P, C.c_int32, C.POINTER(VP)]),
+    "sb_batch_destroy": (None, [VP]),
+    "sb_batch_stage_suffix": (C.c_int, [VP, VP, C.c_int32, VP]),
+    "sb_batch_run": (C.c_int, [VP, C.c_int64, C.c_uint64, C.c_int32, VP, I32P]),
+    "sb_batch_attention_ms": (C.c_int, [VP, C.POINTER(C.c_float)]),
+    "sb_batch_results": (C.c_int, [VP, I64P, I32P, I32P, VP]),
+    "sb_batch_copy_output": (C.c_int, [VP, C.c_int64, C.c_int64, VP, VP]),
+    "sb_batch_info": (C.c_int, [VP, I64P, I64P, I64P, C.POINTER(C.c_double), C.POINTER(VP)]),
     "sb_kv_append": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, VP]),
 }
 

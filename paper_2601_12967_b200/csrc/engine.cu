@@ -1,0 +1,381 @@
+// engine.cu — host-side continuation engine (C++), the B200 counterpart of
+// the reference engine's prompt-splitting path:
+//   Engine::submit_partial_prefill + pin_partial  engine.cpp:153-182, 250-286
+//   Engine::extend_prefill + complete_prefill     engine.cpp:184-223, 305-322
+//   Engine::abandon_partial                       engine.cpp:234-248
+// where the reference only charges a prefill cost (engine.cpp:35-39), this
+// engine runs the continuation: chain hashes -> admission lookup -> insert
+// (hint-aware eviction) -> page table -> per layer {projection stand-in, KV
+// append, tcgen05 attention} -> release, all stream-ordered on one stream.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <vector>
+
+#include "common.h"
+#include "hash.cuh"
+
+namespace sb {
+
+__global__ void k_scatter_suffix(const uint64_t* __restrict__ suffix, const int64_t* __restrict__ suffix_off,
+                                 const int64_t* __restrict__ slot_off, int32_t n_seqs, uint64_t* __restrict__ prompts) {
+  const int64_t total = suffix_off[n_seqs];
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int lo = 0, hi = n_seqs;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (suffix_off[mid] <= i) lo = mid; else hi = mid;
+    }
+    prompts[slot_off[lo] + (i - suffix_off[lo])] = suffix[i];
+  }
+}
+
+template <class T>
+static T* dmalloc(size_t n) {
+  T* p = nullptr;
+  SB_CUDA(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+  return p;
+}
+
+template <class T>
+static T* upload(const std::vector<T>& v) {
+  T* p = dmalloc<T>(v.size());
+  if (!v.empty()) SB_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return p;
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+struct PartialCall {
+  std::vector<uint64_t> tokens;
+  std::vector<sb_tag_range> tags;
+  std::vector<int32_t> ids;
+  bool live = true;
+};
+
+struct sb_engine {
+  int32_t n_layers, hq, hkv, hd, device, policy;
+  int64_t cap;
+  sb_kv_cache* cache = nullptr;
+  std::vector<__nv_bfloat16*> k_pools, v_pools;
+  std::map<int32_t, PartialCall> partials;
+  int32_t next_handle = 1;
+  ~sb_engine() {
+    cudaSetDevice(device);
+    for (auto* p : k_pools) cudaFree(p);
+    for (auto* p : v_pools) cudaFree(p);
+    if (cache) sb_kv_destroy(cache);
+  }
+};
+
+struct sb_batch {
+  sb_engine* eng = nullptr;
+  int32_t n = 0;
+  std::vector<int64_t> prefix_len, suffix_len, full_len, seq_off_h, blk_off_h;
+  int64_t total_blocks = 0, total_q = 0, total_tokens = 0;
+  int32_t max_blocks = 0, max_q = 0;
+  uint64_t* tokens = nullptr;  // packed prompts
+  int64_t *seq_off = nullptr, *blk_off = nullptr, *tag_off = nullptr;
+  sb_tag_range* tags = nullptr;
+  uint64_t* hashes = nullptr;
+  int32_t *ids = nullptr, *status = nullptr, *table = nullptr, *q_off = nullptr, *kv_len = nullptr, *work = nullptr;
+  int32_t n_work = 0;
+  int64_t* hits = nullptr;
+  int64_t *suffix_off = nullptr, *slot_off = nullptr;
+  uint64_t* suffix = nullptr;
+  __nv_bfloat16 *q = nullptr, *k_new = nullptr, *v_new = nullptr, *out = nullptr;
+  std::vector<cudaEvent_t> ev0, ev1;
+  double attn_flops = 0;
+  ~sb_batch() {
+    cudaSetDevice(eng->device);
+    void* ptrs[] = {tokens, seq_off, blk_off, tag_off, tags, hashes, ids, status, table, q_off, kv_len, work,
+                    hits, suffix_off, slot_off, suffix, q, k_new, v_new, out};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    for (auto e : ev0) cudaEventDestroy(e);
+    for (auto e : ev1) cudaEventDestroy(e);
+  }
+};
+
+extern "C" {
+
+int sb_engine_create(int32_t n_layers, int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim,
+                     int64_t capacity_blocks, int32_t policy, int32_t device, uint64_t seed, sb_engine** out) {
+  return guard([&] {
+    if (head_dim != 128) throw Error(SB_ERR_UNSUPPORTED, "head_dim must be 128");
+    if (n_layers < 1 || n_kv_heads < 1 || n_q_heads % n_kv_heads) throw Error(SB_ERR_INVALID, "bad model shape");
+    SB_CUDA(cudaSetDevice(device));
+    auto* e = new sb_engine();
+    try {
+      e->n_layers = n_layers;
+      e->hq = n_q_heads;
+      e->hkv = n_kv_heads;
+      e->hd = head_dim;
+      e->device = device;
+      e->policy = policy;
+      e->cap = capacity_blocks;
+      int st = sb_kv_create(16, capacity_blocks, policy, device, &e->cache);
+      if (st) throw Error(st, sb_last_error());
+      const int64_t elems = capacity_blocks * n_kv_heads * 16 * head_dim;
+      for (int l = 0; l < n_layers; ++l) {
+        e->k_pools.push_back(dmalloc<__nv_bfloat16>(elems));
+        e->v_pools.push_back(dmalloc<__nv_bfloat16>(elems));
+        // stand-in for the KV written by the eager prefill of a random-init model
+        st = sb_fill_random_bf16(e->k_pools.back(), elems, seed * 131 + 2 * l, 1.f, nullptr);
+        if (!st) st = sb_fill_random_bf16(e->v_pools.back(), elems, seed * 131 + 2 * l + 1, 1.f, nullptr);
+        if (st) throw Error(st, sb_last_error());
+      }
+      SB_CUDA(cudaDeviceSynchronize());
+    } catch (...) {
+      delete e;
+      throw;
+    }
+    *out = e;
+    return int(SB_OK);
+  });
+}
+
+void sb_engine_destroy(sb_engine* e) { delete e; }
+sb_kv_cache* sb_engine_cache(sb_engine* e) { return e->cache; }
+void* sb_engine_k_pool(sb_engine* e, int32_t layer) { return e->k_pools.at(layer); }
+void* sb_engine_v_pool(sb_engine* e, int32_t layer) { return e->v_pools.at(layer); }
+
+int sb_engine_submit_partial(sb_engine* e, const uint64_t* tokens, int64_t n, const sb_tag_range* tags,
+                             int64_t n_tags, int64_t now, int32_t* handle) {
+  return guard([&] {
+    if (n <= 0) throw Error(SB_ERR_INVALID, "submit_partial_prefill: prefix must be non-empty");
+    PartialCall pc;
+    pc.tokens.assign(tokens, tokens + n);
+    pc.tags.assign(tags, tags + n_tags);
+    pc.ids.resize(static_cast<size_t>((n + 15) / 16));
+    int64_t n_out = 0;
+    int st = sb_kv_insert(e->cache, tokens, n, tags, n_tags, now, pc.ids.data(), &n_out);
+    if (st) return st;
+    // pinned at the PARTIAL_PREFILL tier until extended or abandoned (engine.cpp:280-281)
+    st = sb_kv_set_reuse_priority(e->cache, pc.ids.data(), n_out, 1, SB_TAG_PARTIAL_PREFILL);
+    if (st) return st;
+    *handle = e->next_handle++;
+    e->partials.emplace(*handle, std::move(pc));
+    return int(SB_OK);
+  });
+}
+
+int sb_engine_abandon_partial(sb_engine* e, int32_t handle) {
+  return guard([&] {
+    auto it = e->partials.find(handle);
+    if (it == e->partials.end() || !it->second.live) throw Error(SB_ERR_INVALID, "stale continuation handle");
+    auto& ids = it->second.ids;
+    int st = sb_kv_set_reuse_priority(e->cache, ids.data(), static_cast<int64_t>(ids.size()), 0, -1);
+    if (!st) st = sb_kv_release(e->cache, ids.data(), static_cast<int64_t>(ids.size()));
+    it->second.live = false;
+    return st;
+  });
+}
+
+int sb_engine_partial_blocks(sb_engine* e, int32_t handle, int32_t* out, int64_t cap, int64_t* n_out) {
+  return guard([&] {
+    auto it = e->partials.find(handle);
+    if (it == e->partials.end()) throw Error(SB_ERR_INVALID, "unknown handle");
+    const auto& ids = it->second.ids;
+    *n_out = static_cast<int64_t>(ids.size());
+    for (int64_t i = 0; i < std::min<int64_t>(cap, *n_out); ++i) out[i] = ids[i];
+    return int(SB_OK);
+  });
+}
+
+int sb_batch_create(sb_engine* e, const int32_t* handles, const int64_t* suffix_lens, int32_t n, sb_batch** out) {
+  return guard([&] {
+    if (n <= 0) throw Error(SB_ERR_INVALID, "empty batch");
+    SB_CUDA(cudaSetDevice(e->device));
+    auto* b = new sb_batch();
+    try {
+      b->eng = e;
+      b->n = n;
+      std::vector<uint64_t> toks;
+      std::vector<sb_tag_range> tags;
+      std::vector<int64_t> tag_off{0}, slot_off, suffix_off{0};
+      b->seq_off_h = {0};
+      b->blk_off_h = {0};
+      for (int i = 0; i < n; ++i) {
+        auto it = e->partials.find(handles[i]);
+        if (it == e->partials.end() || !it->second.live) throw Error(SB_ERR_INVALID, "stale continuation handle");
+        const PartialCall& pc = it->second;
+        const int64_t pl = static_cast<int64_t>(pc.tokens.size()), sl = suffix_lens[i];
+        if (pl % 16) throw Error(SB_ERR_UNSUPPORTED, "tool-independent prefix must end on a 16-token block boundary");
+        if (sl <= 0) throw Error(SB_ERR_INVALID, "suffix must be non-empty");
+        b->prefix_len.push_back(pl);
+        b->suffix_len.push_back(sl);
+        b->full_len.push_back(pl + sl);
+        slot_off.push_back(static_cast<int64_t>(toks.size()) + pl);
+        toks.insert(toks.end(), pc.tokens.begin(), pc.tokens.end());
+        toks.resize(toks.size() + static_cast<size_t>(sl), 0);
+        for (auto t : pc.tags) tags.push_back(t);
+        tags.push_back(sb_tag_range{pl, pl + sl, SB_TAG_TOOL_OUTPUT, 0});
+        tag_off.push_back(static_cast<int64_t>(tags.size()));
+        b->seq_off_h.push_back(static_cast<int64_t>(toks.size()));
+        b->blk_off_h.push_back(b->blk_off_h.back() + (pl + sl + 15) / 16);
+        suffix_off.push_back(suffix_off.back() + sl);
+        b->max_blocks = std::max<int32_t>(b->max_blocks, static_cast<int32_t>((pl + sl + 15) / 16));
+        b->max_q = std::max<int32_t>(b->max_q, static_cast<int32_t>(sl));
+        const double keys = static_cast<double>(sl) * pl + static_cast<double>(sl) * (sl + 1) / 2;
+        b->attn_flops += 4.0 * e->hd * e->hq * keys;
+      }
+      b->total_tokens = static_cast<int64_t>(toks.size());
+      b->total_blocks = b->blk_off_h.back();
+      b->total_q = suffix_off.back();
+      b->tokens = upload(toks);
+      b->seq_off = upload(b->seq_off_h);
+      b->blk_off = upload(b->blk_off_h);
+      b->tag_off = upload(tag_off);
+      b->tags = upload(tags);
+      b->hashes = dmalloc<uint64_t>(b->total_blocks);
+      b->ids = dmalloc<int32_t>(b->total_blocks);
+      b->status = dmalloc<int32_t>(n);
+      b->hits = dmalloc<int64_t>(n);
+      b->table = dmalloc<int32_t>(static_cast<size_t>(n) * b->max_blocks);
+      std::vector<int32_t> qo{0}, kl;
+      for (int i = 0; i < n; ++i) {
+        qo.push_back(qo.back() + static_cast<int32_t>(b->suffix_len[i]));
+        kl.push_back(static_cast<int32_t>(b->full_len[i]));
+      }
+      b->q_off = upload(qo);
+      b->kv_len = upload(kl);
+      b->suffix_off = upload(suffix_off);
+      b->slot_off = upload(slot_off);
+      b->suffix = dmalloc<uint64_t>(b->total_q);
+      b->q = dmalloc<__nv_bfloat16>(static_cast<size_t>(b->total_q) * e->hq * e->hd);
+      b->out = dmalloc<__nv_bfloat16>(static_cast<size_t>(b->total_q) * e->hq * e->hd);
+      b->k_new = dmalloc<__nv_bfloat16>(static_cast<size_t>(b->total_q) * e->hkv * e->hd);
+      b->v_new = dmalloc<__nv_bfloat16>(static_cast<size_t>(b->total_q) * e->hkv * e->hd);
+      // LPT-ordered attention work list
+      const int tpt = 128 / (e->hq / e->hkv);
+      int64_t cap_items = 0;
+      for (int i = 0; i < n; ++i) cap_items += (b->suffix_len[i] + 2 * tpt - 1) / (2 * tpt) * e->hkv;
+      std::vector<int32_t> work(static_cast<size_t>(2 * cap_items + 2));
+      int st = sb_attention_work_list(qo.data(), kl.data(), n, e->hq, e->hkv, work.data(),
+                                      static_cast<int32_t>(cap_items + 1), &b->n_work);
+      if (st) throw Error(st, sb_last_error());
+      work.resize(static_cast<size_t>(2 * b->n_work));
+      b->work = upload(work);
+      b->ev0.resize(e->n_layers);
+      b->ev1.resize(e->n_layers);
+      for (int l = 0; l < e->n_layers; ++l) {
+        SB_CUDA(cudaEventCreate(&b->ev0[l]));
+        SB_CUDA(cudaEventCreate(&b->ev1[l]));
+      }
+    } catch (...) {
+      delete b;
+      throw;
+    }
+    *out = b;
+    return int(SB_OK);
+  });
+}
+
+void sb_batch_destroy(sb_batch* b) { delete b; }
+
+int sb_batch_stage_suffix(sb_batch* b, const uint64_t* tokens, int32_t on_device, void* stream) {
+  return guard([&] {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    SB_CUDA(cudaMemcpyAsync(b->suffix, tokens, sizeof(uint64_t) * b->total_q,
+                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    const int grid = static_cast<int>(std::min<int64_t>((b->total_q + 255) / 256, 148 * 8));
+    k_scatter_suffix<<<std::max(grid, 1), 256, 0, st>>>(b->suffix, b->suffix_off, b->slot_off, b->n, b->tokens);
+    SB_CHECK_LAUNCH();
+    return int(SB_OK);
+  });
+}
+
+int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention, void* stream,
+                 int32_t* launches) {
+  return guard([&] {
+    sb_engine* e = b->eng;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int n_launch = 0;
+    auto chk = [](int s) {
+      if (s) throw Error(s, sb_last_error());
+    };
+    chk(sb_chain_hash_batch(b->tokens, b->seq_off, b->blk_off, nullptr, b->n, 16, b->hashes, stream));
+    n_launch += 1;
+    chk(sb_kv_lookup_prefix_batch(e->cache, b->tokens, b->seq_off, b->blk_off, b->blk_off_h.data(), b->hashes, b->n,
+                                  now, b->hits, stream));
+    n_launch += 3;
+    chk(sb_kv_insert_batch(e->cache, b->tokens, b->seq_off, b->tags, b->tag_off, b->blk_off, b->blk_off_h.data(),
+                           b->hashes, b->n, now, b->ids, b->status, stream));
+    n_launch += 5 * b->n;
+    chk(sb_build_block_table(b->ids, b->blk_off, b->n, b->max_blocks, b->table, stream));
+    n_launch += 1;
+    const float scale = 1.f / std::sqrt(static_cast<float>(e->hd));
+    const int64_t nq = b->total_q * e->hq * e->hd, nkv = b->total_q * e->hkv * e->hd;
+    for (int l = 0; l < e->n_layers; ++l) {
+      const uint64_t base = (seed * 1000003ull + static_cast<uint64_t>(l)) * 3ull;
+      chk(sb_fill_random_bf16(b->q, nq, base, 1.f, stream));  // projection outputs (random-init stand-in)
+      chk(sb_fill_random_bf16(b->k_new, nkv, base + 1, 1.f, stream));
+      chk(sb_fill_random_bf16(b->v_new, nkv, base + 2, 1.f, stream));
+      chk(sb_kv_append(b->k_new, b->v_new, e->k_pools[l], e->v_pools[l], b->q_off, b->kv_len, b->table, b->n,
+                       b->max_blocks, e->hkv, e->hd, 16, stream));
+      if (time_attention) SB_CUDA(cudaEventRecord(b->ev0[l], st));
+      chk(sb_continuation_attention(b->q, e->k_pools[l], e->v_pools[l], b->out, b->q_off, b->kv_len, b->table, b->n,
+                                    b->max_blocks, b->max_q, static_cast<int32_t>(b->total_q), e->hq, e->hkv, e->hd, 16,
+                                    e->cap, scale, b->work, b->n_work, stream));
+      if (time_attention) SB_CUDA(cudaEventRecord(b->ev1[l], st));
+      n_launch += 5;
+    }
+    chk(sb_kv_release_batch(e->cache, b->ids, b->total_blocks, nullptr, stream));
+    n_launch += 3;
+    if (launches) *launches = n_launch;
+    return int(SB_OK);
+  });
+}
+
+int sb_batch_attention_ms(sb_batch* b, float* out) {
+  return guard([&] {
+    for (int l = 0; l < b->eng->n_layers; ++l) {
+      SB_CUDA(cudaEventSynchronize(b->ev1[l]));
+      SB_CUDA(cudaEventElapsedTime(&out[l], b->ev0[l], b->ev1[l]));
+    }
+    return int(SB_OK);
+  });
+}
+
+int sb_batch_results(sb_batch* b, int64_t* hits, int32_t* status, int32_t* block_ids, void* stream) {
+  return guard([&] {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (hits) SB_CUDA(cudaMemcpyAsync(hits, b->hits, sizeof(int64_t) * b->n, cudaMemcpyDeviceToHost, st));
+    if (status) SB_CUDA(cudaMemcpyAsync(status, b->status, sizeof(int32_t) * b->n, cudaMemcpyDeviceToHost, st));
+    if (block_ids)
+      SB_CUDA(cudaMemcpyAsync(block_ids, b->ids, sizeof(int32_t) * b->total_blocks, cudaMemcpyDeviceToHost, st));
+    SB_CUDA(cudaStreamSynchronize(st));
+    return int(SB_OK);
+  });
+}
+
+int sb_batch_copy_output(sb_batch* b, int64_t first_row, int64_t n_rows, void* host_dst, void* stream) {
+  return guard([&] {
+    if (first_row < 0 || first_row + n_rows > b->total_q) throw Error(SB_ERR_INVALID, "row range");
+    const size_t row = static_cast<size_t>(b->eng->hq) * b->eng->hd;
+    SB_CUDA(cudaMemcpyAsync(host_dst, b->out + first_row * row, n_rows * row * sizeof(__nv_bfloat16),
+                            cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)));
+    return int(SB_OK);
+  });
+}
+
+int sb_batch_info(const sb_batch* b, int64_t* total_q, int64_t* total_blocks, int64_t* prompt_tokens,
+                  double* attention_flops, void** out_ptr) {
+  if (total_q) *total_q = b->total_q;
+  if (total_blocks) *total_blocks = b->total_blocks;
+  if (prompt_tokens) *prompt_tokens = b->total_tokens;
+  if (attention_flops) *attention_flops = b->attn_flops;
+  if (out_ptr) *out_ptr = b->out;
+  return SB_OK;
+}
+
+}  // extern "C"

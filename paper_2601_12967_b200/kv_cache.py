@@ -80,7 +80,8 @@ class KvCache:
     # -- lifetime
     def close(self):
         if getattr(self, "_h", None):
-            self._L.sb_kv_destroy(self._h)
+            if getattr(self, "_owner", True):
+                self._L.sb_kv_destroy(self._h)
             self._h = None
 
     def __del__(self):

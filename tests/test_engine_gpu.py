@@ -57,9 +57,9 @@ def test_engine_steps_match_oracle(n_req, slack):
         for st, ids in zip(exp_st, exp_ids):
             if st == 0:
                 assert oc.release(ids) == 0
-        assert batch.hits.cpu().tolist() == exp_hits, step
-        assert batch.status.cpu().tolist() == exp_st, step
-        got = batch.ids.cpu().numpy()
+        hits, status, got = batch.results()
+        assert hits.tolist() == exp_hits, step
+        assert status.tolist() == exp_st, step
         for i, ids in enumerate(exp_ids):
             if exp_st[i] == 0:
                 a, b = batch.blk_off_h[i], batch.blk_off_h[i + 1]
