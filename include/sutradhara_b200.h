@@ -285,6 +285,23 @@ int sb_batch_copy_output(sb_batch* batch, int64_t first_row, int64_t n_rows, voi
 int sb_batch_info(const sb_batch* batch, int64_t* total_q, int64_t* total_blocks,
                   int64_t* prompt_tokens, double* attention_flops, void** out);
 
+/* ---- agentic trace replay on the B200 pool (FTR / hit rate) ---------- */
+/* Generates the reference's synthetic agent trace (trace_gen.cpp:96-193;
+ * workload "default" | "tool_heavy" | "iteration_heavy", gen[8] overrides as
+ * [prompt_median, tool_out_median, decode_inter_median, decode_final_median,
+ * qps, depth_p, fanout_p, ratio_scale], <= 0 keeps the default) and replays it
+ * with the reference's engine/orchestrator timing rules (engine.cpp,
+ * orchestrator.cpp) while every KV decision runs on a fresh B200 pool.
+ * preset: 0 baseline, 1 baseline_sched, 2 sutradhara (runner.cpp:120-153).
+ * cost (NULL = reference defaults): [prefill_ms_per_token,
+ * decode_ms_per_token, batch_decode_overhead_ms, chunk_size].  Outputs per
+ * request: FTR, e2e (virtual ms), prefix-hit and prompt tokens. */
+int sb_replay_generated(const char* workload, const double* gen, int32_t n_requests,
+                        uint64_t seed, int32_t preset, int64_t capacity_blocks,
+                        int64_t block_size, const double* cost, int32_t device, int64_t* ftr,
+                        int64_t* e2e, int64_t* hit_tokens, int64_t* prompt_tokens,
+                        uint64_t* evictions);
+
 #ifdef __cplusplus
 }
 #endif

@@ -88,6 +88,8 @@ SIGNATURES = {
     "sb_batch_results": (C.c_int, [VP, I64P, I32P, I32P, VP]),
     "sb_batch_copy_output": (C.c_int, [VP, C.c_int64, C.c_int64, VP, VP]),
     "sb_batch_info": (C.c_int, [VP, I64P, I64P, I64P, C.POINTER(C.c_double), C.POINTER(VP)]),
+    "sb_replay_generated": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), C.c_int32, C.c_uint64, C.c_int32, C.c_int64,
+                                      C.c_int64, C.POINTER(C.c_double), C.c_int32, I64P, I64P, I64P, I64P, U64P]),
     "sb_kv_append": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, VP]),
 }
 
