@@ -182,20 +182,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_3d(sQ + t * kTileBytes + a * kAtomBytes, &tm_q, &ss.q_full, a * 64, kvh * p.group,
                       q0 + first_q + t * p.tpt);
       const int32_t* trow = p.table + static_cast<int64_t>(seq) * p.max_blocks;
+      int rows[8], next_rows[8];
+      auto fetch_rows = [&](int j, int (&r)[8]) {
+#pragma unroll
+        for (int pg = 0; pg < 8; ++pg) {
+          const int jb = j * 8 + pg;
+          const int page = (jb * 16 < kv_limit) ? __ldg(trow + jb) : -1;  // -1: no page (failed insert)
+          r[pg] = page >= 0 ? (page * p.n_kv_heads + kvh) * 16 : p.oob_row;
+        }
+      };
+      fetch_rows(0, rows);
       for (int i = 0; i < 2 * n_kv; ++i) {
         const int j = i >> 1, which = i & 1, stage = i % kStages;
+        if (which == 0 && j + 1 < n_kv) fetch_rows(j + 1, next_rows);  // page ids one tile ahead
         mbar_wait(&ss.kv_empty[stage], ((i / kStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&ss.kv_full[stage], kTileBytes);
         uint8_t* dst = sKV + stage * kTileBytes;
         const void* tm = which ? static_cast<const void*>(&tm_v) : static_cast<const void*>(&tm_k);
 #pragma unroll
-        for (int pg = 0; pg < 8; ++pg) {
-          const int jb = j * 8 + pg;
-          const int page = (jb * 16 < kv_limit) ? trow[jb] : -1;  // -1: no page (failed insert)
-          const int row = page >= 0 ? (page * p.n_kv_heads + kvh) * 16 : p.oob_row;
+        for (int pg = 0; pg < 8; ++pg)
 #pragma unroll
-          for (int a = 0; a < 2; ++a) tma_load_2d(dst + a * kAtomBytes + pg * 2048, tm, &ss.kv_full[stage], a * 64, row);
-        }
+          for (int a = 0; a < 2; ++a)
+            tma_load_2d(dst + a * kAtomBytes + pg * 2048, tm, &ss.kv_full[stage], a * 64, rows[pg]);
+        if (which == 1 && j + 1 < n_kv)
+#pragma unroll
+          for (int pg = 0; pg < 8; ++pg) rows[pg] = next_rows[pg];
       }
     }
   } else if (warp == 1) {
@@ -468,17 +479,28 @@ extern "C" int sb_attention_work_list(const int32_t* h_q_offsets, const int32_t*
   return guard([&] {
     if (n_kv_heads <= 0 || n_q_heads % n_kv_heads) throw Error(SB_ERR_INVALID, "n_q_heads % n_kv_heads != 0");
     const int tpt = 128 / (n_q_heads / n_kv_heads);
-    struct It { int64_t work; int32_t seq, kvh, pair; };
+    // LPT over (sequence, kv head) groups, each group's tiles adjacent so the
+    // CTAs running together share the group's K/V pages in L2; inside a
+    // group the longest tiles (largest causal key range) go first.
+    struct It { int64_t group_work, work; int32_t seq, kvh, pair; };
     std::vector<It> items;
     for (int s = 0; s < n_seqs; ++s) {
       const int q_len = h_q_offsets[s + 1] - h_q_offsets[s];
       const int prefix = h_kv_lens[s] - q_len;
-      for (int pr = 0; pr * 2 * tpt < q_len; ++pr) {
-        const int64_t kv_limit = prefix + std::min(q_len, (pr + 1) * 2 * tpt);
-        for (int h = 0; h < n_kv_heads; ++h) items.push_back({kv_limit, s, h, pr});
-      }
+      int64_t gw = 0;
+      for (int pr = 0; pr * 2 * tpt < q_len; ++pr) gw += prefix + std::min(q_len, (pr + 1) * 2 * tpt);
+      for (int h = 0; h < n_kv_heads; ++h)
+        for (int pr = 0; pr * 2 * tpt < q_len; ++pr) {
+          const int64_t kv_limit = prefix + std::min(q_len, (pr + 1) * 2 * tpt);
+          items.push_back({gw, kv_limit, s, h, pr});
+        }
     }
-    std::stable_sort(items.begin(), items.end(), [](const It& a, const It& b) { return a.work > b.work; });
+    std::stable_sort(items.begin(), items.end(), [](const It& a, const It& b) {
+      if (a.group_work != b.group_work) return a.group_work > b.group_work;
+      if (a.seq != b.seq) return a.seq < b.seq;
+      if (a.kvh != b.kvh) return a.kvh < b.kvh;
+      return a.work > b.work;
+    });
     if (static_cast<int64_t>(items.size()) > cap) throw Error(SB_ERR_INVALID, "work list capacity too small");
     for (size_t i = 0; i < items.size(); ++i) {
       out[2 * i] = items[i].seq;
