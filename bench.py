@@ -255,7 +255,6 @@ def run_ours(args, rank, world, local_rank):
             "scope": "hash + lookup + insert/evict + KV append + attention; dense projections/MLP not measured",
         },
         "hit_rate": hit_rate,
-        "p50_ftr_ms": None,
         "evicted_blocks_per_step": stats["evicted_blocks"] / max(1, (args.warmup + 2 * args.steps)),
         "e2e": {"value": total_tokens / (ms_e2e * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": tokens_per_step * 8, "d2h_bytes_per_step": d2h // args.steps},
@@ -267,9 +266,47 @@ def run_ours(args, rank, world, local_rank):
                      "launches_timed": len(attn_ms)},
         "clocks": clk,
     }
+    line.update(trace_replay_metrics(line["value"], local_rank))
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(reqs, budget_s=20.0)
     return line
+
+
+TRACE = dict(n_requests=60, seed=1, capacity_blocks=8192, workload="default")
+
+
+def trace_replay_metrics(tokens_per_s: float, device: int):
+    """p50 FTR and hint-aware hit rate on the reference's synthetic agent
+    trace (trace_gen default workload, 60 requests, 8192-block pool),
+    replayed with every KV decision on the B200 pool (csrc/replay.cu):
+    - reference cost model: identical to the reference simulator's numbers
+      (tests/test_replay_gpu.py), for the Sutradhara and Baseline presets;
+    - B200-calibrated: prefill charged at the measured continuation-prefill
+      rate instead of the reference's 0.05 ms/token (decode model unchanged)."""
+    from paper_2601_12967_b200.replay import replay
+
+    out = {}
+    t0 = time.perf_counter()
+    sut = replay(preset="sutradhara", device=device, **TRACE)
+    wall = time.perf_counter() - t0
+    base = replay(preset="baseline", device=device, **TRACE)
+    cal_cost = [1000.0 / tokens_per_s, 20.0, 2.0, 256]
+    sut_cal = replay(preset="sutradhara", device=device, cost=cal_cost, **TRACE)
+    base_cal = replay(preset="baseline", device=device, cost=cal_cost, **TRACE)
+    out["p50_ftr_ms"] = sut.p50()
+    out["trace"] = {
+        "workload": "reference trace_gen default workload, 60 requests, seed 1, pool 8192 x 16-token blocks",
+        "sutradhara": {"p50_ftr_ms": sut.p50(), "p50_e2e_ms": sut.p50(sut.e2e_ms), "hit_rate": sut.hit_rate,
+                       "evictions": sut.evictions},
+        "baseline": {"p50_ftr_ms": base.p50(), "p50_e2e_ms": base.p50(base.e2e_ms), "hit_rate": base.hit_rate,
+                     "evictions": base.evictions},
+        "b200_calibrated": {"prefill_ms_per_token": cal_cost[0], "sutradhara_p50_ftr_ms": sut_cal.p50(),
+                            "baseline_p50_ftr_ms": base_cal.p50(),
+                            "sutradhara_hit_rate": sut_cal.hit_rate},
+        "replay_wall_s": wall,
+    }
+    out["hint_aware_hit_rate"] = sut.hit_rate
+    return out
 
 
 # ----------------------------------------------------------- CPU reference

@@ -108,3 +108,29 @@ int refrun_thrashing(int32_t tiered, int64_t* it2_hits) {
 }
 
 }  // extern "C"
+
+extern "C" int64_t refrun_timeline(const double* gen, int32_t n_requests, uint64_t seed, int32_t preset,
+                                   int64_t capacity, int64_t block_size, char* buf, int64_t cap) {
+  GeneratorConfig g = default_workload();
+  g.num_requests = n_requests;
+  if (gen) {
+    if (gen[0] > 0) g.prompt_base_median = gen[0];
+    if (gen[1] > 0) g.tool_out_median = gen[1];
+    if (gen[2] > 0) g.decode_inter_median = gen[2];
+    if (gen[3] > 0) g.decode_final_median = gen[3];
+    if (gen[4] > 0) g.qps = gen[4];
+    if (gen[5] > 0) g.depth_p = gen[5];
+    if (gen[6] > 0) g.fanout_p = gen[6];
+    if (gen[7] > 0) g.ratio_scale = gen[7];
+  }
+  auto trace = generate_synthetic_trace(g, seed);
+  SimConfig sim = preset_config(preset, capacity, block_size, seed);
+  SimulationResult res = run_trace(trace, sim);
+  const std::string& s = res.timeline_text;
+  if (buf && cap > 0) {
+    size_t m = std::min<size_t>(s.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(buf, s.data(), m);
+    buf[m] = 0;
+  }
+  return static_cast<int64_t>(s.size());
+}

@@ -33,6 +33,8 @@
 #include <string>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "common.h"
 #include "hash.cuh"
 
@@ -45,6 +47,7 @@ constexpr uint64_t kNoKey = ~uint64_t(0);
 constexpr int kSelectThreads = 1024;
 constexpr int kSortSmemKeys = 8192;
 constexpr int kCandSmem = 16384;  // candidate keys staged in shared memory (128 KB)
+constexpr int64_t kCoopMinCap = 65536;  // pools at least this large use the all-SM scorer
 
 enum Ctr { C_NRES = 0, C_EVICTED, C_LOOKUPS, C_HIT_TOK, C_LOOK_TOK, C_INS_BLOCKS, C_EV_BLOCKS, C_FULL, C_N };
 enum Scal { S_F = 0, S_K, S_FREE, S_NEV, S_STATUS, S_FAILPOS, S_NNEW, S_NCAND, S_ERRIDX, S_NLATE, S_N };
@@ -526,6 +529,225 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
 // Sequential decisions of one insert (kv_cache.cpp:471-506), from the first
 // pre-miss position on.  Single thread: each step is a handful of
 // L1/L2-resident accesses.
+// ---------------------------------------------------------------------------
+// Cooperative (all-SM) variant of k_select for large pools: every CTA scores
+// its slice of the pool once (the only HBM pass: 24 B per block) and keeps
+// its candidate keys in shared memory; the radix passes exchange 2048-bin
+// histograms through global memory between grid barriers; CTA 0 sorts the
+// selected keys.  Same outputs as k_select.
+struct CoopBuf {
+  uint32_t* hist;              // [6][2048]
+  unsigned long long* ctr;     // [0] candidates, [1] selected, [2] pre-hit candidates
+};
+
+__global__ void __launch_bounds__(kSelectThreads, 1)
+    k_select_coop(Pool P, Scratch S, InsertArgs A, int s, int mode, int64_t needed, CoopBuf G) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t warp_sums[33];
+  __shared__ int64_t sh[8];
+  __shared__ uint32_t cnt_b;
+  __shared__ unsigned int n_local;
+  extern __shared__ uint64_t local_keys[];
+  const int t = threadIdx.x;
+  const int cta = blockIdx.x, n_cta = gridDim.x;
+  int64_t P_ = 0, b0 = 0;
+  // ---- phase A (CTA 0): first miss, tag check, exclusions, late candidates
+  if (cta == 0) {
+    for (int i = t; i < 6 * 2048; i += blockDim.x) G.hist[i] = 0;
+    if (t < 3) G.ctr[t] = 0;
+    if (mode == 0) {
+      b0 = A.blk_off[s];
+      P_ = A.blk_off[s + 1] - b0;
+      const int64_t n = A.seq_off[s + 1] - A.seq_off[s];
+      const bool ok = tags_cover(A.tags + A.tag_off[s], A.tag_off[s + 1] - A.tag_off[s], n);
+      if (t == 0) sh[0] = P_;
+      __syncthreads();
+      for (int64_t p = t; p < P_; p += blockDim.x)
+        if (S.prehit[b0 + p] < 0) atomicMin(reinterpret_cast<unsigned long long*>(&sh[0]), (unsigned long long)p);
+      __syncthreads();
+      const int64_t f = sh[0];
+      if (t == 0) {
+        S.scal[S_F] = f;
+        S.scal[S_STATUS] = ok ? 0 : SB_ERR_CACHE;
+        S.scal[S_NLATE] = 0;
+      }
+      __syncthreads();
+      if (ok) {
+        for (int64_t p = t; p < P_; p += blockDim.x) {
+          const int32_t id = S.prehit[b0 + p];
+          if (p < f) {
+            S.kind[p] = 0;
+            S.rank_of[id] = -2;
+            if (P.ref[id] == -1 && P.pinned[id] == 0) {
+              const int64_t at = atomicAdd(reinterpret_cast<unsigned long long*>(&S.scal[S_NLATE]), 1ull);
+              if (at < kLateMax) {
+                S.late[2 * at] = static_cast<int32_t>(p);
+                S.late[2 * at + 1] = id;
+              }
+            }
+          } else if (id >= 0 && is_candidate(P, id)) {
+            atomicAdd(&G.ctr[2], 1ull);
+          }
+        }
+      }
+    } else if (t == 0) {
+      S.scal[S_F] = 0;
+      S.scal[S_STATUS] = 0;
+    }
+  }
+  grid.sync();
+  if (S.scal[S_STATUS] != 0) {
+    if (cta == 0 && t == 0) {
+      S.scal[S_K] = 0;
+      S.scal[S_FREE] = 0;
+    }
+    return;  // uniform across the grid
+  }
+  // ---- phase B (all CTAs): score the slice, keep candidate keys in smem
+  const int64_t chunk = (P.cap + n_cta - 1) / n_cta;
+  const int64_t lo = cta * chunk, hi = min(P.cap, lo + chunk);
+  if (t == 0) n_local = 0;
+  __syncthreads();
+  for (int64_t i = lo + t; i < hi; i += blockDim.x) {
+    const int32_t id = static_cast<int32_t>(i);
+    if (!is_candidate(P, id) || S.rank_of[id] == -2) continue;
+    local_keys[atomicAdd(&n_local, 1u)] = victim_key(P, id);
+  }
+  __syncthreads();
+  const int64_t nl = n_local;
+  if (t == 0) atomicAdd(&G.ctr[0], static_cast<unsigned long long>(nl));
+  grid.sync();
+  if (cta == 0 && mode == 0) {
+    const int64_t f = S.scal[S_F];
+    b0 = A.blk_off[s];
+    for (int64_t p = t; p < f; p += blockDim.x) S.rank_of[S.prehit[b0 + p]] = -1;
+  }
+  const int64_t ncand = static_cast<int64_t>(G.ctr[0]);
+  const int64_t free_cnt = P.cap - static_cast<int64_t>(P.ctr[C_NRES]);
+  int64_t K, Fp = 0;
+  if (mode == 0) {
+    P_ = A.blk_off[s + 1] - A.blk_off[s];
+    const int64_t rest = P_ - S.scal[S_F];
+    Fp = min(free_cnt, rest);
+    K = min(ncand, (rest > free_cnt ? rest - free_cnt : int64_t(0)) + static_cast<int64_t>(G.ctr[2]));
+  } else {
+    K = min(ncand, needed);
+  }
+  uint64_t prefix = 0, mask = 0;
+  if (K > 0 && K < ncand) {
+    int64_t need = K;
+    const int shifts[6] = {53, 42, 31, 20, 10, 0};
+    const int widths[6] = {11, 11, 11, 11, 10, 10};
+    for (int pass = 0; pass < 6; ++pass) {
+      const int sh_ = shifts[pass], wd = widths[pass];
+      const uint64_t bmask = (uint64_t(1) << wd) - 1;
+      hist[2 * t] = 0;
+      hist[2 * t + 1] = 0;
+      __syncthreads();
+      for (int64_t i = t; i < nl; i += blockDim.x) {
+        const uint64_t k = local_keys[i];
+        if ((k & mask) == prefix) atomicAdd(&hist[(k >> sh_) & bmask], 1u);
+      }
+      __syncthreads();
+      uint32_t* gh = G.hist + pass * 2048;
+      if (hist[2 * t]) atomicAdd(&gh[2 * t], hist[2 * t]);
+      if (hist[2 * t + 1]) atomicAdd(&gh[2 * t + 1], hist[2 * t + 1]);
+      grid.sync();
+      hist[2 * t] = gh[2 * t];
+      hist[2 * t + 1] = gh[2 * t + 1];
+      __syncthreads();
+      const uint32_t a0 = hist[2 * t], a1 = hist[2 * t + 1];
+      block_scan_2048(hist, warp_sums);
+      const uint32_t e0 = hist[2 * t], e1 = hist[2 * t + 1];
+      if (e0 < need && need <= e0 + a0) {
+        sh[4] = 2 * t;
+        sh[5] = e0;
+        cnt_b = a0;
+      }
+      if (e1 < need && need <= e1 + a1) {
+        sh[4] = 2 * t + 1;
+        sh[5] = e1;
+        cnt_b = a1;
+      }
+      __syncthreads();
+      need -= sh[5];
+      prefix |= static_cast<uint64_t>(sh[4]) << sh_;
+      mask |= bmask << sh_;
+      const bool done = static_cast<int64_t>(cnt_b) == need;
+      __syncthreads();
+      if (done) break;
+    }
+  }
+  if (K > 0)
+    for (int64_t i = t; i < nl; i += blockDim.x) {
+      const uint64_t k = local_keys[i];
+      if (K == ncand || (k & mask) <= prefix) S.sortbuf[atomicAdd(&G.ctr[1], 1ull)] = k;
+    }
+  grid.sync();
+  if (cta != 0) return;
+  // ---- phase D (CTA 0): sort the K selected keys, publish, free list
+  if (K > 0) {
+    int64_t n2 = 1;
+    while (n2 < K) n2 <<= 1;
+    uint64_t* dst = S.sortbuf;
+    const bool in_smem = K <= kSortSmemKeys;  // dynamic smem holds >= kSortSmemKeys keys
+    if (in_smem) {
+      for (int64_t i = t; i < n2; i += blockDim.x) local_keys[i] = i < K ? S.sortbuf[i] : kNoKey;
+      __syncthreads();
+      bitonic_smem(local_keys, static_cast<int>(n2));
+      dst = local_keys;
+    } else {
+      for (int64_t i = K + t; i < n2; i += blockDim.x) S.sortbuf[i] = kNoKey;
+      __syncthreads();
+      bitonic_global(S.sortbuf, n2);
+    }
+    for (int64_t r = t; r < K; r += blockDim.x) {
+      const uint64_t k = dst[r];
+      S.victims[r] = k;
+      S.taken[r] = 0;
+      S.rank_of[k & kIdMask] = static_cast<int32_t>(r);
+    }
+  }
+  if (Fp > 0) {
+    __shared__ uint32_t wcnt[33];
+    __shared__ int64_t found;
+    if (t == 0) found = 0;
+    __syncthreads();
+    const int lane = t & 31, w = t >> 5;
+    for (int64_t base = 0; base < P.cap; base += blockDim.x) {
+      if (found >= Fp) break;
+      const int64_t i = base + t;
+      const bool fr = i < P.cap && P.ntok[i] == 0;
+      const unsigned ball = __ballot_sync(0xffffffffu, fr);
+      if (lane == 0) wcnt[w] = __popc(ball);
+      __syncthreads();
+      if (t == 0) {
+        uint32_t acc = 0;
+        for (int k = 0; k < 32; ++k) {
+          const uint32_t cnt = wcnt[k];
+          wcnt[k] = acc;
+          acc += cnt;
+        }
+        wcnt[32] = acc;
+      }
+      __syncthreads();
+      const int64_t rank = found + wcnt[w] + __popc(ball & ((1u << lane) - 1));
+      if (fr && rank < Fp) S.freel[rank] = static_cast<int32_t>(i);
+      __syncthreads();
+      if (t == 0) found += wcnt[32];
+      __syncthreads();
+    }
+  }
+  if (t == 0) {
+    S.scal[S_K] = K;
+    S.scal[S_FREE] = Fp;
+    S.scal[S_STATUS] = 0;
+    S.scal[S_NCAND] = ncand;
+  }
+}
+
 constexpr int kWalkSmemVictims = 4096;
 
 __global__ void __launch_bounds__(32, 1) k_walk(Pool P, Scratch S, InsertArgs A, int s) {
@@ -837,6 +1059,28 @@ struct sb_kv_cache {
   int64_t* d_batch_blk = nullptr;
   int64_t* d_batch_first = nullptr;
   int64_t batch_cap = 0;
+  // cooperative scorer (large pools)
+  CoopBuf G{};
+  int coop_grid = 0;
+  size_t coop_smem = 0;
+
+  bool use_coop() const { return P.cap >= kCoopMinCap && coop_grid > 0; }
+
+  void launch_select(const InsertArgs& A, int s, int mode, int64_t needed) {
+    if (!use_coop()) {
+      k_select<<<1, kSelectThreads, select_smem(), stream>>>(P, S, A, s, mode, needed);
+      return;
+    }
+    Pool p_ = P;
+    Scratch s_ = S;
+    InsertArgs a_ = A;
+    int sv = s, mv = mode;
+    int64_t nv = needed;
+    CoopBuf g_ = G;
+    void* args[] = {&p_, &s_, &a_, &sv, &mv, &nv, &g_};
+    SB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_select_coop), dim3(coop_grid), dim3(kSelectThreads),
+                                        args, coop_smem, stream));
+  }
 
   void ensure_batch(int64_t n) {
     if (n <= batch_cap) return;
@@ -852,7 +1096,7 @@ struct sb_kv_cache {
     // S.prehit aliases d_prehit_all: freed once below
     void* ptrs[] = {P.tok, P.ntok, P.chain, P.parent, P.tag, P.ref, P.pinned, P.last, P.tkey, P.tval, P.slot, P.ctr,
                     S.hashes, S.chain_out, S.kind, S.freel, S.evicted, S.victims, S.taken, S.rank_of, S.keys,
-                    S.sortbuf, S.scal, S.late, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first};
+                    S.sortbuf, S.scal, S.late, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first, G.hist, G.ctr};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
@@ -959,7 +1203,7 @@ struct sb_kv_cache {
       if (np > 0)
         k_probe_seq<<<static_cast<int>((np + 255) / 256), 256, 0, stream>>>(P, tokens, seq_off, blk_off, hashes, s,
                                                                             S.prehit);
-      k_select<<<1, kSelectThreads, select_smem(), stream>>>(P, S, A, s, 0, 0);
+      launch_select(A, s, 0, 0);
       k_walk<<<1, 32, 0, stream>>>(P, S, A, s);
       k_commit_evict<<<grid_for(np), 256, 0, stream>>>(P, S);
       k_commit_apply<<<grid_for(std::max<int64_t>(np, 1) + 2 * np), 256, 0, stream>>>(P, S, A, s);
@@ -1048,6 +1292,20 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
       c->d_hit = dalloc<int64_t>(4);
       SB_CUDA(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(c->select_smem())));
+      if (capacity_blocks >= kCoopMinCap) {
+        int n_sm = 0, per_sm = 0;
+        SB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
+        const int64_t chunk = (capacity_blocks + n_sm - 1) / n_sm;
+        c->coop_smem = static_cast<size_t>(std::max<int64_t>(chunk, kSortSmemKeys)) * sizeof(uint64_t);
+        if (c->coop_smem <= 200 * 1024) {
+          SB_CUDA(cudaFuncSetAttribute(k_select_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(c->coop_smem)));
+          SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_coop, kSelectThreads, c->coop_smem));
+          if (per_sm >= 1) c->coop_grid = n_sm;
+          c->G.hist = dalloc<uint32_t>(6 * 2048);
+          c->G.ctr = dalloc<unsigned long long>(4);
+        }
+      }
       SB_CHECK_LAUNCH();
       SB_CUDA(cudaStreamSynchronize(c->stream));
     } catch (...) {
@@ -1210,7 +1468,7 @@ int sb_kv_evict(sb_kv_cache* c, int64_t needed, int32_t* out_ids, int64_t* n_out
     c->ensure_positions(std::min<int64_t>(needed, c->P.cap));
     c->ensure_ids(std::min<int64_t>(needed, c->P.cap) + 1);
     InsertArgs A{};
-    k_select<<<1, kSelectThreads, c->select_smem(), c->stream>>>(c->P, c->S, A, 0, 1, needed);
+    c->launch_select(A, 0, 1, needed);
     k_evict_out<<<grid_for(c->P.cap), 256, 0, c->stream>>>(c->S, c->d_ids, c->d_first);
     k_commit_evict<<<grid_for(c->P.cap), 256, 0, c->stream>>>(c->P, c->S);
     SB_CHECK_LAUNCH();

@@ -19,16 +19,18 @@
 //   presets                       runner.cpp:120-153
 //   nearest-rank percentiles      metrics.cpp:136-151
 // Differences in mechanics only: block tags of a pinned prefix are read and
-// updated with one batched pool call instead of one call per block, and the
-// streaming JSON parser is replaced by its observable effect on synthesized
-// transcripts (each tool is dispatched at the decode token holding its
-// closing brace, orchestrator.cpp:38-91).
+// updated with one batched pool call instead of one call per block.  The
+// engine's step-event rules are kept exactly, including a wake() issued from
+// inside a step's completions starting a second step chain (token callbacks
+// then repeat, and the streaming parser sees repeated chunks).
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
+#include <memory>
 #include <optional>
 #include <queue>
 #include <random>
@@ -43,6 +45,12 @@ namespace sb {
 namespace rp {
 
 using Time = int64_t;
+// SB_REPLAY_TRACE=1 prints an orchestrator timeline (same wording as the
+// reference's, orchestrator.cpp:173-177) to stderr for debugging.
+static const bool g_trace = [] {
+  const char* v = std::getenv("SB_REPLAY_TRACE");
+  return v && v[0] == '1';
+}();
 
 // ------------------------------------------------------------ randomness
 struct Rng {
@@ -194,6 +202,225 @@ void append_section(std::vector<uint64_t>& toks, std::vector<sb_tag_range>& tags
   for (int64_t i = 0; i < s.len; ++i) toks.push_back(splitmix64(seed + static_cast<uint64_t>(i)));
   tags.push_back(sb_tag_range{b, b + s.len, kv_tag_of(s.tag), 0});
 }
+
+
+// ------------------------------------------------- tool-call transcript
+// Decode transcript of an intermediate iteration and its per-token character
+// spans (orchestrator.cpp:38-91): tool j's closing brace lands in decode token
+// emit_j.  Fed to the streaming parser token by token, so repeated token
+// callbacks (the engine can run two step chains, engine.cpp:119-123 +
+// 379-383) reach the parser exactly as in the reference.
+struct Transcript {
+  std::string text;
+  std::vector<std::pair<size_t, size_t>> spans;
+};
+
+Transcript make_transcript(const Iter& it, const std::string& rid, size_t iter) {
+  Transcript t;
+  std::vector<int64_t> close;
+  t.text = "[";
+  for (size_t j = 0; j < it.tools.size(); ++j) {
+    if (j) t.text += ", ";
+    t.text += "{\"tool\": \"" + it.tools[j].name + "\", \"query\": \"" + rid + "/" + std::to_string(iter) + "/" +
+              std::to_string(j) + "\", \"call\": " + std::to_string(j) + "}";
+    close.push_back(static_cast<int64_t>(t.text.size()) - 1);
+  }
+  t.text += "]";
+  const int64_t n = it.decode_len;
+  std::vector<int64_t> cnt(static_cast<size_t>(n), 0);
+  int64_t pt = -1, pc = -1;
+  auto spread = [&](int64_t first, int64_t toks, int64_t chars) {
+    for (int64_t k = 0; k < toks; ++k) cnt[static_cast<size_t>(first + k)] = (k + 1) * chars / toks - k * chars / toks;
+  };
+  for (size_t j = 0; j < close.size(); ++j) {
+    spread(pt + 1, it.tools[j].emit - pt, close[j] - pc);
+    pt = it.tools[j].emit;
+    pc = close[j];
+  }
+  const int64_t rem_chars = static_cast<int64_t>(t.text.size()) - 1 - pc, rem_toks = n - 1 - pt;
+  if (rem_toks <= 0) {
+    if (pt >= 0) cnt[static_cast<size_t>(pt)] += rem_chars;
+  } else {
+    spread(pt + 1, rem_toks, rem_chars);
+  }
+  size_t pos = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    t.spans.emplace_back(pos, pos + static_cast<size_t>(cnt[static_cast<size_t>(i)]));
+    pos += static_cast<size_t>(cnt[static_cast<size_t>(i)]);
+  }
+  return t;
+}
+
+// Incremental tool-call parser with the reference's acceptance rules
+// (streaming_parser.cpp): flat array of objects, string / raw / one-level
+// nested values, sink state on malformed input.  Only what dispatch needs is
+// kept: the emitted tool names and their close token.
+struct ToolParser {
+  enum Ph { kBefore, kFirst, kObj, kAfterVal, kFirstKey, kKey, kKeyStr, kColon, kVal, kStr, kRaw, kNested, kObjAfter,
+            kAfterArr, kSink };
+  Ph ph = kBefore;
+  bool esc = false, n_str = false, n_esc = false;
+  int nested = 0;
+  std::string key, val;
+  std::map<std::string, std::string> params;
+
+  static bool ws(char c) { return c == ' ' || c == '\t' || c == '\n' || c == '\r'; }
+  void esc_append(std::string& o, char c) {
+    switch (c) {
+      case '"': o += '"'; break;
+      case '\\': o += '\\'; break;
+      case '/': o += '/'; break;
+      case 'b': o += '\b'; break;
+      case 'f': o += '\f'; break;
+      case 'n': o += '\n'; break;
+      case 'r': o += '\r'; break;
+      case 't': o += '\t'; break;
+      default: o += '\\'; o += c; break;  // includes \u: the hex digits follow verbatim
+    }
+  }
+  void finish_value() {
+    params[key] = val;
+    key.clear();
+    val.clear();
+  }
+  void close(std::vector<std::string>& out) {
+    auto it = params.find("tool");
+    if (it == params.end() || it->second.empty()) {
+      ph = kSink;
+      return;
+    }
+    out.push_back(it->second);
+    params.clear();
+    ph = kAfterVal;
+  }
+  // returns false when c must be re-processed (end of a raw value)
+  bool step(char c, std::vector<std::string>& out) {
+    switch (ph) {
+      case kBefore:
+        if (c == '[') ph = kFirst;
+        return true;
+      case kFirst:
+      case kObj:
+        if (ws(c)) return true;
+        if (c == '{') {
+          params.clear();
+          ph = kFirstKey;
+        } else if (c == ']' && ph == kFirst) {
+          ph = kAfterArr;
+        } else {
+          ph = kSink;
+        }
+        return true;
+      case kAfterVal:
+        if (ws(c)) return true;
+        ph = c == ',' ? kObj : c == ']' ? kAfterArr : kSink;
+        return true;
+      case kFirstKey:
+      case kKey:
+        if (ws(c)) return true;
+        if (c == '"') {
+          key.clear();
+          ph = kKeyStr;
+        } else if (c == '}' && ph == kFirstKey) {
+          close(out);
+        } else {
+          ph = kSink;
+        }
+        return true;
+      case kKeyStr:
+        if (esc) {
+          esc_append(key, c);
+          esc = false;
+        } else if (c == '\\') {
+          esc = true;
+        } else if (c == '"') {
+          ph = kColon;
+        } else {
+          key += c;
+        }
+        return true;
+      case kColon:
+        if (ws(c)) return true;
+        ph = c == ':' ? kVal : kSink;
+        return true;
+      case kVal:
+        if (ws(c)) return true;
+        if (c == '"') {
+          val.clear();
+          ph = kStr;
+        } else if (c == '{' || c == '[') {
+          val.assign(1, c);
+          nested = 1;
+          n_str = n_esc = false;
+          ph = kNested;
+        } else if (c == '}' || c == ']' || c == ',') {
+          ph = kSink;
+        } else {
+          val.assign(1, c);
+          ph = kRaw;
+        }
+        return true;
+      case kStr:
+        if (esc) {
+          esc_append(val, c);
+          esc = false;
+        } else if (c == '\\') {
+          esc = true;
+        } else if (c == '"') {
+          finish_value();
+          ph = kObjAfter;
+        } else {
+          val += c;
+        }
+        return true;
+      case kRaw:
+        if (ws(c) || c == ',' || c == '}') {
+          finish_value();
+          ph = kObjAfter;
+          return ws(c);
+        }
+        if (c == ']' || c == '{' || c == '[') ph = kSink;
+        else val += c;
+        return true;
+      case kNested:
+        val += c;
+        if (n_str) {
+          if (n_esc) n_esc = false;
+          else if (c == '\\') n_esc = true;
+          else if (c == '"') n_str = false;
+        } else if (c == '"') {
+          n_str = true;
+        } else if (c == '{' || c == '[') {
+          ++nested;
+        } else if ((c == '}' || c == ']') && --nested == 0) {
+          finish_value();
+          ph = kObjAfter;
+        }
+        return true;
+      case kObjAfter:
+        if (ws(c)) return true;
+        if (c == ',') ph = kKey;
+        else if (c == '}') close(out);
+        else ph = kSink;
+        return true;
+      case kAfterArr:
+      case kSink:
+        return true;
+    }
+    return true;
+  }
+  std::vector<std::string> feed(const char* s, size_t n) {
+    std::vector<std::string> out;
+    if (ph == kSink) return out;
+    for (size_t i = 0; i < n; ++i) {
+      while (!step(s[i], out))
+        if (ph == kSink) break;
+      if (ph == kSink) break;
+    }
+    return out;
+  }
+  bool malformed() const { return ph == kSink; }
+};
 
 // ------------------------------------------------------------- sim core
 struct Loop {
@@ -511,7 +738,9 @@ struct Orchestrator {
     int64_t call = 0;
     std::vector<ToolRt> tools;
     size_t pending = 0, next_dispatch = 0;
-    bool decoded = false, advanced = false;
+    bool decoded = false, advanced = false, fallback = false;
+    Transcript transcript;
+    std::unique_ptr<ToolParser> parser;
   };
   struct ReqRt {
     std::optional<int64_t> continuation;
@@ -522,6 +751,9 @@ struct Orchestrator {
   std::vector<ReqRt> reqs;
 
   Orchestrator(Sim& s, const std::vector<Request>& t) : sim(s), trace(t) {}
+  void note(size_t r, const std::string& what) const {
+    if (g_trace) std::fprintf(stderr, "t=%lld request=%s %s\n", static_cast<long long>(sim.loop.now), trace[r].id.c_str(), what.c_str());
+  }
 
   static void build(const std::vector<Section>& secs, std::vector<uint64_t>& toks, std::vector<sb_tag_range>& tags) {
     for (const auto& s : secs) append_section(toks, tags, s);
@@ -548,6 +780,7 @@ struct Orchestrator {
       build(dep, toks, tags);
       it.call = h;
       sim.extend(h, toks, tags, spec.decode_len, [this, r, i](Time at) { on_decoded(r, i, at); });
+      note(r, "extend_prefill iteration=" + std::to_string(i));
     } else {
       Call c;
       c.agentic_arrival = trace[r].arrival;
@@ -557,21 +790,33 @@ struct Orchestrator {
       c.stream_key = stream_key(r, i);
       c.on_decoded = [this, r, i](Time at) { on_decoded(r, i, at); };
       it.call = sim.submit(std::move(c));
+      note(r, "submit iteration=" + std::to_string(i));
     }
     if (spec.final) return;
+    it.transcript = make_transcript(spec, trace[r].id, i);
     it.tools.assign(spec.tools.size(), ToolRt{});
     it.pending = spec.tools.size();
-    if (sim.streaming)
+    if (sim.streaming) {
+      it.parser = std::make_unique<ToolParser>();
       sim.calls.at(it.call).on_token = [this, r, i](int64_t tok, Time at) { on_token(r, i, tok, at); };
+    }
   }
   void on_token(size_t r, size_t i, int64_t tok, Time at) {
     IterRt& it = reqs[r].iters[i];
+    if (!it.parser || it.fallback) return;
+    const auto idx = static_cast<size_t>(tok);
+    if (idx >= it.transcript.spans.size()) return;
+    const auto [b, e] = it.transcript.spans[idx];
     const auto& tools = trace[r].iters[i].tools;
-    // the streaming parser closes tool j on the token holding its '}' (emit index)
-    while (it.next_dispatch < tools.size() && tools[it.next_dispatch].emit == tok) {
+    for (const std::string& name : it.parser->feed(it.transcript.text.data() + b, e - b)) {
+      if (it.next_dispatch >= tools.size() || name != tools[it.next_dispatch].name) {
+        it.fallback = true;
+        break;
+      }
       dispatch(r, i, it.next_dispatch, at, tok);
       ++it.next_dispatch;
     }
+    if (it.parser->malformed()) it.fallback = true;
   }
   void dispatch(size_t r, size_t i, size_t j, Time now, int64_t close) {
     IterRt& it = reqs[r].iters[i];
@@ -584,12 +829,14 @@ struct Orchestrator {
       lat = std::max<Time>(static_cast<Time>(std::ceil(t.ratio * static_cast<double>(llm))), 1);
     }
     it.tools[j].dispatched = now;
+    note(r, "dispatch_tool iteration=" + std::to_string(i) + " tool=" + std::to_string(j) + " name=" + t.name);
     sim.loop.at(now + lat, [this, r, i, j] { on_tool_done(r, i, j); });
   }
   void on_tool_done(size_t r, size_t i, size_t j) {
     IterRt& it = reqs[r].iters[i];
     it.tools[j].done = true;
     it.pending -= 1;
+    note(r, "tool_complete iteration=" + std::to_string(i) + " tool=" + std::to_string(j));
     advance(r, i);
   }
   void submit_partial(size_t r, size_t i) {
@@ -605,22 +852,28 @@ struct Orchestrator {
     c.agentic_arrival = trace[r].arrival;
     c.iteration = static_cast<int32_t>(next);
     c.stream_key = stream_key(r, next);
-    c.on_pin_failed = [this, r](Time) { reqs[r].continuation.reset(); };
+    c.on_pin_failed = [this, r, next](Time) {
+      reqs[r].continuation.reset();
+      note(r, "partial_pin_failed iteration=" + std::to_string(next));
+    };
     const int64_t id = sim.submit(std::move(c));
     req.continuation = id;
     req.continuation_for = next;
     req.iters[next].call = id;
+    note(r, "submit_partial iteration=" + std::to_string(next));
   }
   void on_decoded(size_t r, size_t i, Time at) {
     ReqRt& req = reqs[r];
     IterRt& it = req.iters[i];
     const Iter& spec = trace[r].iters[i];
     it.decoded = true;
+    note(r, "decode_complete iteration=" + std::to_string(i));
     if (spec.final) {
       req.done = true;
+      note(r, "request_done");
       return;
     }
-    if (!sim.streaming || it.next_dispatch < spec.tools.size()) {
+    if (!sim.streaming || it.fallback || it.next_dispatch < spec.tools.size()) {
       for (size_t j = it.next_dispatch; j < spec.tools.size(); ++j) dispatch(r, i, j, at, spec.tools[j].emit);
       it.next_dispatch = spec.tools.size();
     }
@@ -638,7 +891,10 @@ struct Orchestrator {
     reqs.resize(trace.size());
     for (size_t r = 0; r < trace.size(); ++r) {
       reqs[r].iters.resize(trace[r].iters.size());
-      sim.loop.at(trace[r].arrival, [this, r] { submit_iteration(r, 0); });
+      sim.loop.at(trace[r].arrival, [this, r] {
+        note(r, "arrival");
+        submit_iteration(r, 0);
+      });
     }
     sim.loop.run();
   }
