@@ -396,12 +396,27 @@ def run_reference(args, rank, world):
     v = float(np.mean([x["value"] for x in timed]))
     cb = dict(timed[-1])
     cb["value"] = v
+    trace = None
+    try:  # the reference's own replay of the same synthetic agent trace (its CPU simulator)
+        from oracle import oracle as O
+
+        res = {}
+        for name, preset in (("sutradhara", 2), ("baseline", 0)):
+            ftr, e2e, hit, prm, ev, wall = O.ref_run_trace(TRACE["n_requests"], TRACE["seed"], preset,
+                                                           TRACE["capacity_blocks"], 16)
+            f = np.sort(ftr)
+            res[name] = {"p50_ftr_ms": float(f[max(1, int(np.ceil(0.5 * len(f)))) - 1]),
+                         "hit_rate": float(hit.sum()) / float(prm.sum()), "evictions": ev, "replay_wall_s": wall}
+        trace = res
+    except Exception as e:  # pragma: no cover
+        trace = {"unavailable": str(e)}
     return {
         "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean([x["step_s_extrapolated"] for x in timed])),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "configs[1] (same requests/tokens as our arm)", "host_threads": cb["cores"]},
-        "impl": "reference", "cpu_baseline": cb,
+        "impl": "reference", "cpu_baseline": cb, "trace": trace,
+        "p50_ftr_ms": trace.get("sutradhara", {}).get("p50_ftr_ms") if isinstance(trace, dict) else None,
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
