@@ -165,3 +165,31 @@ def test_batch_apis_match_sequential_oracle():
     torch.cuda.synchronize()
     assert hits.cpu().tolist() == exp_hits
     assert c.dump() == o.dump()
+
+
+@pytest.mark.gpu
+def test_large_pool_cooperative_scorer():
+    """Pools of >= 65536 blocks use the all-SM cooperative scorer
+    (k_select_coop): eviction order, insert ids under pressure and the full
+    dump must still equal the oracle."""
+    bs, cap = 1, 70000
+    c = product(bs, cap, 1)
+    o = O.OracleCache(bs, cap, 1)
+    rng = np.random.default_rng(21)
+    live = []
+    for k in range(34):
+        t = O.materialize(int(rng.integers(4)), 2000, 500 + k)
+        tags = [(0, 1000, int(rng.integers(6))), (1000, 2000, int(rng.integers(6)))]
+        a, b = o.insert(t, tags, k), c.insert(t, tags, k)
+        assert a == b, k
+        live.append(a[1])
+    for ids in live[::2]:
+        assert o.release(ids) == c.release(ids) == 0
+    for needed in (1, 777, 5000):
+        assert o.evict(needed) == c.evict(needed), needed
+    for k in range(2):  # inserts that must evict
+        t = O.materialize(1, 3000, 900 + k)
+        tags = [(0, 3000, 1)]
+        assert o.insert(t, tags, 100 + k) == c.insert(t, tags, 100 + k)
+    assert o.dump() == c.dump()
+    assert o.total_evicted() == c.total_evicted()
