@@ -9,7 +9,7 @@ Algorithmic bytes per unit:
   chain hash     8 B read per token + 8 B written per block
   lookup         per full block position: 128 B query tokens + 128 B stored
                  tokens + 20 B block metadata + 12 B index slot
-  evict scoring  per pool block: ntok/ref/pinned/tag (16 B) + last (8 B)
+  evict scoring  per pool block: ntok/ref/pinned/tag/exclusion mark (20 B) + last (8 B)
   kv append      per token and layer: 2 x H_kv x 128 x 2 B read + same written
 """
 from __future__ import annotations
@@ -30,25 +30,105 @@ def peaks():
     return json.load(open(p)) if os.path.exists(p) else {"hbm_gbs": 6650.0}
 
 
-def timed(fn, reps=10, warm=3):
+_FLUSH = None
+
+
+def flush_l2():
+    """Overwrite a buffer twice the size of L2 so the next launch reads HBM."""
     import torch
+
+    global _FLUSH
+    if _FLUSH is None:
+        _FLUSH = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
+    _FLUSH.fill_(1)
+
+
+def timed(fn, reps=10, warm=3, kernels=(), flush=False):
+    """Median CUDA-event time of fn() and, via the CUDA profiler (CUPTI
+    activity records, no replay), the mean device duration of each kernel
+    whose name contains one of `kernels`."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
 
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
     for a, b in ev:
+        if flush:
+            flush_l2()
         a.record()
         fn()
         b.record()
     torch.cuda.synchronize()
-    return float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e-3
+    api = float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e-3
+    dev = {}
+    if kernels:
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            for _ in range(reps):
+                if flush:
+                    flush_l2()
+                fn()
+            torch.cuda.synchronize()
+        for e in prof.key_averages():
+            for k in kernels:
+                if k in e.key and e.count:
+                    d = dev.setdefault(k, [0.0, 0])
+                    d[0] += e.device_time_total * 1e-6
+                    d[1] += e.count
+        dev = {k: v[0] / v[1] for k, v in dev.items()}
+    return api, dev
 
 
-def emit(kernel, config, bytes_, sec, hbm):
+def emit(kernel, config, bytes_, api_s, dev_s, hbm, launches=1):
+    """frac uses the kernel's own device time when the profiler saw it."""
+    sec = dev_s * launches if dev_s else api_s
     gbs = bytes_ / sec / 1e9
-    print(json.dumps({"kernel": kernel, "config": config, "seconds": sec, "algorithmic_bytes": bytes_,
+    print(json.dumps({"kernel": kernel, "config": config, "seconds": sec, "api_seconds": api_s,
+                      "timing": "kernel (CUPTI)" if dev_s else "api (CUDA events)", "algorithmic_bytes": bytes_,
                       "achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm}), flush=True)
+
+
+def fill_pool(L, cache, dev, n_seqs, toks, st):
+    """Insert n_seqs random prompts of toks tokens (one SYSTEM tag range each),
+    then release them: every block resident with ref 0 (an eviction candidate)."""
+    import torch
+    from paper_2601_12967_b200 import _lib
+
+    p = lambda t: C.c_void_p(t.data_ptr())
+    n = n_seqs * toks
+    tokens = torch.randint(0, 2**62, (n,), dtype=torch.int64, device=dev)
+    seq_off = torch.arange(0, n + 1, toks, dtype=torch.int64, device=dev)
+    blk_off = torch.arange(0, n // 16 + 1, toks // 16, dtype=torch.int64, device=dev)
+    blk_off_h = np.arange(0, n // 16 + 1, toks // 16, dtype=np.int64)
+    tags = (_lib.TagRange * n_seqs)()
+    for i in range(n_seqs):
+        tags[i].begin, tags[i].end, tags[i].tag = 0, toks, 3
+    tag_dev = torch.frombuffer(bytearray(tags), dtype=torch.uint8).to(dev)
+    tag_off = torch.arange(n_seqs + 1, dtype=torch.int64, device=dev)
+    ids = torch.empty(n // 16, dtype=torch.int32, device=dev)
+    status = torch.empty(n_seqs, dtype=torch.int32, device=dev)
+    _lib.check(L.sb_kv_insert_batch(cache.handle, p(tokens), p(seq_off), p(tag_dev), p(tag_off), p(blk_off),
+                                    blk_off_h.ctypes.data_as(_lib.I64P), None, n_seqs, 1, p(ids), p(status), st))
+    _lib.check(L.sb_kv_release_batch(cache.handle, p(ids), n // 16, None, st))
+    torch.cuda.synchronize()
+
+
+def evict_bench(L, cache, cap, hbm):
+    from paper_2601_12967_b200 import _lib
+
+    for needed in (64, 4096):
+        def ev():
+            out = np.zeros(needed, dtype=np.int32)
+            k = C.c_int64(0)
+            L.sb_kv_evict(cache.handle, needed, out.ctypes.data_as(_lib.I32P), C.byref(k))
+        res = cache.resident_blocks()
+        api, kt = timed(ev, reps=5, warm=1, kernels=("k_plan", "k_score", "k_select_coop"), flush=True)
+        cfg = f"pool {cap} blocks, ~{res} resident (all candidates), evict {needed}"
+        # scoring: 24 B of metadata read per pool block (ntok/ref/pinned/tag + last) + one 8 B key per candidate
+        emit("k_score (hint-aware eviction scoring)", cfg, cap * 24 + res * 8, api, kt.get("k_score"), hbm)
+        tot = sum(kt.get(k, 0.0) for k in ("k_plan", "k_score", "k_select_coop"))
+        emit("evict total (k_plan + k_score + k_select_coop)", cfg, cap * 24 + res * 8, api, tot or None, hbm)
 
 
 def main():
@@ -63,14 +143,17 @@ def main():
     st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
     # ---- chain hashing: latency-bound per sequence, throughput over sequences
-    for n_seqs, toks in ((64, 8192), (4096, 1024), (65536, 512)):
+    for n_seqs, toks in ((64, 8192), (4096, 1024), (65536, 512), (262144, 128)):
         n = n_seqs * toks
         tokens = torch.randint(0, 2**62, (n,), dtype=torch.int64, device=dev)
         seq_off = torch.arange(0, n + 1, toks, dtype=torch.int64, device=dev)
         blk_off = torch.arange(0, n // 16 + 1, toks // 16, dtype=torch.int64, device=dev)
         out = torch.empty(n // 16, dtype=torch.int64, device=dev)
-        sec = timed(lambda: L.sb_chain_hash_batch(p(tokens), p(seq_off), p(blk_off), None, n_seqs, 16, p(out), st))
-        emit("k_chain_hash", f"{n_seqs} seqs x {toks} tokens", 8 * n + 8 * (n // 16), sec, hbm)
+        api, kt = timed(lambda: L.sb_chain_hash_batch(p(tokens), p(seq_off), p(blk_off), None, n_seqs, 16, p(out), st),
+                         kernels=("k_chain_hash16",), flush=True)
+        emit("k_chain_hash16", f"{n_seqs} seqs x {toks} tokens", 8 * n + 8 * (n // 16), api,
+             kt.get("k_chain_hash16"), hbm)
+        del tokens
 
     # ---- batched lookup over a populated pool (all-hit prefixes)
     cap = 1 << 20
@@ -96,22 +179,21 @@ def main():
     _lib.check(L.sb_kv_release_batch(cache.handle, p(ids), n // 16, None, st))
     torch.cuda.synchronize()
     hits = torch.empty(n_seqs, dtype=torch.int64, device=dev)
-    sec = timed(lambda: L.sb_kv_lookup_prefix_batch(cache.handle, p(tokens), p(seq_off), p(blk_off),
-                                                    blk_off_h.ctypes.data_as(_lib.I64P), p(hashes), n_seqs, 2,
-                                                    p(hits), st))
+    api, kt = timed(lambda: L.sb_kv_lookup_prefix_batch(cache.handle, p(tokens), p(seq_off), p(blk_off),
+                                                         blk_off_h.ctypes.data_as(_lib.I64P), p(hashes), n_seqs, 2,
+                                                         p(hits), st), kernels=("k_probe_batch",), flush=True)
     assert int(hits.sum()) == n
-    emit("k_probe_batch (+init/finish)", f"{n_seqs} seqs x {toks} tokens, pool {cap} blocks, all hit",
-         (n // 16) * (128 + 128 + 20 + 12), sec, hbm)
+    emit("k_probe_batch", f"{n_seqs} seqs x {toks} tokens, pool {cap} blocks, all hit",
+         (n // 16) * (128 + 128 + 20 + 12), api, kt.get("k_probe_batch"), hbm)
 
-    # ---- eviction scoring at pool scale: evict() = score + select + sort
-    for needed in (64, 4096):
-        def ev():
-            out = np.zeros(needed, dtype=np.int32)
-            k = C.c_int64(0)
-            L.sb_kv_evict(cache.handle, needed, out.ctypes.data_as(_lib.I32P), C.byref(k))
-        sec = timed(ev, reps=5, warm=1)
-        emit("k_select (evict)", f"pool {cap} blocks, {cache.resident_blocks()} resident, evict {needed}",
-             cap * 24, sec, hbm)
+    # ---- eviction at pool scale: evict() = k_plan + k_score (HBM pass) + k_select_coop
+    evict_bench(L, cache, cap, hbm)
+    del cache
+    big = 1 << 21
+    cache2 = KvCache(CacheConfig(16, big, 1))
+    fill_pool(L, cache2, dev, 1024, 16384, st)
+    evict_bench(L, cache2, big, hbm)
+    del cache2
 
     # ---- KV append (Llama-3-8B kv heads), one layer
     tok_n, hkv, pages = 98896, 8, 27281
@@ -122,9 +204,10 @@ def main():
     q_off = torch.tensor([0, tok_n], dtype=torch.int32, device=dev)
     kv_len = torch.tensor([tok_n], dtype=torch.int32, device=dev)
     table = torch.randperm(pages, device=dev)[: (tok_n + 15) // 16].to(torch.int32).reshape(1, -1).contiguous()
-    sec = timed(lambda: L.sb_kv_append(p(k_new), p(v_new), p(kp), p(vp), p(q_off), p(kv_len), p(table), 1,
-                                       table.shape[1], hkv, 128, 16, st))
-    emit("k_kv_append", f"{tok_n} tokens x {hkv} kv heads", 2 * 2 * tok_n * hkv * 128 * 2, sec, hbm)
+    api, kt = timed(lambda: L.sb_kv_append(p(k_new), p(v_new), p(kp), p(vp), p(q_off), p(kv_len), p(table), 1,
+                                            table.shape[1], hkv, 128, 16, st), kernels=("k_kv_append",), flush=True)
+    emit("k_kv_append", f"{tok_n} tokens x {hkv} kv heads", 2 * 2 * tok_n * hkv * 128 * 2, api,
+         kt.get("k_kv_append"), hbm)
 
 
 if __name__ == "__main__":

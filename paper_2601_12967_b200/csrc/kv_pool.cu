@@ -104,22 +104,7 @@ __device__ __forceinline__ uint64_t victim_key(const Pool& P, int32_t id) {
   return k;
 }
 
-// Resident block with (chain_hash, parent_hash, tokens), -1 if none
-// (find_chain_block, kv_cache.cpp:403-416).
-__device__ int32_t probe_find(const Pool& P, uint64_t h, uint64_t parent, const uint64_t* __restrict__ t, int len) {
-  uint64_t s = index_slot(h, P.tcap);
-  for (;;) {
-    const int32_t id = P.tval[s];
-    if (id == -1) return -1;
-    if (id >= 0 && P.tkey[s] == h && P.ntok[id] == len && P.parent[id] == parent) {
-      const uint64_t* bt = P.tok + static_cast<int64_t>(id) * P.bs;
-      bool eq = true;
-      for (int i = 0; i < len; ++i) eq &= (bt[i] == t[i]);
-      if (eq) return id;
-    }
-    s = (s + 1) & static_cast<uint64_t>(P.tcap - 1);
-  }
-}
+// find_chain_block (kv_cache.cpp:403-416) is probe_find_g8 below.
 
 __device__ void index_insert(const Pool& P, uint64_t h, int32_t id) {
   uint64_t s = index_slot(h, P.tcap);
@@ -166,50 +151,217 @@ __global__ void k_chain_hash(const uint64_t* __restrict__ tokens, const int64_t*
   }
 }
 
+// 16-token blocks: a warp hashes 32 sequences (one per lane) but loads their
+// tokens cooperatively — each warp load instruction covers the current block
+// of two sequences (16 lanes x 8 B, contiguous), staged through shared memory
+// and prefetched one block ahead in registers — instead of 32 scattered 8 B
+// loads per instruction (which made the per-lane fold L1-wavefront bound).
+constexpr int kHashWarps = 2;
+__global__ void __launch_bounds__(32 * kHashWarps)
+    k_chain_hash16(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ seq_off,
+                   const int64_t* __restrict__ blk_off, const uint64_t* __restrict__ parent0, int n_seqs,
+                   int full_only, uint64_t* __restrict__ out) {
+  __shared__ uint64_t stage[kHashWarps][32][17];  // 17-word rows: conflict-free per half warp
+  __shared__ int64_t seq_b[kHashWarps][32], seq_e[kHashWarps][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = (blockIdx.x * kHashWarps + w) * 32 + lane;
+  int64_t b = 0, e = 0, ob = 0, nblk = 0;
+  uint64_t h = kRootHash;
+  if (s < n_seqs) {
+    b = seq_off[s];
+    e = seq_off[s + 1];
+    ob = blk_off[s];
+    if (parent0) h = parent0[s];
+    nblk = full_only ? (e - b) / 16 : (e - b + 15) / 16;
+  }
+  seq_b[w][lane] = b;
+  seq_e[w][lane] = e;
+  const int nb_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(nblk)));
+  __syncwarp();
+  const int half = lane >> 4, k = lane & 15;
+  uint64_t v[16];
+  auto load = [&](int64_t j) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int q = 2 * r + half;
+      const int64_t pos = seq_b[w][q] + 16 * j + k;
+      v[r] = pos < seq_e[w][q] ? __ldg(reinterpret_cast<const unsigned long long*>(tokens + pos)) : 0ull;
+    }
+  };
+  if (nb_max > 0) load(0);
+  for (int j = 0; j < nb_max; ++j) {
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) stage[w][2 * r + half][k] = v[r];
+    __syncwarp();
+    if (j + 1 < nb_max) load(j + 1);
+    if (j < nblk) {
+      const int64_t len = e - (b + 16 * static_cast<int64_t>(j));
+      if (len >= 16) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) h = chain_step(h, stage[w][lane][i] + kGolden);
+      } else {
+        for (int i = 0; i < len; ++i) h = chain_step(h, stage[w][lane][i] + kGolden);
+      }
+      out[ob + j] = h;
+    }
+  }
+}
+
+static void launch_chain_hash(const uint64_t* tokens, const int64_t* seq_off, const int64_t* blk_off,
+                              const uint64_t* parent0, int n_seqs, int64_t bs, int full_only, uint64_t* out,
+                              cudaStream_t st) {
+  if (n_seqs <= 0) return;
+  if (bs == 16) {
+    const int per = 32 * kHashWarps;
+    k_chain_hash16<<<(n_seqs + per - 1) / per, per, 0, st>>>(tokens, seq_off, blk_off, parent0, n_seqs, full_only,
+                                                              out);
+  } else {
+    k_chain_hash<<<(n_seqs + 63) / 64, 64, 0, st>>>(tokens, seq_off, blk_off, parent0, n_seqs, bs, full_only, out);
+  }
+}
+
 // --------------------------------------------------------------- lookups
-__device__ __forceinline__ int find_seq(const int64_t* __restrict__ blk_off, int n_seqs, int64_t g) {
-  int lo = 0, hi = n_seqs;  // blk_off[lo] <= g < blk_off[hi]
+
+// Group probe: the kGroup lanes of an aligned lane group look up ONE block
+// position together.  They walk the index identically (same addresses, one
+// transaction per load), fetch the slot's id and key together, then load the
+// candidate block's metadata and its tokens at once (lane i compares tokens
+// i, i+kGroup, ... of the block) and vote.  The dependent chain per position
+// is chain hash -> index slot -> (metadata + tokens).
+constexpr int kGroup = 4;
+__device__ __forceinline__ int32_t ld_keep_i32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_keep_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ int32_t probe_find_g(const Pool& P, uint64_t h, uint64_t parent, const uint64_t* __restrict__ t, int len,
+                                int part, unsigned gmask) {
+  constexpr int R = 16 / kGroup;  // tokens per lane of a 16-token block
+  uint64_t tq[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = part + kGroup * r;
+    tq[r] = i < len ? t[i] : 0ull;
+  }
+  uint64_t s = index_slot(h, P.tcap);
+  for (;;) {
+    // both halves of the slot in flight together (volatile: not sunk below the branch)
+    const int32_t id = ld_keep_i32(P.tval + s);
+    const uint64_t key = ld_keep_u64(P.tkey + s);
+    if (id == -1) return -1;
+    if (id >= 0 && key == h) {
+      const uint64_t* bt = P.tok + static_cast<int64_t>(id) * P.bs;
+      const int nt = P.ntok[id];
+      const uint64_t par = P.parent[id];
+      bool eq = true;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = part + kGroup * r;
+        if (i < len) eq &= bt[i] == tq[r];
+      }
+      for (int i = part + 16; i < len; i += kGroup) eq &= bt[i] == t[i];
+      if (__all_sync(gmask, eq && nt == len && par == parent)) return id;
+    }
+    s = (s + 1) & static_cast<uint64_t>(P.tcap - 1);
+  }
+}
+
+// Warp-wide 32-ary search: s with blk_off[s] <= x < blk_off[s + 1]
+// (requires blk_off[0] <= x < blk_off[n]).  All 32 lanes call it with the
+// same x; two rounds cover 1000+ sequences.
+__device__ __forceinline__ int warp_search(const int64_t* __restrict__ blk_off, int n, int64_t x) {
+  const int lane = threadIdx.x & 31;
+  int lo = 0, hi = n;
   while (hi - lo > 1) {
-    int mid = (lo + hi) >> 1;
-    if (blk_off[mid] <= g) lo = mid; else hi = mid;
+    const int64_t span = hi - lo;
+    const int piv = lo + static_cast<int>((span * (lane + 1)) / 33);  // in [lo, hi), nondecreasing in lane
+    const unsigned m = __ballot_sync(0xffffffffu, blk_off[piv] <= x);
+    const int k = __popc(m);
+    const int a = __shfl_sync(0xffffffffu, piv, k > 0 ? k - 1 : 0);
+    const int b = __shfl_sync(0xffffffffu, piv, k < 32 ? k : 31);
+    const int nlo = k > 0 ? a : lo, nhi = k < 32 ? b : hi;
+    lo = nlo;
+    hi = nhi;
   }
   return lo;
 }
 
-// Pre-state probe of every block position of a batch of sequences.
-__global__ void k_probe_batch(Pool P, const uint64_t* __restrict__ tokens, const int64_t* __restrict__ seq_off,
-                              const int64_t* __restrict__ blk_off, int n_seqs, const uint64_t* __restrict__ hashes,
-                              int64_t total_blocks, int32_t* __restrict__ prehit, int64_t* __restrict__ first_miss,
-                              int full_only_check) {
-  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (g >= total_blocks) return;
-  const int s = find_seq(blk_off, n_seqs, g);
+// Sequence of position g for every lane of a warp whose positions ascend
+// with the lane: bracket the warp's range with two warp searches, then a
+// per-lane binary search inside the bracket (usually empty).
+__device__ __forceinline__ int find_seq_warp(const int64_t* __restrict__ blk_off, int n_seqs, int64_t g,
+                                             int64_t total) {
+  const int64_t gc = min(g, total - 1);
+  const int64_t g0 = __shfl_sync(0xffffffffu, gc, 0), g1 = __shfl_sync(0xffffffffu, gc, 31);
+  int lo = warp_search(blk_off, n_seqs, g0);
+  int hi = warp_search(blk_off, n_seqs, g1) + 1;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (blk_off[mid] <= gc) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Pre-state probe of every block position of a batch of sequences
+// (kGroup lanes per position).
+__global__ void __launch_bounds__(256) k_probe_batch(Pool P, const uint64_t* __restrict__ tokens,
+                                                     const int64_t* __restrict__ seq_off,
+                                                     const int64_t* __restrict__ blk_off, int n_seqs,
+                                                     const uint64_t* __restrict__ hashes, int64_t total_blocks,
+                                                     int32_t* __restrict__ prehit, int64_t* __restrict__ first_miss,
+                                                     int full_only_check) {
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t g = tid / kGroup;
+  const int part = threadIdx.x % kGroup;
+  const unsigned gmask = ((1u << kGroup) - 1) << (threadIdx.x & 31 & ~(kGroup - 1));
+  if (blockIdx.x * static_cast<int64_t>(blockDim.x) / kGroup + (threadIdx.x & ~31) / kGroup >= total_blocks) return;
+  // chain hashes do not depend on the sequence: in flight before the search
+  const int64_t gc = min(g, total_blocks - 1);
+  const uint64_t h = hashes[gc];
+  const uint64_t hprev = gc ? hashes[gc - 1] : kRootHash;
+  const int s = find_seq_warp(blk_off, n_seqs, g, total_blocks);  // whole warp
+  if (g >= total_blocks) return;  // uniform per group
   const int64_t j = g - blk_off[s];
   const int64_t base = seq_off[s] + j * P.bs;
   const int len = static_cast<int>(min(P.bs, seq_off[s + 1] - base));
   if (full_only_check && len < P.bs) {  // lookups never match a partial block (kv_cache.cpp:423)
-    prehit[g] = -1;
-    if (first_miss) atomicMin(reinterpret_cast<unsigned long long*>(first_miss + s), static_cast<unsigned long long>(j));
+    if (part == 0) {
+      prehit[g] = -1;
+      if (first_miss) atomicMin(reinterpret_cast<unsigned long long*>(first_miss + s), static_cast<unsigned long long>(j));
+    }
     return;
   }
-  const uint64_t parent = j ? hashes[g - 1] : kRootHash;
-  const int32_t id = probe_find(P, hashes[g], parent, tokens + base, len);
-  prehit[g] = id;
-  if (id < 0 && first_miss) atomicMin(reinterpret_cast<unsigned long long*>(first_miss + s), static_cast<unsigned long long>(j));
+  const uint64_t parent = j ? hprev : kRootHash;
+  const int32_t id = probe_find_g(P, h, parent, tokens + base, len, part, gmask);
+  if (part == 0) {
+    prehit[g] = id;
+    if (id < 0 && first_miss)
+      atomicMin(reinterpret_cast<unsigned long long*>(first_miss + s), static_cast<unsigned long long>(j));
+  }
 }
 
-// Pre-state probe of the block positions of insert sequence s.
+// Pre-state probe of the block positions of insert sequence s (kGroup lanes
+// per position).
 __global__ void k_probe_seq(Pool P, const uint64_t* __restrict__ tokens, const int64_t* __restrict__ seq_off,
                             const int64_t* __restrict__ blk_off, const uint64_t* __restrict__ hashes, int s,
                             int32_t* __restrict__ prehit) {
   const int64_t b0 = blk_off[s];
   const int64_t np = blk_off[s + 1] - b0;
-  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / kGroup;
+  const int part = threadIdx.x % kGroup;
+  const unsigned gmask = ((1u << kGroup) - 1) << (threadIdx.x & 31 & ~(kGroup - 1));
   if (p >= np) return;
   const int64_t base = seq_off[s] + p * P.bs;
   const int len = static_cast<int>(min(P.bs, seq_off[s + 1] - base));
   const uint64_t parent = p ? hashes[b0 + p - 1] : kRootHash;
-  prehit[b0 + p] = probe_find(P, hashes[b0 + p], parent, tokens + base, len);
+  const int32_t id = probe_find_g(P, hashes[b0 + p], parent, tokens + base, len, part, gmask);
+  if (part == 0) prehit[b0 + p] = id;
 }
 
 __global__ void k_lookup_init(const int64_t* __restrict__ blk_off, int n_seqs, int64_t* first_miss) {
@@ -228,8 +380,9 @@ __global__ void k_lookup_finish(Pool P, const int64_t* __restrict__ seq_off, con
     atomicAdd(&P.ctr[C_HIT_TOK], static_cast<unsigned long long>(first_miss[g] * P.bs));
     atomicAdd(&P.ctr[C_LOOK_TOK], static_cast<unsigned long long>(seq_off[g + 1] - seq_off[g]));
   }
+  if (total_blocks == 0 || blockIdx.x * static_cast<int64_t>(blockDim.x) + (threadIdx.x & ~31) >= total_blocks) return;
+  const int s = find_seq_warp(blk_off, n_seqs, g, total_blocks);  // whole warp
   if (g >= total_blocks) return;
-  const int s = find_seq(blk_off, n_seqs, g);
   if (g - blk_off[s] < first_miss[s]) P.last[prehit[g]] = now;
 }
 
@@ -304,6 +457,71 @@ __device__ void bitonic_global(uint64_t* a, int64_t n) {
       __syncthreads();
     }
   }
+}
+
+// Hint-aware eviction scoring of pool blocks [lo, hi) (lo % 4 == 0): every
+// field the decision needs is read with 16 B vector loads, unconditionally
+// (no dependent short-circuit loads), and the keys (tier, last_used, id) of
+// the candidates — resident, ref 0, unpinned, not excluded (rank_of -2) —
+// are appended with one shared/global atomic per warp and element slot.
+template <int U, bool kRank, class Emit>
+__device__ __forceinline__ void score_slice(const Pool& P, const int32_t* rank_of, int64_t lo, int64_t hi, Emit emit) {
+  const int64_t hi4 = lo + ((hi - lo) & ~int64_t(3));
+  const bool tiered = P.policy == SB_POLICY_TIERED;
+  auto one = [&](int32_t id, int nt, int rf, int pn, int rk, int tg, int64_t last) {
+    const bool c = nt > 0 && rf == 0 && pn == 0 && rk != -2;
+    uint64_t k = (static_cast<uint64_t>(last + kLastBias) << kIdBits) | static_cast<uint64_t>(id);
+    if (tiered) k |= static_cast<uint64_t>(tier_of(tg)) << 61;
+    emit(c, k, nt == 0);
+  };
+  // U 4-block groups per thread in flight before any decision
+  const int64_t step = 4 * static_cast<int64_t>(blockDim.x);
+  for (int64_t i0 = lo + 4 * static_cast<int64_t>(threadIdx.x); i0 < hi4; i0 += U * step) {
+    int4 nt[U], rf[U], pn[U], rk[U], tg[U];
+    longlong2 l0[U], l1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * step;
+      if (i < hi4) {
+        nt[u] = *reinterpret_cast<const int4*>(P.ntok + i);
+        rf[u] = *reinterpret_cast<const int4*>(P.ref + i);
+        pn[u] = *reinterpret_cast<const int4*>(P.pinned + i);
+        if (kRank) rk[u] = *reinterpret_cast<const int4*>(rank_of + i);
+        else rk[u] = make_int4(0, 0, 0, 0);
+        tg[u] = *reinterpret_cast<const int4*>(P.tag + i);
+        l0[u] = *reinterpret_cast<const longlong2*>(P.last + i);
+        l1[u] = *reinterpret_cast<const longlong2*>(P.last + i + 2);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * step;
+      if (i < hi4) {
+        const int32_t id = static_cast<int32_t>(i);
+        one(id, nt[u].x, rf[u].x, pn[u].x, rk[u].x, tg[u].x, l0[u].x);
+        one(id + 1, nt[u].y, rf[u].y, pn[u].y, rk[u].y, tg[u].y, l0[u].y);
+        one(id + 2, nt[u].z, rf[u].z, pn[u].z, rk[u].z, tg[u].z, l1[u].x);
+        one(id + 3, nt[u].w, rf[u].w, pn[u].w, rk[u].w, tg[u].w, l1[u].y);
+      }
+    }
+  }
+  for (int64_t i = hi4 + threadIdx.x; i < hi; i += blockDim.x)
+    one(static_cast<int32_t>(i), P.ntok[i], P.ref[i], P.pinned[i], kRank ? rank_of[i] : 0, P.tag[i], P.last[i]);
+}
+
+// Warp-aggregated append: one atomic per warp for the set lanes.
+template <class Counter>
+__device__ __forceinline__ uint64_t warp_append_slot(bool c, Counter* cnt, bool& mine) {
+  const unsigned act = __activemask();
+  const unsigned m = __ballot_sync(act, c);
+  mine = c;
+  if (!m) return 0;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  uint64_t base = 0;
+  if (lane == leader) base = static_cast<uint64_t>(atomicAdd(cnt, static_cast<Counter>(__popc(m))));
+  base = __shfl_sync(act, base, leader);
+  return base + __popc(m & ((1u << lane) - 1));
 }
 
 // Tag coverage check (kv_cache.cpp:438-448): ranges must tile [0, n).
@@ -398,13 +616,13 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
   }
   // ---- score every block, compact the candidates
   // (first into shared memory; overflow keeps going into global S.keys)
-  for (int64_t i = t; i < P.cap; i += blockDim.x) {
-    const int32_t id = static_cast<int32_t>(i);
-    if (!is_candidate(P, id) || S.rank_of[id] == -2) continue;
-    const unsigned long long at = atomicAdd(&n_cand, 1ull);
-    const uint64_t k = victim_key(P, id);
-    if (at < kCandSmem) cand_s[at] = k; else S.keys[at - kCandSmem] = k;
-  }
+  score_slice<1, true>(P, S.rank_of, 0, P.cap, [&](bool c, uint64_t k, bool) {
+    bool mine;
+    const uint64_t at = warp_append_slot(c, &n_cand, mine);
+    if (mine) {
+      if (at < kCandSmem) cand_s[at] = k; else S.keys[at - kCandSmem] = k;
+    }
+  });
   __syncthreads();
   if (mode == 0)
     for (int64_t p = t; p < f; p += blockDim.x) S.rank_of[S.prehit[b0 + p]] = -1;
@@ -530,15 +748,138 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
 // pre-miss position on.  Single thread: each step is a handful of
 // L1/L2-resident accesses.
 // ---------------------------------------------------------------------------
-// Cooperative (all-SM) variant of k_select for large pools: every CTA scores
-// its slice of the pool once (the only HBM pass: 24 B per block) and keeps
-// its candidate keys in shared memory; the radix passes exchange 2048-bin
-// histograms through global memory between grid barriers; CTA 0 sorts the
-// selected keys.  Same outputs as k_select.
+// Large pools (>= kCoopMinCap blocks): the same decisions as k_select, split
+// into three kernels so the HBM pass runs on every SM at streaming rate:
+//   k_plan         1 CTA: first miss, tag check, exclusion marks, late
+//                  candidates (phase A of k_select)
+//   k_score        all SMs: hint-aware key (tier, last_used, id) of every
+//                  block (24 B read per block, 16 B vectors), candidates
+//                  compacted per CTA in shared memory then appended to a
+//                  global key list; free blocks counted per slice; key range
+//   k_select_coop  cooperative: radix select of the K smallest keys from the
+//                  highest differing bit of the key range (histograms
+//                  exchanged between grid barriers), CTA 0 sorts them; the
+//                  lowest free ids are listed in parallel from the per-slice
+//                  free counts.
 struct CoopBuf {
-  uint32_t* hist;              // [6][2048]
-  unsigned long long* ctr;     // [0] candidates, [1] selected, [2] pre-hit candidates
+  uint32_t* hist;            // [6][2048]
+  unsigned long long* ctr;   // [0] candidates [1] selected [2] pre-hit candidates [3] min key [4] max key
+  uint64_t* keys;            // candidate keys, slice sl at [sl * slice, + ncnt[sl])
+  uint32_t* fcnt;            // free blocks per score slice, [n_slices]
+  uint32_t* ncnt;            // candidates per score slice, [n_slices]
+  uint64_t* kmin;            // smallest / largest candidate key per slice, [n_slices]
+  uint64_t* kmax;
+  int n_slices;
+  int64_t slice;             // blocks per score slice (multiple of 4)
 };
+constexpr int kScoreThreads = 512;
+constexpr int kSlicesPerSm = 2;  // k_score CTAs per SM (one wave)
+
+__global__ void __launch_bounds__(kSelectThreads, 1)
+    k_plan(Pool P, Scratch S, InsertArgs A, int s, int mode, CoopBuf G) {
+  __shared__ int64_t first;
+  const int t = threadIdx.x;
+  for (int i = t; i < 6 * 2048; i += blockDim.x) G.hist[i] = 0;
+  if (t < 3) G.ctr[t] = 0;
+  if (t == 3) G.ctr[3] = ~0ull;
+  if (t == 4) G.ctr[4] = 0;
+  if (mode != 0) {
+    if (t == 0) {
+      S.scal[S_F] = 0;
+      S.scal[S_STATUS] = 0;
+    }
+    return;
+  }
+  const int64_t b0 = A.blk_off[s];
+  const int64_t P_ = A.blk_off[s + 1] - b0;
+  const int64_t n = A.seq_off[s + 1] - A.seq_off[s];
+  const bool ok = tags_cover(A.tags + A.tag_off[s], A.tag_off[s + 1] - A.tag_off[s], n);
+  if (t == 0) first = P_;
+  __syncthreads();
+  for (int64_t p = t; p < P_; p += blockDim.x)
+    if (S.prehit[b0 + p] < 0) atomicMin(reinterpret_cast<unsigned long long*>(&first), (unsigned long long)p);
+  __syncthreads();
+  const int64_t f = first;
+  if (t == 0) {
+    S.scal[S_F] = f;
+    S.scal[S_STATUS] = ok ? 0 : SB_ERR_CACHE;
+    S.scal[S_NLATE] = 0;
+    if (!ok) {
+      S.scal[S_K] = 0;
+      S.scal[S_FREE] = 0;
+    }
+  }
+  if (!ok) return;
+  for (int64_t p = t; p < P_; p += blockDim.x) {
+    const int32_t id = S.prehit[b0 + p];
+    if (p < f) {
+      S.kind[p] = 0;
+      const int32_t pn = P.pinned[id];
+      if (P.ref[id] == -1 && pn == 0) {
+        const int64_t at = atomicAdd(reinterpret_cast<unsigned long long*>(&S.scal[S_NLATE]), 1ull);
+        if (at < kLateMax) {
+          S.late[2 * at] = static_cast<int32_t>(p);
+          S.late[2 * at + 1] = id;
+        }
+      }
+      // temporary exclusion mark read by k_score (pinned blocks are never
+      // candidates), cleared by k_select_coop; blocks at distinct positions
+      // are distinct
+      P.pinned[id] = pn | 2;
+    } else if (id >= 0 && is_candidate(P, id)) {
+      atomicAdd(&G.ctr[2], 1ull);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kScoreThreads, kSlicesPerSm) k_score(Pool P, Scratch S, CoopBuf G) {
+  extern __shared__ uint64_t cand[];  // [G.slice]
+  __shared__ unsigned int n_c, n_free;
+  __shared__ unsigned long long kmin, kmax;
+  if (S.scal[S_STATUS] != 0) return;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    n_c = 0;
+    n_free = 0;
+    kmin = ~0ull;
+    kmax = 0;
+  }
+  __syncthreads();
+  const int64_t lo = blockIdx.x * G.slice, hi = min(P.cap, lo + G.slice);
+  uint64_t mn = ~0ull, mx = 0;
+  unsigned nf = 0;
+  score_slice<1, false>(P, nullptr, lo, hi, [&](bool c, uint64_t k, bool fr) {
+    bool mine;
+    const uint64_t at = warp_append_slot(c, &n_c, mine);
+    if (mine) {
+      cand[at] = k;
+      mn = min(mn, k);
+      mx = max(mx, k);
+    }
+    nf += fr;
+  });
+  nf = __reduce_add_sync(0xffffffffu, nf);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((t & 31) == 0) {
+    atomicAdd(&n_free, nf);
+    atomicMin(&kmin, mn);
+    atomicMax(&kmax, mx);
+  }
+  __syncthreads();
+  const unsigned nc = n_c;
+  if (t == 0) {
+    G.fcnt[blockIdx.x] = n_free;
+    G.ncnt[blockIdx.x] = nc;
+    G.kmin[blockIdx.x] = kmin;
+    G.kmax[blockIdx.x] = kmax;
+  }
+  uint64_t* out = G.keys + lo;  // the slice's own region: no global atomics
+  for (unsigned i = t; i < nc; i += blockDim.x) out[i] = cand[i];
+}
 
 __global__ void __launch_bounds__(kSelectThreads, 1)
     k_select_coop(Pool P, Scratch S, InsertArgs A, int s, int mode, int64_t needed, CoopBuf G) {
@@ -548,100 +889,111 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
   __shared__ uint32_t warp_sums[33];
   __shared__ int64_t sh[8];
   __shared__ uint32_t cnt_b;
-  __shared__ unsigned int n_local;
   extern __shared__ uint64_t local_keys[];
+  if (S.scal[S_STATUS] != 0) return;  // uniform across the grid
+  __shared__ unsigned long long red[3];
   const int t = threadIdx.x;
   const int cta = blockIdx.x, n_cta = gridDim.x;
-  int64_t P_ = 0, b0 = 0;
-  // ---- phase A (CTA 0): first miss, tag check, exclusions, late candidates
-  if (cta == 0) {
-    for (int i = t; i < 6 * 2048; i += blockDim.x) G.hist[i] = 0;
-    if (t < 3) G.ctr[t] = 0;
-    if (mode == 0) {
-      b0 = A.blk_off[s];
-      P_ = A.blk_off[s + 1] - b0;
-      const int64_t n = A.seq_off[s + 1] - A.seq_off[s];
-      const bool ok = tags_cover(A.tags + A.tag_off[s], A.tag_off[s + 1] - A.tag_off[s], n);
-      if (t == 0) sh[0] = P_;
-      __syncthreads();
-      for (int64_t p = t; p < P_; p += blockDim.x)
-        if (S.prehit[b0 + p] < 0) atomicMin(reinterpret_cast<unsigned long long*>(&sh[0]), (unsigned long long)p);
-      __syncthreads();
-      const int64_t f = sh[0];
-      if (t == 0) {
-        S.scal[S_F] = f;
-        S.scal[S_STATUS] = ok ? 0 : SB_ERR_CACHE;
-        S.scal[S_NLATE] = 0;
-      }
-      __syncthreads();
-      if (ok) {
-        for (int64_t p = t; p < P_; p += blockDim.x) {
-          const int32_t id = S.prehit[b0 + p];
-          if (p < f) {
-            S.kind[p] = 0;
-            S.rank_of[id] = -2;
-            if (P.ref[id] == -1 && P.pinned[id] == 0) {
-              const int64_t at = atomicAdd(reinterpret_cast<unsigned long long*>(&S.scal[S_NLATE]), 1ull);
-              if (at < kLateMax) {
-                S.late[2 * at] = static_cast<int32_t>(p);
-                S.late[2 * at + 1] = id;
-              }
-            }
-          } else if (id >= 0 && is_candidate(P, id)) {
-            atomicAdd(&G.ctr[2], 1ull);
-          }
-        }
-      }
-    } else if (t == 0) {
-      S.scal[S_F] = 0;
-      S.scal[S_STATUS] = 0;
-    }
-  }
-  grid.sync();
-  if (S.scal[S_STATUS] != 0) {
-    if (cta == 0 && t == 0) {
-      S.scal[S_K] = 0;
-      S.scal[S_FREE] = 0;
-    }
-    return;  // uniform across the grid
-  }
-  // ---- phase B (all CTAs): score the slice, keep candidate keys in smem
-  const int64_t chunk = (P.cap + n_cta - 1) / n_cta;
-  const int64_t lo = cta * chunk, hi = min(P.cap, lo + chunk);
-  if (t == 0) n_local = 0;
-  __syncthreads();
-  for (int64_t i = lo + t; i < hi; i += blockDim.x) {
-    const int32_t id = static_cast<int32_t>(i);
-    if (!is_candidate(P, id) || S.rank_of[id] == -2) continue;
-    local_keys[atomicAdd(&n_local, 1u)] = victim_key(P, id);
+  // per-slice results of k_score: total candidates and key range
+  if (t == 0) {
+    red[0] = 0;
+    red[1] = ~0ull;
+    red[2] = 0;
   }
   __syncthreads();
-  const int64_t nl = n_local;
-  if (t == 0) atomicAdd(&G.ctr[0], static_cast<unsigned long long>(nl));
-  grid.sync();
-  if (cta == 0 && mode == 0) {
-    const int64_t f = S.scal[S_F];
-    b0 = A.blk_off[s];
-    for (int64_t p = t; p < f; p += blockDim.x) S.rank_of[S.prehit[b0 + p]] = -1;
+  {
+    unsigned long long c = 0, mn = ~0ull, mx = 0;
+    for (int i = t; i < G.n_slices; i += blockDim.x)
+      if (G.ncnt[i]) {
+        c += G.ncnt[i];
+        mn = min(mn, static_cast<unsigned long long>(G.kmin[i]));
+        mx = max(mx, static_cast<unsigned long long>(G.kmax[i]));
+      }
+    if (c) {
+      atomicAdd(&red[0], c);
+      atomicMin(&red[1], mn);
+      atomicMax(&red[2], mx);
+    }
   }
-  const int64_t ncand = static_cast<int64_t>(G.ctr[0]);
+  __syncthreads();
+  const int64_t ncand = static_cast<int64_t>(red[0]);
+  const uint64_t key_lo = red[1], key_hi = red[2];
+  if (cta == 0 && mode == 0) {  // drop the exclusion marks (k_score has read them)
+    const int64_t f = S.scal[S_F], b0 = A.blk_off[s];
+    for (int64_t p = t; p < f; p += blockDim.x) P.pinned[S.prehit[b0 + p]] &= ~2;
+  }
   const int64_t free_cnt = P.cap - static_cast<int64_t>(P.ctr[C_NRES]);
   int64_t K, Fp = 0;
   if (mode == 0) {
-    P_ = A.blk_off[s + 1] - A.blk_off[s];
+    const int64_t P_ = A.blk_off[s + 1] - A.blk_off[s];
     const int64_t rest = P_ - S.scal[S_F];
     Fp = min(free_cnt, rest);
     K = min(ncand, (rest > free_cnt ? rest - free_cnt : int64_t(0)) + static_cast<int64_t>(G.ctr[2]));
   } else {
     K = min(ncand, needed);
   }
+  // ---- lowest Fp free ids, ascending: each CTA lists the free ids of its
+  // score slices, offset by the free counts of all lower slices
+  if (Fp > 0) {
+    const int lane = t & 31, w = t >> 5;
+    __shared__ uint32_t wcnt[33];
+    __shared__ unsigned long long below;
+    for (int sl = cta; sl < G.n_slices; sl += n_cta) {
+      if (t == 0) below = 0;
+      __syncthreads();
+      unsigned long long part = 0;
+      for (int i = t; i < sl; i += blockDim.x) part += G.fcnt[i];
+      part = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(part));
+      if (lane == 0 && part) atomicAdd(&below, part);
+      __syncthreads();
+      int64_t found = static_cast<int64_t>(below);
+      __syncthreads();
+      if (found >= Fp || G.fcnt[sl] == 0) continue;  // uniform
+      const int64_t lo = sl * G.slice, hi = min(P.cap, lo + G.slice);
+      for (int64_t b = lo; b < hi && found < Fp; b += blockDim.x) {
+        const int64_t i = b + t;
+        const bool fr = i < hi && P.ntok[i] == 0;
+        const unsigned ball = __ballot_sync(0xffffffffu, fr);
+        if (lane == 0) wcnt[w] = __popc(ball);
+        __syncthreads();
+        if (w == 0) {
+          const uint32_t c = lane < 32 ? wcnt[lane] : 0;
+          uint32_t x = c;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          wcnt[lane] = x - c;
+          if (lane == 31) wcnt[32] = x;
+        }
+        __syncthreads();
+        const int64_t rank = found + wcnt[w] + __popc(ball & ((1u << lane) - 1));
+        if (fr && rank < Fp) S.freel[rank] = static_cast<int32_t>(i);
+        found += wcnt[32];
+        __syncthreads();
+      }
+    }
+  }
+  // ---- radix select of the K smallest candidate keys (keys are unique)
+  int64_t nl = 0;
+  for (int sl = cta; sl < G.n_slices; sl += n_cta) {
+    const int64_t c = G.ncnt[sl];
+    const uint64_t* src = G.keys + sl * G.slice;
+    for (int64_t i = t; i < c; i += blockDim.x) local_keys[nl + i] = src[i];
+    nl += c;
+  }
+  __syncthreads();
   uint64_t prefix = 0, mask = 0;
   if (K > 0 && K < ncand) {
+    const uint64_t kmin = key_lo, diff = key_lo ^ key_hi;
+    int hi_bit = 64 - __clzll(static_cast<long long>(diff));  // bits above are shared by every candidate
+    mask = hi_bit >= 64 ? 0ull : ~((uint64_t(1) << hi_bit) - 1);
+    prefix = kmin & mask;
     int64_t need = K;
-    const int shifts[6] = {53, 42, 31, 20, 10, 0};
-    const int widths[6] = {11, 11, 11, 11, 10, 10};
-    for (int pass = 0; pass < 6; ++pass) {
-      const int sh_ = shifts[pass], wd = widths[pass];
+    for (int pass = 0; hi_bit > 0; ++pass) {
+      const int wd = min(11, hi_bit), sh_ = hi_bit - wd;
+      hi_bit = sh_;
       const uint64_t bmask = (uint64_t(1) << wd) - 1;
       hist[2 * t] = 0;
       hist[2 * t + 1] = 0;
@@ -687,7 +1039,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
     }
   grid.sync();
   if (cta != 0) return;
-  // ---- phase D (CTA 0): sort the K selected keys, publish, free list
+  // ---- CTA 0: sort the K selected keys, publish them with their ranks
   if (K > 0) {
     int64_t n2 = 1;
     while (n2 < K) n2 <<= 1;
@@ -708,36 +1060,6 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
       S.victims[r] = k;
       S.taken[r] = 0;
       S.rank_of[k & kIdMask] = static_cast<int32_t>(r);
-    }
-  }
-  if (Fp > 0) {
-    __shared__ uint32_t wcnt[33];
-    __shared__ int64_t found;
-    if (t == 0) found = 0;
-    __syncthreads();
-    const int lane = t & 31, w = t >> 5;
-    for (int64_t base = 0; base < P.cap; base += blockDim.x) {
-      if (found >= Fp) break;
-      const int64_t i = base + t;
-      const bool fr = i < P.cap && P.ntok[i] == 0;
-      const unsigned ball = __ballot_sync(0xffffffffu, fr);
-      if (lane == 0) wcnt[w] = __popc(ball);
-      __syncthreads();
-      if (t == 0) {
-        uint32_t acc = 0;
-        for (int k = 0; k < 32; ++k) {
-          const uint32_t cnt = wcnt[k];
-          wcnt[k] = acc;
-          acc += cnt;
-        }
-        wcnt[32] = acc;
-      }
-      __syncthreads();
-      const int64_t rank = found + wcnt[w] + __popc(ball & ((1u << lane) - 1));
-      if (fr && rank < Fp) S.freel[rank] = static_cast<int32_t>(i);
-      __syncthreads();
-      if (t == 0) found += wcnt[32];
-      __syncthreads();
     }
   }
   if (t == 0) {
@@ -1071,6 +1393,8 @@ struct sb_kv_cache {
       k_select<<<1, kSelectThreads, select_smem(), stream>>>(P, S, A, s, mode, needed);
       return;
     }
+    k_plan<<<1, kSelectThreads, 0, stream>>>(P, S, A, s, mode, G);
+    k_score<<<G.n_slices, kScoreThreads, G.slice * sizeof(uint64_t), stream>>>(P, S, G);
     Pool p_ = P;
     Scratch s_ = S;
     InsertArgs a_ = A;
@@ -1096,7 +1420,7 @@ struct sb_kv_cache {
     // S.prehit aliases d_prehit_all: freed once below
     void* ptrs[] = {P.tok, P.ntok, P.chain, P.parent, P.tag, P.ref, P.pinned, P.last, P.tkey, P.tval, P.slot, P.ctr,
                     S.hashes, S.chain_out, S.kind, S.freel, S.evicted, S.victims, S.taken, S.rank_of, S.keys,
-                    S.sortbuf, S.scal, S.late, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first, G.hist, G.ctr};
+                    S.sortbuf, S.scal, S.late, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first, G.hist, G.ctr, G.keys, G.fcnt, G.ncnt, G.kmin, G.kmax};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
@@ -1192,8 +1516,7 @@ struct sb_kv_cache {
     const uint64_t* hashes = hashes_in;
     if (!hashes) {
       ensure_hash_all(std::max<int64_t>(total_blocks, 1));
-      k_chain_hash<<<(n_seqs + 127) / 128, 128, 0, stream>>>(tokens, seq_off, blk_off, nullptr, n_seqs, P.bs, 0,
-                                                           d_hash_all);
+      launch_chain_hash(tokens, seq_off, blk_off, nullptr, n_seqs, P.bs, 0, d_hash_all, stream);
       SB_CHECK_LAUNCH();
       hashes = d_hash_all;
     }
@@ -1201,8 +1524,7 @@ struct sb_kv_cache {
     for (int s = 0; s < n_seqs; ++s) {
       const int64_t np = h_blk_off[s + 1] - h_blk_off[s];
       if (np > 0)
-        k_probe_seq<<<static_cast<int>((np + 255) / 256), 256, 0, stream>>>(P, tokens, seq_off, blk_off, hashes, s,
-                                                                            S.prehit);
+        k_probe_seq<<<grid_for(np * kGroup), 256, 0, stream>>>(P, tokens, seq_off, blk_off, hashes, s, S.prehit);
       launch_select(A, s, 0, 0);
       k_walk<<<1, 32, 0, stream>>>(P, S, A, s);
       k_commit_evict<<<grid_for(np), 256, 0, stream>>>(P, S);
@@ -1234,8 +1556,8 @@ int sb_chain_hash_batch(const uint64_t* d_tokens, const int64_t* d_seq_offsets, 
   return guard([&] {
     if (n_seqs <= 0) return int(SB_OK);
     if (block_size < 1) throw Error(SB_ERR_INVALID, "block_size must be >= 1");
-    k_chain_hash<<<(n_seqs + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-        d_tokens, d_seq_offsets, d_block_offsets, d_parent, n_seqs, block_size, 0, d_block_hashes);
+    launch_chain_hash(d_tokens, d_seq_offsets, d_block_offsets, d_parent, n_seqs, block_size, 0, d_block_hashes,
+                      static_cast<cudaStream_t>(stream));
     SB_CHECK_LAUNCH();
     return int(SB_OK);
   });
@@ -1295,15 +1617,25 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
       if (capacity_blocks >= kCoopMinCap) {
         int n_sm = 0, per_sm = 0;
         SB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
-        const int64_t chunk = (capacity_blocks + n_sm - 1) / n_sm;
-        c->coop_smem = static_cast<size_t>(std::max<int64_t>(chunk, kSortSmemKeys)) * sizeof(uint64_t);
+        const int n_slices = kSlicesPerSm * n_sm;  // k_score partition; k_select_coop CTA c owns slices c, c + n_sm, ...
+        const int64_t slice = ((capacity_blocks + n_slices - 1) / n_slices + 3) & ~int64_t(3);
+        c->coop_smem = static_cast<size_t>(std::max<int64_t>(kSlicesPerSm * slice, kSortSmemKeys)) * sizeof(uint64_t);
         if (c->coop_smem <= 200 * 1024) {
           SB_CUDA(cudaFuncSetAttribute(k_select_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(c->coop_smem)));
           SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_coop, kSelectThreads, c->coop_smem));
           if (per_sm >= 1) c->coop_grid = n_sm;
           c->G.hist = dalloc<uint32_t>(6 * 2048);
-          c->G.ctr = dalloc<unsigned long long>(4);
+          c->G.ctr = dalloc<unsigned long long>(8);
+          c->G.n_slices = n_slices;
+          c->G.slice = slice;
+          c->G.keys = dalloc<uint64_t>(n_slices * slice);
+          c->G.fcnt = dalloc<uint32_t>(n_slices);
+          c->G.ncnt = dalloc<uint32_t>(n_slices);
+          c->G.kmin = dalloc<uint64_t>(n_slices);
+          c->G.kmax = dalloc<uint64_t>(n_slices);
+          SB_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(c->G.slice * sizeof(uint64_t))));
         }
       }
       SB_CHECK_LAUNCH();
@@ -1335,9 +1667,9 @@ int sb_kv_lookup_prefix(sb_kv_cache* c, const uint64_t* tokens, int64_t n, int64
     SB_CUDA(cudaMemcpyAsync(c->d_meta, meta, sizeof(meta), cudaMemcpyHostToDevice, c->stream));
     const int64_t* seq_off = c->d_meta;
     const int64_t* blk_off = c->d_meta + 2;
-    k_chain_hash<<<1, 32, 0, c->stream>>>(c->d_tok, seq_off, blk_off, nullptr, 1, c->P.bs, 1, c->d_hash_all);
+    launch_chain_hash(c->d_tok, seq_off, blk_off, nullptr, 1, c->P.bs, 1, c->d_hash_all, c->stream);
     k_lookup_init<<<1, 32, 0, c->stream>>>(blk_off, 1, c->d_first);
-    k_probe_batch<<<grid_for(nblk), 256, 0, c->stream>>>(c->P, c->d_tok, seq_off, blk_off, 1, c->d_hash_all, nblk,
+    k_probe_batch<<<grid_for(nblk * kGroup), 256, 0, c->stream>>>(c->P, c->d_tok, seq_off, blk_off, 1, c->d_hash_all, nblk,
                                                          c->d_prehit_all, c->d_first, 0);
     k_lookup_finish<<<grid_for(nblk + 1), 256, 0, c->stream>>>(c->P, seq_off, blk_off, 1, nblk, c->d_prehit_all,
                                                                c->d_first, now, c->d_hit);
@@ -1383,13 +1715,12 @@ int sb_kv_lookup_prefix_batch(sb_kv_cache* c, const uint64_t* d_tokens, const in
       c->ensure_hash_all(total + 1);
       SB_CUDA(cudaMemcpyAsync(c->d_batch_blk, blk.data(), sizeof(int64_t) * (n_seqs + 1), cudaMemcpyHostToDevice, st));
       d_blk = c->d_batch_blk;
-      k_chain_hash<<<(n_seqs + 127) / 128, 128, 0, st>>>(d_tokens, d_seq_offsets, d_blk, nullptr, n_seqs, c->P.bs, 1,
-                                                         c->d_hash_all);
+      launch_chain_hash(d_tokens, d_seq_offsets, d_blk, nullptr, n_seqs, c->P.bs, 1, c->d_hash_all, st);
       hashes = c->d_hash_all;
     }
     k_lookup_init<<<(n_seqs + 127) / 128, 128, 0, st>>>(d_blk, n_seqs, c->d_batch_first);
     if (total > 0)
-      k_probe_batch<<<grid_for(total), 256, 0, st>>>(c->P, d_tokens, d_seq_offsets, d_blk, n_seqs, hashes, total,
+      k_probe_batch<<<grid_for(total * kGroup), 256, 0, st>>>(c->P, d_tokens, d_seq_offsets, d_blk, n_seqs, hashes, total,
                                                      c->d_prehit_all, c->d_batch_first, pre ? 1 : 0);
     k_lookup_finish<<<grid_for(std::max<int64_t>(total, n_seqs)), 256, 0, st>>>(
         c->P, d_seq_offsets, d_blk, n_seqs, total, c->d_prehit_all, c->d_batch_first, now, d_hit_tokens);
