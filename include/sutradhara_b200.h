@@ -35,7 +35,7 @@ enum {
   SB_ERR_UNSUPPORTED = 8       /* shape/config outside the kernels' range */
 };
 
-/* ---- semantic tags (order == agentsim::KvTag, kv_cache.hpp:220-227) ---- */
+/* ---- semantic tags (order == agentsim::KvTag, kv_cache.hpp:21-28) ---- */
 enum {
   SB_TAG_RESPONSE = 0,
   SB_TAG_TOOL_OUTPUT = 1,
@@ -45,10 +45,10 @@ enum {
   SB_TAG_HISTORY = 5
 };
 
-/* ---- eviction policy (agentsim::EvictionPolicy, kv_cache.hpp:235) ------ */
+/* ---- eviction policy (agentsim::EvictionPolicy, kv_cache.hpp:36) ------ */
 enum { SB_POLICY_LRU = 0, SB_POLICY_TIERED = 1 };
 
-/* Half-open token range with a tag (agentsim::TagRange, kv_cache.hpp:244). */
+/* Half-open token range with a tag (agentsim::TagRange, kv_cache.hpp:45). */
 typedef struct sb_tag_range {
   int64_t begin;
   int64_t end;
@@ -56,7 +56,7 @@ typedef struct sb_tag_range {
   int32_t _pad;
 } sb_tag_range;
 
-/* Read-back of one block's metadata (agentsim::KvBlock, kv_cache.hpp:250). */
+/* Read-back of one block's metadata (agentsim::KvBlock, kv_cache.hpp:51). */
 typedef struct sb_block_info {
   int32_t block_id;
   int32_t tag;
@@ -76,7 +76,7 @@ const char* sb_last_error(void);
 /* Library version string. */
 const char* sb_version(void);
 
-/* ---- hashing (common.hpp:136-145, kv_cache.cpp:368-374, trace.cpp:60-83) */
+/* ---- hashing (common.hpp:136-145, kv_cache.cpp:35-41, trace.cpp:60-83) */
 uint64_t sb_kv_root_hash(void);
 /* Host-side single chain hash, for bindings that need one value. */
 uint64_t sb_kv_chain_hash_host(uint64_t parent, const uint64_t* tokens, int64_t n);
@@ -87,7 +87,7 @@ uint64_t sb_kv_chain_hash_host(uint64_t parent, const uint64_t* tokens, int64_t 
  * d_block_hashes[d_block_offsets[s] + j].  The chain for sequence s starts
  * from d_parent[s] (NULL = kv_root_hash()).  Replaces the per-block
  * kv_chain_hash loop inside KvCache::lookup_prefix / insert
- * (kv_cache.cpp:423-431, 471-475). */
+ * (kv_cache.cpp:90-98, 471-475). */
 int sb_chain_hash_batch(const uint64_t* d_tokens, const int64_t* d_seq_offsets,
                         const int64_t* d_block_offsets, const uint64_t* d_parent,
                         int32_t n_seqs, int64_t block_size, uint64_t* d_block_hashes,
@@ -101,52 +101,52 @@ int sb_materialize_tokens(int32_t section_tag, int64_t length, uint64_t content_
 int sb_decode_tokens(uint64_t stream_key, int64_t first_index, int64_t count, uint64_t* d_out,
                      void* stream);
 
-/* ---- KV block pool / block table: agentsim::KvCache (kv_cache.hpp:269) -- */
-/* KvCache::KvCache(const CacheConfig&)          kv_cache.cpp:376 */
+/* ---- KV block pool / block table: agentsim::KvCache (kv_cache.hpp:70) -- */
+/* KvCache::KvCache(const CacheConfig&)          kv_cache.cpp:43 */
 int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, int32_t device,
                  sb_kv_cache** out);
 void sb_kv_destroy(sb_kv_cache* cache);
 
-/* KvCache::lookup_prefix(tokens, now)            kv_cache.cpp:418  (host tokens) */
+/* KvCache::lookup_prefix(tokens, now)            kv_cache.cpp:85  (host tokens) */
 int sb_kv_lookup_prefix(sb_kv_cache* cache, const uint64_t* tokens, int64_t n_tokens,
                         int64_t now, int64_t* hit_tokens);
-/* KvCache::insert(tokens, tags, now)             kv_cache.cpp:436
+/* KvCache::insert(tokens, tags, now)             kv_cache.cpp:103
  * out_ids must hold ceil(n_tokens / block_size) entries.  On CacheFull the
- * reference's rollback is reproduced (kv_cache.cpp:463-469, 481-487). */
+ * reference's rollback is reproduced (kv_cache.cpp:130-136, 481-487). */
 int sb_kv_insert(sb_kv_cache* cache, const uint64_t* tokens, int64_t n_tokens,
                  const sb_tag_range* tags, int64_t n_tags, int64_t now, int32_t* out_ids,
                  int64_t* n_out);
-/* KvCache::evict(needed)                         kv_cache.cpp:510
+/* KvCache::evict(needed)                         kv_cache.cpp:177
  * out_ids must hold `needed` entries; *n_out < needed signals shortfall. */
 int sb_kv_evict(sb_kv_cache* cache, int64_t needed, int32_t* out_ids, int64_t* n_out);
-/* KvCache::set_reuse_priority(ids, update)       kv_cache.cpp:542
+/* KvCache::set_reuse_priority(ids, update)       kv_cache.cpp:209
  * pinned: -1 = leave, 0 = unpin, 1 = pin; tier_override: -1 = none, else tag. */
 int sb_kv_set_reuse_priority(sb_kv_cache* cache, const int32_t* ids, int64_t n, int32_t pinned,
                              int32_t tier_override);
-/* KvCache::set_tag(id, tag)                      kv_cache.cpp:555 */
+/* KvCache::set_tag(id, tag)                      kv_cache.cpp:222 */
 int sb_kv_set_tag(sb_kv_cache* cache, int32_t id, int32_t tag);
-/* KvCache::release(ids)                          kv_cache.cpp:561 */
+/* KvCache::release(ids)                          kv_cache.cpp:228 */
 int sb_kv_release(sb_kv_cache* cache, const int32_t* ids, int64_t n);
-/* KvCache::touch(ids, now)                       kv_cache.cpp:571 */
+/* KvCache::touch(ids, now)                       kv_cache.cpp:238 */
 int sb_kv_touch(sb_kv_cache* cache, const int32_t* ids, int64_t n, int64_t now);
 
 int64_t sb_kv_block_size(const sb_kv_cache* cache);
-int64_t sb_kv_resident_blocks(const sb_kv_cache* cache); /* kv_cache.hpp:300 */
-int64_t sb_kv_capacity_blocks(const sb_kv_cache* cache); /* kv_cache.hpp:301 */
-int64_t sb_kv_free_blocks(const sb_kv_cache* cache);     /* kv_cache.hpp:302 */
-uint64_t sb_kv_total_evicted(const sb_kv_cache* cache);  /* kv_cache.hpp:303 */
+int64_t sb_kv_resident_blocks(const sb_kv_cache* cache); /* kv_cache.hpp:101 */
+int64_t sb_kv_capacity_blocks(const sb_kv_cache* cache); /* kv_cache.hpp:102 */
+int64_t sb_kv_free_blocks(const sb_kv_cache* cache);     /* kv_cache.hpp:103 */
+uint64_t sb_kv_total_evicted(const sb_kv_cache* cache);  /* kv_cache.hpp:104 */
 int32_t sb_kv_policy(const sb_kv_cache* cache);
-/* KvCache::contains(id) — 1 resident, 0 not      kv_cache.hpp:305 */
+/* KvCache::contains(id) — 1 resident, 0 not      kv_cache.hpp:106 */
 int sb_kv_contains(const sb_kv_cache* cache, int32_t id);
 /* Resident block ids in ascending order (the key set of KvCache::blocks_,
- * kv_cache.hpp:323); out holds capacity entries. */
+ * kv_cache.hpp:124); out holds capacity entries. */
 int sb_kv_resident_ids(const sb_kv_cache* cache, int32_t* out, int64_t* n_out);
 /* KvCache::block(id); tokens_out may be NULL, else holds block_size u64. */
 int sb_kv_block(const sb_kv_cache* cache, int32_t id, sb_block_info* info, uint64_t* tokens_out);
-/* KvCache::audit()                                kv_cache.cpp:575 */
+/* KvCache::audit()                                kv_cache.cpp:242 */
 int sb_kv_audit(const sb_kv_cache* cache);
 /* KvCache::dump() — byte-identical text; *len receives the full length
- * (call with buf=NULL to size).                   kv_cache.cpp:601 */
+ * (call with buf=NULL to size).                   kv_cache.cpp:268 */
 int sb_kv_dump(const sb_kv_cache* cache, char* buf, int64_t cap, int64_t* len);
 
 /* ---- batched, stream-ordered engine path (no host round trip) --------- */

@@ -2,7 +2,7 @@
 // the reference (agentsim) to run its UNMODIFIED engine/orchestrator on the
 // B200 block pool: this file replaces src/kv_cache.cpp at link time and
 // implements every non-inline member of agentsim::KvCache
-// (include/agentsim/kv_cache.hpp:269-327) through the C-ABI of
+// (include/agentsim/kv_cache.hpp:70-128) through the C-ABI of
 // include/sutradhara_b200.h.  Exceptions are re-raised with the reference's
 // own types (common.hpp:72-90).
 //

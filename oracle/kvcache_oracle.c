@@ -12,14 +12,14 @@
  *
  * Reference (paths relative to /root/reference/proj):
  *   splitmix64 / hash_combine     include/agentsim/common.hpp:136-145
- *   kv_root_hash / kv_chain_hash  src/kv_cache.cpp:368-374
- *   eviction_tier                 src/kv_cache.cpp:356-366
- *   lookup_prefix                 src/kv_cache.cpp:418-434
- *   insert (+rollback)            src/kv_cache.cpp:436-508
- *   evict                         src/kv_cache.cpp:510-530
- *   set_reuse_priority / set_tag  src/kv_cache.cpp:542-559
- *   release / touch               src/kv_cache.cpp:561-573
- *   audit / dump                  src/kv_cache.cpp:575-614
+ *   kv_root_hash / kv_chain_hash  src/kv_cache.cpp:35-41
+ *   eviction_tier                 src/kv_cache.cpp:23-33
+ *   lookup_prefix                 src/kv_cache.cpp:85-101
+ *   insert (+rollback)            src/kv_cache.cpp:103-175
+ *   evict                         src/kv_cache.cpp:177-197
+ *   set_reuse_priority / set_tag  src/kv_cache.cpp:209-226
+ *   release / touch               src/kv_cache.cpp:228-240
+ *   audit / dump                  src/kv_cache.cpp:242-281
  *   materialize_tokens            src/trace.cpp:50-78
  *   decode_token                  src/trace.cpp:80-83
  */

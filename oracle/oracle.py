@@ -3,7 +3,7 @@
 Two checkers live here:
 
 * ``OracleCache`` — the plain-C restatement (oracle/kvcache_oracle.c) of the
-  reference KvCache (/root/reference/proj/src/kv_cache.cpp:356-614) and its
+  reference KvCache (/root/reference/proj/src/kv_cache.cpp:23-281) and its
   hashing (include/agentsim/common.hpp:136-145, src/trace.cpp:50-83).
 * ``RefCache`` / ``ref_*`` — the reference itself compiled from its own sources
   into oracle/_ref/ by oracle/Makefile (see oracle/ref_capi.cpp).

@@ -1,6 +1,6 @@
 // hash.cuh — the reference's token/block hashing, restated for host and device.
 //   splitmix64 / hash_combine   include/agentsim/common.hpp:136-145
-//   kv_root_hash / kv_chain_hash src/kv_cache.cpp:368-374
+//   kv_root_hash / kv_chain_hash src/kv_cache.cpp:35-41
 //   materialize_tokens           src/trace.cpp:50-78
 //   decode_token                 src/trace.cpp:80-83
 #pragma once
@@ -44,7 +44,7 @@ SB_HD uint64_t decode_token(uint64_t stream_key, int64_t index) {
   return splitmix64(splitmix64(stream_key ^ 0xdec0de0000000001ULL) + static_cast<uint64_t>(index));
 }
 
-// Eviction tier of a tag (kv_cache.cpp:356-366).
+// Eviction tier of a tag (kv_cache.cpp:23-33).
 SB_HD int tier_of(int tag) {
   return tag == 0 ? 0 : tag == 1 ? 1 : (tag == 2 || tag == 5) ? 2 : tag == 3 ? 3 : tag == 4 ? 4 : 0;
 }

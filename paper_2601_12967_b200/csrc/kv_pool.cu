@@ -10,7 +10,7 @@
 //   index: open-addressed multimap chain_hash -> block id (tcap = 4*cap
 //          slots, -1 empty, -2 tombstone), slot[cap] = index slot of a block
 //
-// One insert (kv_cache.cpp:436-508) is five stream-ordered kernels, no host
+// One insert (kv_cache.cpp:103-175) is five stream-ordered kernels, no host
 // round trip:
 //   k_probe   (all positions in parallel) find the resident block of each
 //             position in the PRE-insert state (chain hash + parent + tokens)
@@ -104,7 +104,7 @@ __device__ __forceinline__ uint64_t victim_key(const Pool& P, int32_t id) {
   return k;
 }
 
-// find_chain_block (kv_cache.cpp:403-416) is probe_find_g8 below.
+// find_chain_block (kv_cache.cpp:70-83) is probe_find_g8 below.
 
 __device__ void index_insert(const Pool& P, uint64_t h, int32_t id) {
   uint64_t s = index_slot(h, P.tcap);
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(256) k_probe_batch(Pool P, const uint64_t* __r
   const int64_t j = g - blk_off[s];
   const int64_t base = seq_off[s] + j * P.bs;
   const int len = static_cast<int>(min(P.bs, seq_off[s + 1] - base));
-  if (full_only_check && len < P.bs) {  // lookups never match a partial block (kv_cache.cpp:423)
+  if (full_only_check && len < P.bs) {  // lookups never match a partial block (kv_cache.cpp:90)
     if (part == 0) {
       prehit[g] = -1;
       if (first_miss) atomicMin(reinterpret_cast<unsigned long long*>(first_miss + s), static_cast<unsigned long long>(j));
@@ -369,7 +369,7 @@ __global__ void k_lookup_init(const int64_t* __restrict__ blk_off, int n_seqs, i
   if (s < n_seqs) first_miss[s] = blk_off[s + 1] - blk_off[s];
 }
 
-// Touch the hit prefix (kv_cache.cpp:432) and emit hit lengths.
+// Touch the hit prefix (kv_cache.cpp:99) and emit hit lengths.
 __global__ void k_lookup_finish(Pool P, const int64_t* __restrict__ seq_off, const int64_t* __restrict__ blk_off,
                                 int n_seqs, int64_t total_blocks, const int32_t* __restrict__ prehit,
                                 const int64_t* __restrict__ first_miss, int64_t now, int64_t* __restrict__ hit_tokens) {
@@ -524,7 +524,7 @@ __device__ __forceinline__ uint64_t warp_append_slot(bool c, Counter* cnt, bool&
   return base + __popc(m & ((1u << lane) - 1));
 }
 
-// Tag coverage check (kv_cache.cpp:438-448): ranges must tile [0, n).
+// Tag coverage check (kv_cache.cpp:105-115): ranges must tile [0, n).
 __device__ bool tags_cover(const sb_tag_range* tags, int64_t ntags, int64_t n) {
   int64_t covered = 0;
   for (int64_t r = 0; r < ntags; ++r) {
@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
   }
 }
 
-// Sequential decisions of one insert (kv_cache.cpp:471-506), from the first
+// Sequential decisions of one insert (kv_cache.cpp:138-173), from the first
 // pre-miss position on.  Single thread: each step is a handful of
 // L1/L2-resident accesses.
 // ---------------------------------------------------------------------------
@@ -1270,7 +1270,7 @@ __global__ void k_commit_apply(Pool P, Scratch S, InsertArgs A, int s) {
 }
 
 // --------------------------------------------------------- small ops
-// First failing index of a release (kv_cache.cpp:561-569): UnknownBlock /
+// First failing index of a release (kv_cache.cpp:228-236): UnknownBlock /
 // ZeroRefRelease, checked in id order; apply only if none.
 __global__ void k_validate_ids(Pool P, const int32_t* ids, int64_t n, int check_ref, int64_t* scal,
                                int skip_negative = 0) {

@@ -9,7 +9,7 @@
 // Reference behaviour restated (paths under /root/reference/proj/src):
 //   trace generator              trace_gen.cpp:96-193 (+ Rng, common.hpp:161-197)
 //   token materialisation         trace.cpp:50-83
-//   event loop ordering           sim.cpp:227-250 ((time, sequence) order)
+//   event loop ordering           sim.cpp:28-43 ((time, sequence) order)
 //   engine: admission, chunked prefill + decode steps, scheduler policies,
 //           partial prefill pins, extension, completion inserts/releases
 //                                 engine.cpp:35-475

@@ -1,5 +1,5 @@
 """Host-side mirror of the reference's ``agentsim::KvCache``
-(/root/reference/proj/include/agentsim/kv_cache.hpp:269-327), backed by the
+(/root/reference/proj/include/agentsim/kv_cache.hpp:70-128), backed by the
 device-resident block pool in csrc/kv_pool.cu through the C-ABI.
 
 Same method names, argument meaning and error behaviour as the reference:
@@ -18,14 +18,14 @@ import numpy as np
 from . import _lib
 from .errors import CacheError, CacheFull, UnknownBlock, ZeroRefRelease  # noqa: F401 (re-export)
 
-# KvTag (kv_cache.hpp:220-227) and EvictionPolicy (kv_cache.hpp:235)
+# KvTag (kv_cache.hpp:21-28) and EvictionPolicy (kv_cache.hpp:36)
 RESPONSE, TOOL_OUTPUT, USER_QUERY, SYSTEM_PROMPT, PARTIAL_PREFILL, HISTORY = range(6)
 LRU, TIERED = 0, 1
 TAG_NAMES = ["response", "tool_output", "user_query", "system_prompt", "partial_prefill", "history"]
 
 
 def eviction_tier(tag: int) -> int:
-    """kv_cache.cpp:356-366."""
+    """kv_cache.cpp:23-33."""
     return (0, 1, 2, 3, 4, 2)[tag]
 
 
