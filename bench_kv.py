@@ -8,8 +8,9 @@ algorithmic GB/s against the measured HBM copy bandwidth.
 Algorithmic bytes per unit:
   chain hash     8 B read per token + 8 B written per block
   lookup         per full block position: 128 B query tokens + 128 B stored
-                 tokens + 20 B block metadata + 12 B index slot
-  evict scoring  per pool block: ntok/ref/pinned/tag/exclusion mark (20 B) + last (8 B)
+                 tokens + 24 B index slot (chain hash, parent, id, ntok) + 8 B
+                 chain hash of the position
+  evict scoring  per pool block: ntok/ref/pinned(+exclusion mark)/tag (16 B) + last (8 B)
   kv append      per token and layer: 2 x H_kv x 128 x 2 B read + same written
 """
 from __future__ import annotations
@@ -132,10 +133,15 @@ def evict_bench(L, cache, cap, hbm):
 
 
 def main():
+    import argparse
+
     import torch
     from paper_2601_12967_b200 import _lib
     from paper_2601_12967_b200.kv_cache import CacheConfig, KvCache
 
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="hash,probe,probe_big,evict,evict_big,append")
+    only = set(ap.parse_args().only.split(","))
     L = _lib.lib()
     hbm = float(peaks()["hbm_gbs"])
     dev = torch.device("cuda")
@@ -143,7 +149,7 @@ def main():
     st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
     # ---- chain hashing: latency-bound per sequence, throughput over sequences
-    for n_seqs, toks in ((64, 8192), (4096, 1024), (65536, 512), (262144, 128)):
+    for n_seqs, toks in ((64, 8192), (4096, 1024), (65536, 512), (262144, 128), (262144, 512)) if "hash" in only else ():
         n = n_seqs * toks
         tokens = torch.randint(0, 2**62, (n,), dtype=torch.int64, device=dev)
         seq_off = torch.arange(0, n + 1, toks, dtype=torch.int64, device=dev)
@@ -155,10 +161,29 @@ def main():
              kt.get("k_chain_hash16"), hbm)
         del tokens
 
+    if "probe" in only:
+        probe_bench(L, dev, st, hbm, 1 << 20, 1024, 8192, evict=True)
+    if "probe_big" in only:
+        probe_bench(L, dev, st, hbm, 1 << 22, 4096, 8192, evict=False)
+    # ---- eviction at pool scale: evict() = k_plan + k_score (HBM pass) + k_select_coop
+    for big, n_fill in ((1 << 22, 2048), (1 << 24, 8192)):
+        if ("evict" if big == 1 << 22 else "evict_big") in only:
+            cache2 = KvCache(CacheConfig(16, big, 1))
+            fill_pool(L, cache2, dev, n_fill, 16384, st)
+            evict_bench(L, cache2, big, hbm)
+            del cache2
+    if "append" in only:
+        append_bench(L, dev, st, hbm)
+
+
+def probe_bench(L, dev, st, hbm, cap, n_seqs, toks, evict):
+    import torch
+    from paper_2601_12967_b200 import _lib
+    from paper_2601_12967_b200.kv_cache import CacheConfig, KvCache
+
+    p = lambda t: C.c_void_p(t.data_ptr())
     # ---- batched lookup over a populated pool (all-hit prefixes)
-    cap = 1 << 20
     cache = KvCache(CacheConfig(16, cap, 1))
-    n_seqs, toks = 1024, 8192
     n = n_seqs * toks
     host = np.random.default_rng(0).integers(0, 2**62, n, dtype=np.int64)
     tokens = torch.from_numpy(host).to(dev)
@@ -181,20 +206,20 @@ def main():
     hits = torch.empty(n_seqs, dtype=torch.int64, device=dev)
     api, kt = timed(lambda: L.sb_kv_lookup_prefix_batch(cache.handle, p(tokens), p(seq_off), p(blk_off),
                                                          blk_off_h.ctypes.data_as(_lib.I64P), p(hashes), n_seqs, 2,
-                                                         p(hits), st), kernels=("k_probe_batch",), flush=True)
+                                                         p(hits), st), kernels=("k_probe_rows",), flush=True)
     assert int(hits.sum()) == n
-    emit("k_probe_batch", f"{n_seqs} seqs x {toks} tokens, pool {cap} blocks, all hit",
-         (n // 16) * (128 + 128 + 20 + 12), api, kt.get("k_probe_batch"), hbm)
+    emit("k_probe_rows", f"{n_seqs} seqs x {toks} tokens, pool {cap} blocks, all hit",
+         (n // 16) * (128 + 128 + 24 + 8), api, kt.get("k_probe_rows"), hbm)
 
-    # ---- eviction at pool scale: evict() = k_plan + k_score (HBM pass) + k_select_coop
-    evict_bench(L, cache, cap, hbm)
+    if evict:
+        evict_bench(L, cache, cap, hbm)
     del cache
-    big = 1 << 21
-    cache2 = KvCache(CacheConfig(16, big, 1))
-    fill_pool(L, cache2, dev, 1024, 16384, st)
-    evict_bench(L, cache2, big, hbm)
-    del cache2
 
+
+def append_bench(L, dev, st, hbm):
+    import torch
+
+    p = lambda t: C.c_void_p(t.data_ptr())
     # ---- KV append (Llama-3-8B kv heads), one layer
     tok_n, hkv, pages = 98896, 8, 27281
     kp = torch.empty(pages, hkv, 16, 128, dtype=torch.bfloat16, device=dev)

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -37,12 +38,17 @@
 
 #include "common.h"
 #include "hash.cuh"
+#include "sm100.cuh"
 
 namespace sb {
 
-constexpr int64_t kLastBias = int64_t(1) << 39;
-constexpr int kIdBits = 21;
-constexpr uint64_t kIdMask = (uint64_t(1) << kIdBits) - 1;
+// Victim keys pack (tier:3 | last_used + bias | block id) into 64 bits, so
+// one unsigned compare orders candidates exactly as the reference's sort
+// (kv_cache.cpp:184-188).  The id field is idb = max(21, ceil(log2(cap)))
+// bits wide (pools up to 2^kMaxIdBits blocks); last_used gets the remaining
+// 61 - idb bits, i.e. |now| < 2^(60 - idb) (2^39 for pools up to 2M blocks).
+constexpr int kMinIdBits = 21;
+constexpr int kMaxIdBits = 24;
 constexpr uint64_t kNoKey = ~uint64_t(0);
 constexpr int kSelectThreads = 1024;
 constexpr int kSortSmemKeys = 8192;
@@ -56,9 +62,25 @@ enum Scal { S_F = 0, S_K, S_FREE, S_NEV, S_STATUS, S_FAILPOS, S_NNEW, S_NCAND, S
 // many are tracked per insert.
 constexpr int kLateMax = 64;
 
+// One 32 B index slot (= one DRAM sector): a probe learns from a single
+// sector whether the slot is empty/tombstone, its chain hash, and the parent
+// hash and token count the reference's find_chain_block compares
+// (kv_cache.cpp:77) — only the block's tokens remain a second access.
+// parent/ntok of a resident block never change, so the copies stay valid.
+struct alignas(32) IdxEntry {
+  uint64_t key;     // chain hash
+  uint64_t parent;  // parent chain hash of the block
+  int32_t id;       // block id, -1 empty, -2 tombstone
+  int32_t ntok;     // tokens in the block
+  int64_t pad;
+};
+
 struct Pool {
   int64_t bs, cap, tcap;
   int32_t policy;
+  int32_t idb;      // id bits of a victim key
+  uint64_t idmask;  // (1 << idb) - 1
+  int64_t lbias;    // 2^(60 - idb): last_used + lbias is non-negative
   uint64_t* tok;
   int32_t* ntok;
   uint64_t* chain;
@@ -67,8 +89,7 @@ struct Pool {
   int32_t* ref;
   int32_t* pinned;
   int64_t* last;
-  uint64_t* tkey;
-  int32_t* tval;
+  IdxEntry* idx;
   int32_t* slot;
   unsigned long long* ctr;
 };
@@ -99,19 +120,23 @@ __device__ __forceinline__ bool is_candidate(const Pool& P, int32_t id) {
 }
 
 __device__ __forceinline__ uint64_t victim_key(const Pool& P, int32_t id) {
-  uint64_t k = (static_cast<uint64_t>(P.last[id] + kLastBias) << kIdBits) | static_cast<uint64_t>(id);
+  uint64_t k = (static_cast<uint64_t>(P.last[id] + P.lbias) << P.idb) | static_cast<uint64_t>(id);
   if (P.policy == SB_POLICY_TIERED) k |= static_cast<uint64_t>(tier_of(P.tag[id])) << 61;
   return k;
 }
 
-// find_chain_block (kv_cache.cpp:70-83) is probe_find_g8 below.
+// find_chain_block (kv_cache.cpp:70-83) is probe_find_g below.
 
-__device__ void index_insert(const Pool& P, uint64_t h, int32_t id) {
+// Entries are written by commit/rebuild kernels and read by probes of later
+// launches only, so no reader ever sees a half-written slot.
+__device__ void index_insert(const Pool& P, uint64_t h, int32_t id, uint64_t parent, int32_t ntok) {
   uint64_t s = index_slot(h, P.tcap);
   for (;;) {
-    int32_t v = P.tval[s];
-    if (v < 0 && atomicCAS(&P.tval[s], v, id) == v) {
-      P.tkey[s] = h;
+    int32_t v = P.idx[s].id;
+    if (v < 0 && atomicCAS(&P.idx[s].id, v, id) == v) {
+      P.idx[s].key = h;
+      P.idx[s].parent = parent;
+      P.idx[s].ntok = ntok;
       P.slot[id] = static_cast<int32_t>(s);
       return;
     }
@@ -156,54 +181,74 @@ __global__ void k_chain_hash(const uint64_t* __restrict__ tokens, const int64_t*
 // of two sequences (16 lanes x 8 B, contiguous), staged through shared memory
 // and prefetched one block ahead in registers — instead of 32 scattered 8 B
 // loads per instruction (which made the per-lane fold L1-wavefront bound).
-constexpr int kHashWarps = 2;
-__global__ void __launch_bounds__(32 * kHashWarps)
+// The fold itself is ALU-pipe bound (ncu: alu 77 %, math-pipe throttle), so
+// the load path is kept off the ALU pipe: while every sequence of the warp
+// still has a full block j (warp-uniform), a load is one LDS of the
+// sequence's base pointer + one IMAD.WIDE + the LDG, no bounds checks.
+// Persistent grid (whole waves): warps stride over 32-sequence groups.
+constexpr int kHashWarps = 4;
+__global__ void __launch_bounds__(32 * kHashWarps, 8)
     k_chain_hash16(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ seq_off,
                    const int64_t* __restrict__ blk_off, const uint64_t* __restrict__ parent0, int n_seqs,
                    int full_only, uint64_t* __restrict__ out) {
   __shared__ uint64_t stage[kHashWarps][32][17];  // 17-word rows: conflict-free per half warp
+  __shared__ const uint64_t* seq_p[kHashWarps][32];
   __shared__ int64_t seq_b[kHashWarps][32], seq_e[kHashWarps][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = (blockIdx.x * kHashWarps + w) * 32 + lane;
-  int64_t b = 0, e = 0, ob = 0, nblk = 0;
-  uint64_t h = kRootHash;
-  if (s < n_seqs) {
-    b = seq_off[s];
-    e = seq_off[s + 1];
-    ob = blk_off[s];
-    if (parent0) h = parent0[s];
-    nblk = full_only ? (e - b) / 16 : (e - b + 15) / 16;
-  }
-  seq_b[w][lane] = b;
-  seq_e[w][lane] = e;
-  const int nb_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(nblk)));
-  __syncwarp();
   const int half = lane >> 4, k = lane & 15;
-  uint64_t v[16];
-  auto load = [&](int64_t j) {
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const int q = 2 * r + half;
-      const int64_t pos = seq_b[w][q] + 16 * j + k;
-      v[r] = pos < seq_e[w][q] ? __ldg(reinterpret_cast<const unsigned long long*>(tokens + pos)) : 0ull;
+  const int n_groups = (n_seqs + 31) >> 5;
+  for (int grp = blockIdx.x * kHashWarps + w; grp < n_groups; grp += gridDim.x * kHashWarps) {
+    const int s = grp * 32 + lane;
+    int64_t b = 0, e = 0, ob = 0, nblk = 0;
+    uint64_t h = kRootHash;
+    if (s < n_seqs) {
+      b = seq_off[s];
+      e = seq_off[s + 1];
+      ob = blk_off[s];
+      if (parent0) h = parent0[s];
+      nblk = full_only ? (e - b) / 16 : (e - b + 15) / 16;
     }
-  };
-  if (nb_max > 0) load(0);
-  for (int j = 0; j < nb_max; ++j) {
     __syncwarp();
-#pragma unroll
-    for (int r = 0; r < 16; ++r) stage[w][2 * r + half][k] = v[r];
+    seq_b[w][lane] = b;
+    seq_e[w][lane] = e;
+    seq_p[w][lane] = tokens + b + k;  // lane k of a half warp loads token k of a block
+    const int nb_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(nblk)));
+    // blocks every sequence of the group holds in full (empty lanes hold none)
+    const int nb_full = static_cast<int>(
+        __reduce_min_sync(0xffffffffu, s < n_seqs ? static_cast<unsigned>((e - b) / 16) : 0u));
     __syncwarp();
-    if (j + 1 < nb_max) load(j + 1);
-    if (j < nblk) {
-      const int64_t len = e - (b + 16 * static_cast<int64_t>(j));
-      if (len >= 16) {
+    uint64_t v[16];
+    auto load = [&](int j) {
+      if (j < nb_full) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) h = chain_step(h, stage[w][lane][i] + kGolden);
+        for (int r = 0; r < 16; ++r)
+          v[r] = __ldg(reinterpret_cast<const unsigned long long*>(seq_p[w][2 * r + half] + 16 * j));
       } else {
-        for (int i = 0; i < len; ++i) h = chain_step(h, stage[w][lane][i] + kGolden);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const int q = 2 * r + half;
+          const int64_t pos = seq_b[w][q] + 16 * static_cast<int64_t>(j) + k;
+          v[r] = pos < seq_e[w][q] ? __ldg(reinterpret_cast<const unsigned long long*>(tokens + pos)) : 0ull;
+        }
       }
-      out[ob + j] = h;
+    };
+    if (nb_max > 0) load(0);
+    for (int j = 0; j < nb_max; ++j) {
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < 16; ++r) stage[w][2 * r + half][k] = v[r];
+      __syncwarp();
+      if (j + 1 < nb_max) load(j + 1);
+      if (j < nblk) {
+        const int64_t len = e - (b + 16 * static_cast<int64_t>(j));
+        if (len >= 16) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) h = chain_step(h, stage[w][lane][i] + kGolden);
+        } else {
+          for (int i = 0; i < len; ++i) h = chain_step(h, stage[w][lane][i] + kGolden);
+        }
+        out[ob + j] = h;
+      }
     }
   }
 }
@@ -213,9 +258,18 @@ static void launch_chain_hash(const uint64_t* tokens, const int64_t* seq_off, co
                               cudaStream_t st) {
   if (n_seqs <= 0) return;
   if (bs == 16) {
-    const int per = 32 * kHashWarps;
-    k_chain_hash16<<<(n_seqs + per - 1) / per, per, 0, st>>>(tokens, seq_off, blk_off, parent0, n_seqs, full_only,
-                                                              out);
+    static int grid_cap = 0;  // whole waves of resident CTAs
+    auto kern = k_chain_hash16;
+    if (!grid_cap) {
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kHashWarps, 0);
+      grid_cap = std::max(1, sms * std::max(per_sm, 1));
+    }
+    const int groups = (n_seqs + 31) / 32;
+    const int grid = std::min(grid_cap, (groups + kHashWarps - 1) / kHashWarps);
+    kern<<<grid, 32 * kHashWarps, 0, st>>>(tokens, seq_off, blk_off, parent0, n_seqs, full_only, out);
   } else {
     k_chain_hash<<<(n_seqs + 63) / 64, 64, 0, st>>>(tokens, seq_off, blk_off, parent0, n_seqs, bs, full_only, out);
   }
@@ -223,53 +277,89 @@ static void launch_chain_hash(const uint64_t* tokens, const int64_t* seq_off, co
 
 // --------------------------------------------------------------- lookups
 
-// Group probe: the kGroup lanes of an aligned lane group look up ONE block
-// position together.  They walk the index identically (same addresses, one
-// transaction per load), fetch the slot's id and key together, then load the
-// candidate block's metadata and its tokens at once (lane i compares tokens
-// i, i+kGroup, ... of the block) and vote.  The dependent chain per position
-// is chain hash -> index slot -> (metadata + tokens).
-constexpr int kGroup = 4;
-__device__ __forceinline__ int32_t ld_keep_i32(const int32_t* p) {
-  int32_t v;
-  asm volatile("ld.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
+// Group probe: the kGroup = 2 lanes of an aligned lane pair look up ONE block
+// position together.  Both walk the index identically (same 32 B slot, one
+// sector, broadcast), and on a slot whose (chain hash, parent, ntok) match,
+// each lane compares one half of the block's tokens with the query's (16 B
+// vector loads of the pool's 128 B token row) and the pair votes.  The
+// dependent chain per position is chain hash -> index slot -> block tokens;
+// the query tokens are loaded before the walk.
+// The walk is WARP-converged: every lane runs the loop until all 16 pairs of
+// the warp are done and the vote is one full-warp ballot.  (A per-pair
+// __all_sync inside a data-dependent loop left the warp diverged, so the
+// pairs' probes — and their loads — ran one after another: ncu counted 16
+// vote executions per warp.)  `active` is false for lanes with no position.
+constexpr int kGroup = 2;
+__device__ __forceinline__ void ld_slot(const IdxEntry* e, uint64_t& key, uint64_t& parent, int32_t& id,
+                                        int32_t& ntok) {
+  asm volatile(
+      "ld.global.v2.u64 {%0, %1}, [%4];\n\t"
+      "ld.global.v2.s32 {%2, %3}, [%4+16];"
+      : "=l"(key), "=l"(parent), "=r"(id), "=r"(ntok)
+      : "l"(e));
 }
-__device__ __forceinline__ uint64_t ld_keep_u64(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
-  return v;
+__device__ __forceinline__ void ld_v2(const uint64_t* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
 }
-__device__ int32_t probe_find_g(const Pool& P, uint64_t h, uint64_t parent, const uint64_t* __restrict__ t, int len,
-                                int part, unsigned gmask) {
-  constexpr int R = 16 / kGroup;  // tokens per lane of a 16-token block
-  uint64_t tq[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = part + kGroup * r;
-    tq[r] = i < len ? t[i] : 0ull;
-  }
+template <bool kVec>
+__device__ int32_t probe_find_g(const Pool& P, bool active, uint64_t h, uint64_t parent,
+                                const uint64_t* __restrict__ t, int len, int part) {
+  constexpr int R = 16 / kGroup;  // tokens per lane of a 16-token block: [R*part, R*part + R)
+  const int lane = threadIdx.x & 31;
   uint64_t s = index_slot(h, P.tcap);
-  for (;;) {
-    // both halves of the slot in flight together (volatile: not sunk below the branch)
-    const int32_t id = ld_keep_i32(P.tval + s);
-    const uint64_t key = ld_keep_u64(P.tkey + s);
-    if (id == -1) return -1;
-    if (id >= 0 && key == h) {
-      const uint64_t* bt = P.tok + static_cast<int64_t>(id) * P.bs;
-      const int nt = P.ntok[id];
-      const uint64_t par = P.parent[id];
-      bool eq = true;
+  bool done = !active;
+  int32_t found = -1;
+  // query tokens are only needed once a slot matches: loaded in the same
+  // round trip as the block's tokens (no registers held across the walk)
+  const bool q_vec = kVec && (reinterpret_cast<uintptr_t>(t + R * part) & 15) == 0;
+  while (__any_sync(0xffffffffu, !done)) {
+    bool eq = false, empty = false;
+    int32_t id = -1;
+    if (!done) {
+      uint64_t key, par;
+      int32_t nt;
+      ld_slot(P.idx + s, key, par, id, nt);
+      empty = id == -1;
+      if (id >= 0 && key == h && par == parent && nt == len) {
+        const uint64_t* bt = P.tok + static_cast<int64_t>(id) * P.bs;
+        eq = true;
+        if (kVec) {  // bs == 16: 128 B aligned rows
+          uint64_t x[R], q[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = part + kGroup * r;
-        if (i < len) eq &= bt[i] == tq[r];
+          for (int r = 0; r < R / 2; ++r) ld_v2(bt + R * part + 2 * r, x[2 * r], x[2 * r + 1]);
+          if (q_vec) {
+#pragma unroll
+            for (int r = 0; r < R / 2; ++r) {
+              const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(t + R * part) + r);
+              q[2 * r] = v.x;
+              q[2 * r + 1] = v.y;
+            }
+          } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) q[r] = R * part + r < len ? __ldg(reinterpret_cast<const unsigned long long*>(t + R * part + r)) : 0ull;
+          }
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (R * part + r < len) eq &= x[r] == q[r];
+        } else {
+          for (int i = part; i < len; i += kGroup) eq &= bt[i] == t[i];
+        }
       }
-      for (int i = part + 16; i < len; i += kGroup) eq &= bt[i] == t[i];
-      if (__all_sync(gmask, eq && nt == len && par == parent)) return id;
     }
-    s = (s + 1) & static_cast<uint64_t>(P.tcap - 1);
+    const unsigned vote = __ballot_sync(0xffffffffu, eq);
+    const unsigned pair = (vote >> (lane & ~(kGroup - 1))) & ((1u << kGroup) - 1);
+    if (!done) {
+      if (pair == (1u << kGroup) - 1) {
+        found = id;
+        done = true;
+      } else if (empty) {
+        done = true;
+      } else {
+        s = (s + 1) & static_cast<uint64_t>(P.tcap - 1);
+      }
+    }
   }
+  return found;
 }
 
 // Warp-wide 32-ary search: s with blk_off[s] <= x < blk_off[s + 1]
@@ -308,41 +398,132 @@ __device__ __forceinline__ int find_seq_warp(const int64_t* __restrict__ blk_off
   return lo;
 }
 
-// Pre-state probe of every block position of a batch of sequences
-// (kGroup lanes per position).
-__global__ void __launch_bounds__(256) k_probe_batch(Pool P, const uint64_t* __restrict__ tokens,
-                                                     const int64_t* __restrict__ seq_off,
-                                                     const int64_t* __restrict__ blk_off, int n_seqs,
-                                                     const uint64_t* __restrict__ hashes, int64_t total_blocks,
-                                                     int32_t* __restrict__ prehit, int64_t* __restrict__ first_miss,
-                                                     int full_only_check) {
-  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int64_t g = tid / kGroup;
-  const int part = threadIdx.x % kGroup;
-  const unsigned gmask = ((1u << kGroup) - 1) << (threadIdx.x & 31 & ~(kGroup - 1));
-  if (blockIdx.x * static_cast<int64_t>(blockDim.x) / kGroup + (threadIdx.x & ~31) / kGroup >= total_blocks) return;
-  // chain hashes do not depend on the sequence: in flight before the search
-  const int64_t gc = min(g, total_blocks - 1);
-  const uint64_t h = hashes[gc];
-  const uint64_t hprev = gc ? hashes[gc - 1] : kRootHash;
-  const int s = find_seq_warp(blk_off, n_seqs, g, total_blocks);  // whole warp
-  if (g >= total_blocks) return;  // uniform per group
-  const int64_t j = g - blk_off[s];
-  const int64_t base = seq_off[s] + j * P.bs;
-  const int len = static_cast<int>(min(P.bs, seq_off[s + 1] - base));
-  if (full_only_check && len < P.bs) {  // lookups never match a partial block (kv_cache.cpp:90)
-    if (part == 0) {
-      prehit[g] = -1;
-      if (first_miss) atomicMin(reinterpret_cast<unsigned long long*>(first_miss + s), static_cast<unsigned long long>(j));
-    }
-    return;
+// Pre-state probe of the block positions of a batch of sequences, one CTA
+// per (sequence, run of kProbeRun consecutive positions): grid = (n_seqs,
+// max runs).  The sequence's offsets are three broadcast loads (no search).
+// Each lane pair works through kProbePer positions (j0 + pair + 128 k) as a
+// small state machine — every trip round the loop is ONE memory round trip
+// for every pair: either its current position's index slot (SLOT) or the
+// matched block's tokens + the query's tokens (TOK).  A pair that resolves a
+// position starts the next one in the same trip (its chain hashes were
+// prefetched a position ahead), so extra probes of one pair no longer stall
+// the other 15 pairs of the warp, and a warp keeps 16 positions in flight.
+constexpr int kProbePairs = 128;                   // lane pairs per CTA
+template <int kProbePer>                           // positions per pair
+__global__ void __launch_bounds__(kProbePairs * kGroup, 4) k_probe_rows(Pool P, const uint64_t* __restrict__ tokens,
+                                                                       const int64_t* __restrict__ seq_off,
+                                                                       const int64_t* __restrict__ blk_off,
+                                                                       const uint64_t* __restrict__ hashes,
+                                                                       int32_t* __restrict__ prehit,
+                                                                       int64_t* __restrict__ first_miss,
+                                                                       int full_only_check) {
+  static_assert(kGroup == 2, "pair protocol");
+  constexpr int kProbeRun = kProbePairs * kProbePer;  // positions per CTA
+  const int sq = blockIdx.x;
+  const int64_t b0 = blk_off[sq], np = blk_off[sq + 1] - b0;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.y) * kProbeRun;
+  if (j0 >= np) return;  // CTA-uniform
+  const int64_t t0 = seq_off[sq], t1 = seq_off[sq + 1];
+  const int lane = threadIdx.x & 31, part = lane & 1;
+  const int pair = threadIdx.x >> 1;
+  constexpr int R = 16 / kGroup;
+  const bool vec = P.bs == 16;
+  // position k of this pair
+  auto pos = [&](int k) { return j0 + pair + static_cast<int64_t>(kProbePairs) * k; };
+  int k = 0;
+  int64_t j = pos(0);
+  bool live = j < np;  // pair has a position to resolve
+  uint64_t h = 0, parent = kRootHash, h_nx = 0, parent_nx = kRootHash;
+  if (live) {
+    h = hashes[b0 + j];
+    if (j) parent = hashes[b0 + j - 1];
   }
-  const uint64_t parent = j ? hprev : kRootHash;
-  const int32_t id = probe_find_g(P, h, parent, tokens + base, len, part, gmask);
-  if (part == 0) {
-    prehit[g] = id;
-    if (id < 0 && first_miss)
-      atomicMin(reinterpret_cast<unsigned long long*>(first_miss + s), static_cast<unsigned long long>(j));
+  if (pos(1) < np) {
+    h_nx = hashes[b0 + pos(1)];
+    parent_nx = hashes[b0 + pos(1) - 1];
+  }
+  int len = 0;
+  int64_t base = 0;
+  auto setup = [&]() {  // per-position constants of j
+    base = t0 + j * P.bs;
+    len = static_cast<int>(min(P.bs, t1 - base));
+  };
+  if (live) setup();
+  uint64_t s = index_slot(h, P.tcap);
+  bool tok_phase = false;
+  int32_t cand = -1;
+  // a lookup never matches a partial block (kv_cache.cpp:90)
+  bool skip = live && full_only_check && len < P.bs;
+  while (__any_sync(0xffffffffu, live)) {
+    bool eq = false, resolved = false;
+    const bool was_tok = live && tok_phase && !skip;
+    int32_t result = -1;
+    if (live && skip) {
+      resolved = true;
+    } else if (live && !tok_phase) {
+      uint64_t key, par;
+      int32_t id, nt;
+      ld_slot(P.idx + s, key, par, id, nt);
+      if (id == -1) {
+        resolved = true;
+      } else if (id >= 0 && key == h && par == parent && nt == len) {
+        tok_phase = true;
+        cand = id;
+      } else {
+        s = (s + 1) & static_cast<uint64_t>(P.tcap - 1);
+      }
+    } else if (live) {
+      const uint64_t* bt = P.tok + static_cast<int64_t>(cand) * P.bs;
+      const uint64_t* q = tokens + base;
+      eq = true;
+      if (vec) {
+        uint64_t x[R], y[R];
+#pragma unroll
+        for (int r = 0; r < R / 2; ++r) ld_v2(bt + R * part + 2 * r, x[2 * r], x[2 * r + 1]);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          y[r] = R * part + r < len ? __ldg(reinterpret_cast<const unsigned long long*>(q + R * part + r)) : 0ull;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (R * part + r < len) eq &= x[r] == y[r];
+      } else {
+        for (int i = part; i < len; i += kGroup) eq &= bt[i] == q[i];
+      }
+    }
+    // pair vote (both lanes of a pair are always in the same state)
+    const unsigned vote = __ballot_sync(0xffffffffu, eq);
+    if (was_tok) {
+      if (((vote >> (lane & ~1)) & 3u) == 3u) {
+        resolved = true;
+        result = cand;
+      } else {  // hash collision: keep walking
+        tok_phase = false;
+        s = (s + 1) & static_cast<uint64_t>(P.tcap - 1);
+      }
+    }
+    if (resolved) {
+      if (part == 0) {
+        prehit[b0 + j] = result;
+        if (result < 0 && first_miss)
+          atomicMin(reinterpret_cast<unsigned long long*>(first_miss + sq), static_cast<unsigned long long>(j));
+      }
+      ++k;
+      j = pos(k);
+      live = k < kProbePer && j < np;
+      if (live) {
+        h = h_nx;
+        parent = parent_nx;
+        setup();
+        s = index_slot(h, P.tcap);
+        tok_phase = false;
+        skip = full_only_check && len < P.bs;
+        const int64_t jn = pos(k + 1);
+        if (k + 1 < kProbePer && jn < np) {  // prefetch the next position's chain hashes
+          h_nx = hashes[b0 + jn];
+          parent_nx = hashes[b0 + jn - 1];
+        }
+      }
+    }
   }
 }
 
@@ -355,13 +536,16 @@ __global__ void k_probe_seq(Pool P, const uint64_t* __restrict__ tokens, const i
   const int64_t np = blk_off[s + 1] - b0;
   const int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / kGroup;
   const int part = threadIdx.x % kGroup;
-  const unsigned gmask = ((1u << kGroup) - 1) << (threadIdx.x & 31 & ~(kGroup - 1));
-  if (p >= np) return;
-  const int64_t base = seq_off[s] + p * P.bs;
+  if (blockIdx.x * static_cast<int64_t>(blockDim.x) / kGroup + (threadIdx.x & ~31) / kGroup >= np) return;
+  const bool active = p < np;
+  const int64_t pc = min(p, np - 1);
+  const int64_t base = seq_off[s] + pc * P.bs;
   const int len = static_cast<int>(min(P.bs, seq_off[s + 1] - base));
-  const uint64_t parent = p ? hashes[b0 + p - 1] : kRootHash;
-  const int32_t id = probe_find_g(P, hashes[b0 + p], parent, tokens + base, len, part, gmask);
-  if (part == 0) prehit[b0 + p] = id;
+  const uint64_t parent = pc ? hashes[b0 + pc - 1] : kRootHash;
+  const uint64_t h = hashes[b0 + pc];
+  const int32_t id = P.bs == 16 ? probe_find_g<true>(P, active, h, parent, tokens + base, len, part)
+                                 : probe_find_g<false>(P, active, h, parent, tokens + base, len, part);
+  if (part == 0 && active) prehit[b0 + p] = id;
 }
 
 __global__ void k_lookup_init(const int64_t* __restrict__ blk_off, int n_seqs, int64_t* first_miss) {
@@ -470,7 +654,7 @@ __device__ __forceinline__ void score_slice(const Pool& P, const int32_t* rank_o
   const bool tiered = P.policy == SB_POLICY_TIERED;
   auto one = [&](int32_t id, int nt, int rf, int pn, int rk, int tg, int64_t last) {
     const bool c = nt > 0 && rf == 0 && pn == 0 && rk != -2;
-    uint64_t k = (static_cast<uint64_t>(last + kLastBias) << kIdBits) | static_cast<uint64_t>(id);
+    uint64_t k = (static_cast<uint64_t>(last + P.lbias) << P.idb) | static_cast<uint64_t>(id);
     if (tiered) k |= static_cast<uint64_t>(tier_of(tg)) << 61;
     emit(c, k, nt == 0);
   };
@@ -701,7 +885,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
       const uint64_t k = dst[r];
       S.victims[r] = k;
       S.taken[r] = 0;
-      S.rank_of[k & kIdMask] = static_cast<int32_t>(r);
+      S.rank_of[k & P.idmask] = static_cast<int32_t>(r);
     }
   }
   // ---- lowest Fp free ids, ascending (std::set<int32_t> order)
@@ -771,9 +955,18 @@ struct CoopBuf {
   uint64_t* kmax;
   int n_slices;
   int64_t slice;             // blocks per score slice (multiple of 4)
+  int keys_in_smem;          // k_select_coop stages its slices' keys in shared memory (else reads them in place)
 };
 constexpr int kScoreThreads = 512;
-constexpr int kSlicesPerSm = 2;  // k_score CTAs per SM (one wave)
+constexpr int kSlicesPerSm = 2;  // score slices per SM; k_score CTA c scans slices c and c + n_sm
+// k_score streams the metadata through shared memory with 1-D bulk copies
+// (TMA engine): per stage, kScoreChunk blocks of ntok/ref/pinned/tag (4 B)
+// and last (8 B) = 48 KB; kScoreStages stages in flight per SM.
+constexpr int kScoreChunk = 2048;
+constexpr int kScoreStages = 4;
+constexpr size_t kScoreStageBytes = kScoreChunk * 24;
+constexpr size_t kScoreSmem = kScoreStages * kScoreStageBytes;
+static_assert(kScoreChunk == 4 * kScoreThreads, "k_score: 4 blocks per thread per chunk");
 
 __global__ void __launch_bounds__(kSelectThreads, 1)
     k_plan(Pool P, Scratch S, InsertArgs A, int s, int mode, CoopBuf G) {
@@ -832,53 +1025,142 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
   }
 }
 
-__global__ void __launch_bounds__(kScoreThreads, kSlicesPerSm) k_score(Pool P, Scratch S, CoopBuf G) {
-  extern __shared__ uint64_t cand[];  // [G.slice]
+// One persistent CTA per SM.  Thread 0 keeps kScoreStages chunks in flight
+// (5 bulk copies each, completion on the stage's mbarrier); all threads
+// score a landed chunk from shared memory and append the candidates' keys
+// to the slice's own region of the key list (one shared atomic per warp and
+// element slot).  The metadata of a pool block is read from HBM exactly once.
+__global__ void __launch_bounds__(kScoreThreads, 1) k_score(Pool P, Scratch S, CoopBuf G) {
+  extern __shared__ __align__(128) uint8_t stage_mem[];
+  __shared__ uint64_t full[kScoreStages];
   __shared__ unsigned int n_c, n_free;
   __shared__ unsigned long long kmin, kmax;
-  if (S.scal[S_STATUS] != 0) return;
   const int t = threadIdx.x;
+  const int n_my = (G.n_slices - static_cast<int>(blockIdx.x) + gridDim.x - 1) / gridDim.x;  // slices of this CTA
+  const int64_t chunks_per_slice = (G.slice + kScoreChunk - 1) / kScoreChunk;
+  auto slice_of = [&](int k) { return static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x); };
+  auto range = [&](int64_t c, int64_t& lo, int64_t& n) {  // chunk c of this CTA -> pool block range
+    const int sl = slice_of(static_cast<int>(c / chunks_per_slice));
+    const int64_t s_lo = sl * G.slice, s_hi = min(P.cap, s_lo + G.slice);
+    lo = s_lo + (c % chunks_per_slice) * kScoreChunk;
+    n = s_hi - lo < 0 ? 0 : (s_hi - lo < kScoreChunk ? s_hi - lo : int64_t(kScoreChunk));
+  };
+  const int64_t n_chunks = n_my * chunks_per_slice;
+  auto issue = [&](int64_t c) {
+    int64_t lo, n;
+    range(c, lo, n);
+    uint64_t* bar = &full[c % kScoreStages];
+    if (n == 0) {  // empty tail chunk: complete the phase without traffic
+      mbar_arrive(bar);
+      return;
+    }
+    uint8_t* st = stage_mem + (c % kScoreStages) * kScoreStageBytes;
+    const uint32_t b4 = static_cast<uint32_t>((n + 3) & ~int64_t(3)) * 4;  // arrays padded to a multiple of 4
+    const uint32_t b8 = static_cast<uint32_t>((n + 1) & ~int64_t(1)) * 8;
+    mbar_arrive_expect_tx(bar, 4 * b4 + b8);
+    bulk_g2s(st, P.ntok + lo, b4, bar);
+    bulk_g2s(st + 4 * kScoreChunk, P.ref + lo, b4, bar);
+    bulk_g2s(st + 8 * kScoreChunk, P.pinned + lo, b4, bar);
+    bulk_g2s(st + 12 * kScoreChunk, P.tag + lo, b4, bar);
+    bulk_g2s(st + 16 * kScoreChunk, P.last + lo, b8, bar);
+  };
   if (t == 0) {
+    for (int i = 0; i < kScoreStages; ++i) mbar_init(&full[i], 1);
+    fence_barrier_init();
     n_c = 0;
     n_free = 0;
     kmin = ~0ull;
     kmax = 0;
   }
   __syncthreads();
-  const int64_t lo = blockIdx.x * G.slice, hi = min(P.cap, lo + G.slice);
+  if (t == 0)
+    for (int64_t c = 0; c < n_chunks && c < kScoreStages; ++c) issue(c);
+  const bool tiered = P.policy == SB_POLICY_TIERED;
+  const int lane = t & 31;
   uint64_t mn = ~0ull, mx = 0;
   unsigned nf = 0;
-  score_slice<1, false>(P, nullptr, lo, hi, [&](bool c, uint64_t k, bool fr) {
-    bool mine;
-    const uint64_t at = warp_append_slot(c, &n_c, mine);
-    if (mine) {
-      cand[at] = k;
-      mn = min(mn, k);
-      mx = max(mx, k);
-    }
-    nf += fr;
-  });
-  nf = __reduce_add_sync(0xffffffffu, nf);
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    int64_t lo, n;
+    range(c, lo, n);
+    const int sl = slice_of(static_cast<int>(c / chunks_per_slice));
+    mbar_wait(&full[c % kScoreStages], static_cast<uint32_t>((c / kScoreStages) & 1));
+    const uint8_t* st = stage_mem + (c % kScoreStages) * kScoreStageBytes;
+    // thread t scores blocks 4t .. 4t+3 of the chunk: 16 B shared loads
+    const int i0 = 4 * t;
+    const int4 nt4 = reinterpret_cast<const int4*>(st)[t];
+    const int4 rf4 = reinterpret_cast<const int4*>(st + 4 * kScoreChunk)[t];
+    const int4 pn4 = reinterpret_cast<const int4*>(st + 8 * kScoreChunk)[t];
+    const int4 tg4 = reinterpret_cast<const int4*>(st + 12 * kScoreChunk)[t];
+    const longlong2 la0 = reinterpret_cast<const longlong2*>(st + 16 * kScoreChunk)[2 * t];
+    const longlong2 la1 = reinterpret_cast<const longlong2*>(st + 16 * kScoreChunk)[2 * t + 1];
+    const int nt[4] = {nt4.x, nt4.y, nt4.z, nt4.w}, rf[4] = {rf4.x, rf4.y, rf4.z, rf4.w};
+    const int pn[4] = {pn4.x, pn4.y, pn4.z, pn4.w}, tg[4] = {tg4.x, tg4.y, tg4.z, tg4.w};
+    const int64_t la[4] = {la0.x, la0.y, la1.x, la1.y};
+    uint64_t key[4];
+    unsigned cm = 0;  // candidate mask of the thread's 4 blocks
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int u = 0; u < 4; ++u) {
+      const bool in = i0 + u < n;
+      const bool cnd = in && nt[u] > 0 && rf[u] == 0 && pn[u] == 0;
+      nf += in && nt[u] == 0;
+      // tier_of as a nibble table: tags 0..5 -> 0,1,2,3,4,2 (kv_cache.cpp:23-33)
+      const uint64_t tier = tiered && static_cast<unsigned>(tg[u]) < 6u ? (0x243210u >> (4 * tg[u])) & 0xFu : 0u;
+      key[u] = (tier << 61) | (static_cast<uint64_t>(la[u] + P.lbias) << P.idb) | static_cast<uint64_t>(lo + i0 + u);
+      cm |= static_cast<unsigned>(cnd) << u;
+      if (cnd) {
+        mn = min(mn, key[u]);
+        mx = max(mx, key[u]);
+      }
+    }
+    // warp-aggregated append: exclusive scan of the per-thread counts
+    const unsigned cnt = __popc(cm);
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    unsigned base = 0;
+    if (lane == 31 && incl) base = atomicAdd(&n_c, incl);
+    base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+    uint64_t* out = G.keys + sl * G.slice;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (cm >> u & 1) out[base++] = key[u];
+    __syncthreads();  // stage consumed by every thread
+    if (t == 0 && c + kScoreStages < n_chunks) {
+      fence_proxy_async();
+      issue(c + kScoreStages);
+    }
+    if ((c + 1) % chunks_per_slice == 0) {  // slice done: publish its counts and key range
+      nf = __reduce_add_sync(0xffffffffu, nf);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      if ((t & 31) == 0) {
+        atomicAdd(&n_free, nf);
+        atomicMin(&kmin, mn);
+        atomicMax(&kmax, mx);
+      }
+      __syncthreads();
+      if (t == 0) {
+        G.fcnt[sl] = n_free;
+        G.ncnt[sl] = n_c;
+        G.kmin[sl] = kmin;
+        G.kmax[sl] = kmax;
+        n_c = 0;
+        n_free = 0;
+        kmin = ~0ull;
+        kmax = 0;
+      }
+      __syncthreads();
+      mn = ~0ull;
+      mx = 0;
+      nf = 0;
+    }
   }
-  if ((t & 31) == 0) {
-    atomicAdd(&n_free, nf);
-    atomicMin(&kmin, mn);
-    atomicMax(&kmax, mx);
-  }
-  __syncthreads();
-  const unsigned nc = n_c;
-  if (t == 0) {
-    G.fcnt[blockIdx.x] = n_free;
-    G.ncnt[blockIdx.x] = nc;
-    G.kmin[blockIdx.x] = kmin;
-    G.kmax[blockIdx.x] = kmax;
-  }
-  uint64_t* out = G.keys + lo;  // the slice's own region: no global atomics
-  for (unsigned i = t; i < nc; i += blockDim.x) out[i] = cand[i];
 }
 
 __global__ void __launch_bounds__(kSelectThreads, 1)
@@ -975,14 +1257,29 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
       }
     }
   }
-  // ---- radix select of the K smallest candidate keys (keys are unique)
+  // ---- radix select of the K smallest candidate keys (keys are unique).
+  // The CTA's keys: its score slices' regions of G.keys, staged in shared
+  // memory when they fit, else read in place each pass (L2-resident).
   int64_t nl = 0;
-  for (int sl = cta; sl < G.n_slices; sl += n_cta) {
-    const int64_t c = G.ncnt[sl];
-    const uint64_t* src = G.keys + sl * G.slice;
-    for (int64_t i = t; i < c; i += blockDim.x) local_keys[nl + i] = src[i];
-    nl += c;
+  if (G.keys_in_smem) {
+    for (int sl = cta; sl < G.n_slices; sl += n_cta) {
+      const int64_t c = G.ncnt[sl];
+      const uint64_t* src = G.keys + sl * G.slice;
+      for (int64_t i = t; i < c; i += blockDim.x) local_keys[nl + i] = src[i];
+      nl += c;
+    }
   }
+  auto for_keys = [&](auto&& f) {
+    if (G.keys_in_smem) {
+      for (int64_t i = t; i < nl; i += blockDim.x) f(local_keys[i]);
+    } else {
+      for (int sl = cta; sl < G.n_slices; sl += n_cta) {
+        const int64_t c = G.ncnt[sl];
+        const uint64_t* src = G.keys + sl * G.slice;
+        for (int64_t i = t; i < c; i += blockDim.x) f(src[i]);
+      }
+    }
+  };
   __syncthreads();
   uint64_t prefix = 0, mask = 0;
   if (K > 0 && K < ncand) {
@@ -998,10 +1295,9 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
       hist[2 * t] = 0;
       hist[2 * t + 1] = 0;
       __syncthreads();
-      for (int64_t i = t; i < nl; i += blockDim.x) {
-        const uint64_t k = local_keys[i];
+      for_keys([&](uint64_t k) {
         if ((k & mask) == prefix) atomicAdd(&hist[(k >> sh_) & bmask], 1u);
-      }
+      });
       __syncthreads();
       uint32_t* gh = G.hist + pass * 2048;
       if (hist[2 * t]) atomicAdd(&gh[2 * t], hist[2 * t]);
@@ -1033,10 +1329,9 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
     }
   }
   if (K > 0)
-    for (int64_t i = t; i < nl; i += blockDim.x) {
-      const uint64_t k = local_keys[i];
+    for_keys([&](uint64_t k) {
       if (K == ncand || (k & mask) <= prefix) S.sortbuf[atomicAdd(&G.ctr[1], 1ull)] = k;
-    }
+    });
   grid.sync();
   if (cta != 0) return;
   // ---- CTA 0: sort the K selected keys, publish them with their ranks
@@ -1059,7 +1354,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
       const uint64_t k = dst[r];
       S.victims[r] = k;
       S.taken[r] = 0;
-      S.rank_of[k & kIdMask] = static_cast<int32_t>(r);
+      S.rank_of[k & P.idmask] = static_cast<int32_t>(r);
     }
   }
   if (t == 0) {
@@ -1096,7 +1391,7 @@ __global__ void __launch_bounds__(32, 1) k_walk(Pool P, Scratch S, InsertArgs A,
       taken_s[r] = 0;
     }
   uint8_t* taken = vs ? taken_s : S.taken;
-  const uint64_t now_bits = static_cast<uint64_t>(A.now + kLastBias) << kIdBits;
+  const uint64_t now_bits = static_cast<uint64_t>(A.now + P.lbias) << P.idb;
   // late candidates: blocks that a hit in this insert raised from ref -1 to 0
   uint64_t lkey[kLateMax];
   int32_t lpos[kLateMax];
@@ -1167,10 +1462,10 @@ __global__ void __launch_bounds__(32, 1) k_walk(Pool P, Scratch S, InsertArgs A,
             break;
           }
           if (use_list) {
-            id = static_cast<int32_t>(vk & kIdMask);
+            id = static_cast<int32_t>(vk & P.idmask);
             ++ptr;
           } else {
-            id = static_cast<int32_t>(lkey[li] & kIdMask);
+            id = static_cast<int32_t>(lkey[li] & P.idmask);
             S.kind[lpos[li]] = 2;  // hit, then evicted later in this insert
             lkey[li] = lkey[nl - 1];
             lpos[li] = lpos[nl - 1];
@@ -1199,7 +1494,7 @@ __global__ void k_commit_evict(Pool P, Scratch S) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nev;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int32_t id = S.evicted[i];
-    P.tval[P.slot[id]] = -2;
+    P.idx[P.slot[id]].id = -2;
     P.ntok[id] = 0;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && nev > 0) {
@@ -1223,7 +1518,7 @@ __global__ void k_commit_apply(Pool P, Scratch S, InsertArgs A, int s) {
   const int64_t K = S.scal[S_K];
   const int64_t gid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t r = gid; r < K; r += stride) S.rank_of[S.victims[r] & kIdMask] = -1;
+  for (int64_t r = gid; r < K; r += stride) S.rank_of[S.victims[r] & P.idmask] = -1;
   if (gid == 0) {
     A.status[s] = static_cast<int32_t>(status);
     if (status == 0) {
@@ -1263,7 +1558,7 @@ __global__ void k_commit_apply(Pool P, Scratch S, InsertArgs A, int s) {
       P.ref[id] = 1;
       P.last[id] = A.now;
       P.pinned[id] = 0;
-      index_insert(P, h, id);
+      index_insert(P, h, id, P.parent[id], len);
     }
     if (status == 0) A.out_ids[b0 + p] = id;
   }
@@ -1305,11 +1600,11 @@ __global__ void k_priority_apply(Pool P, const int32_t* ids, int64_t n, int pinn
 }
 __global__ void k_set_scal(int64_t* scal, int idx, int64_t v) { scal[idx] = v; }
 
-__global__ void k_evict_out(Scratch S, int32_t* out, int64_t* n_out) {
+__global__ void k_evict_out(Pool P, Scratch S, int32_t* out, int64_t* n_out) {
   const int64_t K = S.scal[S_K];
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < K;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int32_t id = static_cast<int32_t>(S.victims[r] & kIdMask);
+    const int32_t id = static_cast<int32_t>(S.victims[r] & P.idmask);
     out[r] = id;
     S.evicted[r] = id;
     S.rank_of[id] = -1;
@@ -1324,12 +1619,12 @@ __global__ void k_evict_out(Scratch S, int32_t* out, int64_t* n_out) {
 __global__ void k_index_clear(Pool P) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < P.tcap;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    P.tval[i] = -1;
+    P.idx[i].id = -1;
 }
 __global__ void k_index_fill(Pool P) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < P.cap;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    if (P.ntok[i] > 0) index_insert(P, P.chain[i], static_cast<int32_t>(i));
+    if (P.ntok[i] > 0) index_insert(P, P.chain[i], static_cast<int32_t>(i), P.parent[i], P.ntok[i]);
 }
 
 __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
@@ -1345,6 +1640,34 @@ static T* dalloc(size_t n) {
   if (n == 0) n = 1;
   SB_CUDA(cudaMalloc(&p, n * sizeof(T)));
   return p;
+}
+
+static void check_now(const Pool& P, int64_t now) {
+  if (now < -P.lbias || now >= P.lbias)
+    throw Error(SB_ERR_UNSUPPORTED, "now outside +-2^" + std::to_string(60 - P.idb) + " for this pool size");
+}
+
+static void launch_probe_rows(const Pool& P, const uint64_t* tokens, const int64_t* seq_off, const int64_t* blk_off,
+                              const uint64_t* hashes, int32_t* prehit, int64_t* first_miss, int full_only_check,
+                              int n_seqs, int64_t max_np, cudaStream_t st) {
+  static int per = -1;
+  if (per < 0) {
+    const char* e = getenv("SB_PROBE_PER");
+    per = e ? atoi(e) : 2;
+  }
+  const int run = kProbePairs * per;
+  const int64_t runs = (max_np + run - 1) / run;
+  if (runs > 65535) throw Error(SB_ERR_UNSUPPORTED, "sequence too long for one lookup launch");
+  const dim3 grid(n_seqs, static_cast<unsigned>(runs));
+  if (per == 1)
+    k_probe_rows<1><<<grid, kProbePairs * kGroup, 0, st>>>(P, tokens, seq_off, blk_off, hashes, prehit, first_miss,
+                                                            full_only_check);
+  else if (per == 2)
+    k_probe_rows<2><<<grid, kProbePairs * kGroup, 0, st>>>(P, tokens, seq_off, blk_off, hashes, prehit, first_miss,
+                                                            full_only_check);
+  else
+    k_probe_rows<4><<<grid, kProbePairs * kGroup, 0, st>>>(P, tokens, seq_off, blk_off, hashes, prehit, first_miss,
+                                                            full_only_check);
 }
 
 static int grid_for(int64_t n, int threads = 256) {
@@ -1394,7 +1717,7 @@ struct sb_kv_cache {
       return;
     }
     k_plan<<<1, kSelectThreads, 0, stream>>>(P, S, A, s, mode, G);
-    k_score<<<G.n_slices, kScoreThreads, G.slice * sizeof(uint64_t), stream>>>(P, S, G);
+    k_score<<<coop_grid, kScoreThreads, kScoreSmem, stream>>>(P, S, G);
     Pool p_ = P;
     Scratch s_ = S;
     InsertArgs a_ = A;
@@ -1418,7 +1741,7 @@ struct sb_kv_cache {
   ~sb_kv_cache() {
     cudaSetDevice(device);
     // S.prehit aliases d_prehit_all: freed once below
-    void* ptrs[] = {P.tok, P.ntok, P.chain, P.parent, P.tag, P.ref, P.pinned, P.last, P.tkey, P.tval, P.slot, P.ctr,
+    void* ptrs[] = {P.tok, P.ntok, P.chain, P.parent, P.tag, P.ref, P.pinned, P.last, P.idx, P.slot, P.ctr,
                     S.hashes, S.chain_out, S.kind, S.freel, S.evicted, S.victims, S.taken, S.rank_of, S.keys,
                     S.sortbuf, S.scal, S.late, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first, G.hist, G.ctr, G.keys, G.fcnt, G.ncnt, G.kmin, G.kmax};
     for (void* p : ptrs)
@@ -1567,7 +1890,7 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
   return guard([&] {
     if (block_size < 1) throw Error(SB_ERR_CONFIG, "cache block_size must be >= 1");
     if (capacity_blocks < 1) throw Error(SB_ERR_CONFIG, "cache capacity_blocks must be >= 1");
-    if (capacity_blocks > (int64_t(1) << kIdBits)) throw Error(SB_ERR_UNSUPPORTED, "capacity above 2^21 blocks");
+    if (capacity_blocks > (int64_t(1) << kMaxIdBits)) throw Error(SB_ERR_UNSUPPORTED, "capacity above 2^24 blocks");
     if (policy != SB_POLICY_LRU && policy != SB_POLICY_TIERED) throw Error(SB_ERR_CONFIG, "unknown policy");
     SB_CUDA(cudaSetDevice(device));
     auto* c = new sb_kv_cache();
@@ -1579,25 +1902,30 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
       P.bs = block_size;
       P.cap = capacity_blocks;
       P.policy = policy;
+      P.idb = kMinIdBits;
+      while ((int64_t(1) << P.idb) < capacity_blocks) ++P.idb;
+      P.idmask = (uint64_t(1) << P.idb) - 1;
+      P.lbias = int64_t(1) << (60 - P.idb);
       P.tcap = 16;
       while (P.tcap < 4 * capacity_blocks) P.tcap <<= 1;
+      // metadata arrays padded to whole 16 B vectors (k_score's bulk copies)
+      const int64_t cap_pad = (capacity_blocks + 3) & ~int64_t(3);
       P.tok = dalloc<uint64_t>(static_cast<size_t>(block_size * capacity_blocks));
-      P.ntok = dalloc<int32_t>(capacity_blocks);
+      P.ntok = dalloc<int32_t>(cap_pad);
       P.chain = dalloc<uint64_t>(capacity_blocks);
       P.parent = dalloc<uint64_t>(capacity_blocks);
-      P.tag = dalloc<int32_t>(capacity_blocks);
-      P.ref = dalloc<int32_t>(capacity_blocks);
-      P.pinned = dalloc<int32_t>(capacity_blocks);
-      P.last = dalloc<int64_t>(capacity_blocks);
-      P.tkey = dalloc<uint64_t>(P.tcap);
-      P.tval = dalloc<int32_t>(P.tcap);
+      P.tag = dalloc<int32_t>(cap_pad);
+      P.ref = dalloc<int32_t>(cap_pad);
+      P.pinned = dalloc<int32_t>(cap_pad);
+      P.last = dalloc<int64_t>(cap_pad);
+      P.idx = dalloc<IdxEntry>(P.tcap);
       P.slot = dalloc<int32_t>(capacity_blocks);
       P.ctr = dalloc<unsigned long long>(C_N);
-      SB_CUDA(cudaMemsetAsync(P.ntok, 0, sizeof(int32_t) * capacity_blocks, c->stream));
-      SB_CUDA(cudaMemsetAsync(P.ref, 0, sizeof(int32_t) * capacity_blocks, c->stream));
-      SB_CUDA(cudaMemsetAsync(P.pinned, 0, sizeof(int32_t) * capacity_blocks, c->stream));
+      SB_CUDA(cudaMemsetAsync(P.ntok, 0, sizeof(int32_t) * cap_pad, c->stream));
+      SB_CUDA(cudaMemsetAsync(P.ref, 0, sizeof(int32_t) * cap_pad, c->stream));
+      SB_CUDA(cudaMemsetAsync(P.pinned, 0, sizeof(int32_t) * cap_pad, c->stream));
       SB_CUDA(cudaMemsetAsync(P.ctr, 0, sizeof(unsigned long long) * C_N, c->stream));
-      k_fill_i32<<<grid_for(P.tcap), 256, 0, c->stream>>>(P.tval, P.tcap, -1);
+      k_index_clear<<<grid_for(P.tcap), 256, 0, c->stream>>>(P);
       Scratch& S = c->S;
       S.rank_of = dalloc<int32_t>(capacity_blocks);
       k_fill_i32<<<grid_for(capacity_blocks), 256, 0, c->stream>>>(S.rank_of, capacity_blocks, -1);
@@ -1619,8 +1947,15 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
         SB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
         const int n_slices = kSlicesPerSm * n_sm;  // k_score partition; k_select_coop CTA c owns slices c, c + n_sm, ...
         const int64_t slice = ((capacity_blocks + n_slices - 1) / n_slices + 3) & ~int64_t(3);
-        c->coop_smem = static_cast<size_t>(std::max<int64_t>(kSlicesPerSm * slice, kSortSmemKeys)) * sizeof(uint64_t);
-        if (c->coop_smem <= 200 * 1024) {
+        cudaFuncAttributes fa{};
+        SB_CUDA(cudaFuncGetAttributes(&fa, k_select_coop));
+        int smem_optin = 0;
+        SB_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        const size_t staged = static_cast<size_t>(std::max<int64_t>(kSlicesPerSm * slice, kSortSmemKeys)) * sizeof(uint64_t);
+        c->G.keys_in_smem = staged + fa.sharedSizeBytes <= static_cast<size_t>(smem_optin);
+        c->coop_smem = c->G.keys_in_smem ? staged : kSortSmemKeys * sizeof(uint64_t);
+        SB_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScoreSmem)));
+        {
           SB_CUDA(cudaFuncSetAttribute(k_select_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(c->coop_smem)));
           SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_coop, kSelectThreads, c->coop_smem));
@@ -1634,8 +1969,6 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
           c->G.ncnt = dalloc<uint32_t>(n_slices);
           c->G.kmin = dalloc<uint64_t>(n_slices);
           c->G.kmax = dalloc<uint64_t>(n_slices);
-          SB_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(c->G.slice * sizeof(uint64_t))));
         }
       }
       SB_CHECK_LAUNCH();
@@ -1655,7 +1988,7 @@ int sb_kv_lookup_prefix(sb_kv_cache* c, const uint64_t* tokens, int64_t n, int64
   return guard([&] {
     std::lock_guard<std::mutex> lk(c->mu);
     SB_CUDA(cudaSetDevice(c->device));
-    if (now < -kLastBias || now >= kLastBias) throw Error(SB_ERR_UNSUPPORTED, "now outside +-2^39");
+    check_now(c->P, now);
     const int64_t nblk = n / c->P.bs;
     *hit_tokens = 0;
     if (nblk == 0) return int(SB_OK);
@@ -1669,8 +2002,8 @@ int sb_kv_lookup_prefix(sb_kv_cache* c, const uint64_t* tokens, int64_t n, int64
     const int64_t* blk_off = c->d_meta + 2;
     launch_chain_hash(c->d_tok, seq_off, blk_off, nullptr, 1, c->P.bs, 1, c->d_hash_all, c->stream);
     k_lookup_init<<<1, 32, 0, c->stream>>>(blk_off, 1, c->d_first);
-    k_probe_batch<<<grid_for(nblk * kGroup), 256, 0, c->stream>>>(c->P, c->d_tok, seq_off, blk_off, 1, c->d_hash_all, nblk,
-                                                         c->d_prehit_all, c->d_first, 0);
+    launch_probe_rows(c->P, c->d_tok, seq_off, blk_off, c->d_hash_all, c->d_prehit_all, c->d_first, 0, 1, nblk,
+                      c->stream);
     k_lookup_finish<<<grid_for(nblk + 1), 256, 0, c->stream>>>(c->P, seq_off, blk_off, 1, nblk, c->d_prehit_all,
                                                                c->d_first, now, c->d_hit);
     SB_CHECK_LAUNCH();
@@ -1688,7 +2021,7 @@ int sb_kv_lookup_prefix_batch(sb_kv_cache* c, const uint64_t* d_tokens, const in
     std::lock_guard<std::mutex> lk(c->mu);
     SB_CUDA(cudaSetDevice(c->device));
     if (n_seqs <= 0) return int(SB_OK);
-    if (now < -kLastBias || now >= kLastBias) throw Error(SB_ERR_UNSUPPORTED, "now outside +-2^39");
+    check_now(c->P, now);
     cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
     std::vector<int64_t> off(n_seqs + 1), blk(n_seqs + 1);
     const bool pre = d_block_hashes && d_block_offsets;
@@ -1719,9 +2052,13 @@ int sb_kv_lookup_prefix_batch(sb_kv_cache* c, const uint64_t* d_tokens, const in
       hashes = c->d_hash_all;
     }
     k_lookup_init<<<(n_seqs + 127) / 128, 128, 0, st>>>(d_blk, n_seqs, c->d_batch_first);
-    if (total > 0)
-      k_probe_batch<<<grid_for(total * kGroup), 256, 0, st>>>(c->P, d_tokens, d_seq_offsets, d_blk, n_seqs, hashes, total,
-                                                     c->d_prehit_all, c->d_batch_first, pre ? 1 : 0);
+    if (total > 0) {
+      const std::vector<int64_t>& bo = pre ? off : blk;
+      int64_t max_np = 0;
+      for (int i = 0; i < n_seqs; ++i) max_np = std::max(max_np, bo[i + 1] - bo[i]);
+      launch_probe_rows(c->P, d_tokens, d_seq_offsets, d_blk, hashes, c->d_prehit_all, c->d_batch_first, pre ? 1 : 0,
+                        n_seqs, max_np, st);
+    }
     k_lookup_finish<<<grid_for(std::max<int64_t>(total, n_seqs)), 256, 0, st>>>(
         c->P, d_seq_offsets, d_blk, n_seqs, total, c->d_prehit_all, c->d_batch_first, now, d_hit_tokens);
     SB_CHECK_LAUNCH();
@@ -1735,7 +2072,7 @@ int sb_kv_insert(sb_kv_cache* c, const uint64_t* tokens, int64_t n, const sb_tag
     std::lock_guard<std::mutex> lk(c->mu);
     SB_CUDA(cudaSetDevice(c->device));
     *n_out = 0;
-    if (now < -kLastBias || now >= kLastBias) throw Error(SB_ERR_UNSUPPORTED, "now outside +-2^39");
+    check_now(c->P, now);
     const int64_t nblk = (n + c->P.bs - 1) / c->P.bs;
     c->ensure_tokens(std::max<int64_t>(n, 1));
     c->ensure_tags(std::max<int64_t>(n_tags, 1));
@@ -1769,7 +2106,7 @@ int sb_kv_insert_batch(sb_kv_cache* c, const uint64_t* d_tokens, const int64_t* 
     std::lock_guard<std::mutex> lk(c->mu);
     SB_CUDA(cudaSetDevice(c->device));
     if (n_seqs <= 0) return int(SB_OK);
-    if (now < -kLastBias || now >= kLastBias) throw Error(SB_ERR_UNSUPPORTED, "now outside +-2^39");
+    check_now(c->P, now);
     std::vector<int64_t> hb(n_seqs + 1);
     if (h_block_offsets)
       std::memcpy(hb.data(), h_block_offsets, sizeof(int64_t) * (n_seqs + 1));
@@ -1800,7 +2137,7 @@ int sb_kv_evict(sb_kv_cache* c, int64_t needed, int32_t* out_ids, int64_t* n_out
     c->ensure_ids(std::min<int64_t>(needed, c->P.cap) + 1);
     InsertArgs A{};
     c->launch_select(A, 0, 1, needed);
-    k_evict_out<<<grid_for(c->P.cap), 256, 0, c->stream>>>(c->S, c->d_ids, c->d_first);
+    k_evict_out<<<grid_for(c->P.cap), 256, 0, c->stream>>>(c->P, c->S, c->d_ids, c->d_first);
     k_commit_evict<<<grid_for(c->P.cap), 256, 0, c->stream>>>(c->P, c->S);
     SB_CHECK_LAUNCH();
     int64_t k = 0;
@@ -1945,9 +2282,10 @@ int sb_kv_block(const sb_kv_cache* c, int32_t id, sb_block_info* info, uint64_t*
 
 namespace {
 struct HostView {
-  std::vector<int32_t> ntok, tag, ref, pinned, tval;
+  std::vector<int32_t> ntok, tag, ref, pinned;
   std::vector<int64_t> last;
-  std::vector<uint64_t> chain, tkey;
+  std::vector<uint64_t> chain, parent;
+  std::vector<IdxEntry> idx;
   unsigned long long nres = 0;
 };
 HostView read_view(const sb_kv_cache* c, bool with_index) {
@@ -1966,11 +2304,11 @@ HostView read_view(const sb_kv_cache* c, bool with_index) {
   SB_CUDA(cudaMemcpy(&v.nres, P.ctr + C_NRES, 8, cudaMemcpyDeviceToHost));
   if (with_index) {
     v.chain.resize(P.cap);
-    v.tkey.resize(P.tcap);
-    v.tval.resize(P.tcap);
+    v.parent.resize(P.cap);
+    v.idx.resize(P.tcap);
     SB_CUDA(cudaMemcpy(v.chain.data(), P.chain, 8 * P.cap, cudaMemcpyDeviceToHost));
-    SB_CUDA(cudaMemcpy(v.tkey.data(), P.tkey, 8 * P.tcap, cudaMemcpyDeviceToHost));
-    SB_CUDA(cudaMemcpy(v.tval.data(), P.tval, 4 * P.tcap, cudaMemcpyDeviceToHost));
+    SB_CUDA(cudaMemcpy(v.parent.data(), P.parent, 8 * P.cap, cudaMemcpyDeviceToHost));
+    SB_CUDA(cudaMemcpy(v.idx.data(), P.idx, sizeof(IdxEntry) * P.tcap, cudaMemcpyDeviceToHost));
   }
   return v;
 }
@@ -1994,9 +2332,11 @@ int sb_kv_audit(const sb_kv_cache* c) {
     if (res != static_cast<int64_t>(v.nres) || res > c->P.cap) throw Error(SB_ERR_CACHE, "audit: block accounting mismatch");
     int64_t indexed = 0;
     for (int64_t s = 0; s < c->P.tcap; ++s) {
-      const int32_t id = v.tval[s];
+      const IdxEntry& e = v.idx[s];
+      const int32_t id = e.id;
       if (id < 0) continue;
-      if (v.ntok[id] == 0 || v.chain[id] != v.tkey[s]) throw Error(SB_ERR_CACHE, "audit: hash index out of sync");
+      if (v.ntok[id] == 0 || v.chain[id] != e.key || v.parent[id] != e.parent || v.ntok[id] != e.ntok)
+        throw Error(SB_ERR_CACHE, "audit: hash index out of sync");
       ++indexed;
     }
     if (indexed != res) throw Error(SB_ERR_CACHE, "audit: hash index size mismatch");

@@ -193,3 +193,27 @@ def test_large_pool_cooperative_scorer():
         assert o.insert(t, tags, 100 + k) == c.insert(t, tags, 100 + k)
     assert o.dump() == c.dump()
     assert o.total_evicted() == c.total_evicted()
+
+
+@pytest.mark.gpu
+def test_huge_pool_keys_read_in_place():
+    """Pools above ~4.1M blocks: k_select_coop cannot stage its slices' keys
+    in shared memory and radix-selects them in place; victim keys carry
+    23 id bits (now limited to +-2^37).  Same oracle parity bar."""
+    bs, cap = 1, 4_500_000
+    c = product(bs, cap, 1)
+    o = O.OracleCache(bs, cap, 1)
+    rng = np.random.default_rng(5)
+    live = []
+    for k in range(12):
+        t = O.materialize(int(rng.integers(4)), 3000, 700 + k)
+        tags = [(0, 1500, int(rng.integers(6))), (1500, 3000, int(rng.integers(6)))]
+        a, b = o.insert(t, tags, k * 1000), c.insert(t, tags, k * 1000)
+        assert a == b, k
+        live.append(a[1])
+    for ids in live[1::2]:
+        assert o.release(ids) == c.release(ids) == 0
+    for needed in (3, 2049, 9000):
+        assert o.evict(needed) == c.evict(needed), needed
+    assert o.dump() == c.dump()
+    c.audit()
