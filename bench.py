@@ -48,6 +48,24 @@ def parse():
     return ap.parse_args()
 
 
+ATTN_NCU = os.path.join(ROOT, "profiles", "r01", "attention_v3_metrics.json")
+
+
+def ncu_traffic(path):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one `ncu --set full`
+    capture of the kernel (committed under profiles/), in bytes per launch."""
+    try:
+        m = json.load(open(path))
+    except Exception:
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tot = 0.0
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        v, u = m[k]
+        tot += float(v) * scale[u]
+    return tot
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -260,7 +278,8 @@ def run_ours(args, rank, world, local_rank):
                 "h2d_bytes_per_step": tokens_per_step * 8, "d2h_bytes_per_step": d2h // args.steps},
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "kernel": "k_continuation_attention", "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": ncu_traffic(ATTN_NCU),
+                     "traffic_source": "profiles/r01/attention_v3_metrics.json (ncu --set full, one launch, bytes)",
                      "peak_source": f"{peak_kind} bf16_tflops_sustained (kernel timed inside a long step)",
                      "flops_per_launch": flops_attn, "avg_launch_ms": attn_avg_ms,
                      "launches_timed": len(attn_ms)},

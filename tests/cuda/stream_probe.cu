@@ -68,6 +68,23 @@ __global__ void k_bulk(const uint8_t* __restrict__ p, int64_t nbytes, int chunk,
   if (acc == 0x12345678u) *out = acc;
 }
 
+// random access: each group of G lanes reads one random aligned line of
+// 16*G bytes (G = 2: 32 B sector, G = 8: 128 B line) from a region.
+template <int G>
+__global__ void k_rand(const int4* __restrict__ p, int64_t region16, int64_t n_reads, unsigned* out) {
+  unsigned acc = 0;
+  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+  const int part = threadIdx.x % G;
+  for (int64_t r = gid / G; r < n_reads; r += (int64_t)gridDim.x * blockDim.x / G) {
+    uint64_t h = (uint64_t)r * 0x9e3779b97f4a7c15ull;
+    h ^= h >> 29;
+    const int64_t line = (int64_t)(h % (uint64_t)(region16 / G));
+    int4 v = __ldg(p + line * G + part);
+    acc ^= v.x ^ v.w;
+  }
+  if (acc == 0x12345678u) *out = acc;
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -122,6 +139,15 @@ int main() {
         float ms = timeit([&] { k_bulk<8><<<sms * ctas, 256, smem>>>(buf, nb, chunk, out); });
         printf("{\"kind\":\"bulk\",\"mb\":%lld,\"chunk\":%d,\"stages\":8,\"ctas_per_sm\":%d,\"us\":%.2f,\"gbs\":%.0f}\n", (long long)(nb >> 20), chunk, ctas, ms * 1e3, nb / (ms * 1e-3) / 1e9);
       }
+    }
+  }
+  for (int64_t nb : {int64_t(100) << 20, int64_t(400) << 20}) {
+    const int64_t region = int64_t(1) << 31;
+    for (int per_sm : {8, 16}) {
+      float ms = timeit([&] { k_rand<2><<<sms * per_sm, 256>>>((const int4*)buf, region / 16, nb / 32, out); });
+      printf("{\"kind\":\"rand32\",\"mb\":%lld,\"ctas_per_sm\":%d,\"us\":%.2f,\"gbs\":%.0f}\n", (long long)(nb >> 20), per_sm, ms * 1e3, nb / (ms * 1e-3) / 1e9);
+      ms = timeit([&] { k_rand<8><<<sms * per_sm, 256>>>((const int4*)buf, region / 16, nb / 128, out); });
+      printf("{\"kind\":\"rand128\",\"mb\":%lld,\"ctas_per_sm\":%d,\"us\":%.2f,\"gbs\":%.0f}\n", (long long)(nb >> 20), per_sm, ms * 1e3, nb / (ms * 1e-3) / 1e9);
     }
   }
   cudaError_t e = cudaDeviceSynchronize();
