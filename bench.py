@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--requests", type=int, default=N_REQ)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true", help="skip the configs[2] full-model measurement")
     return ap.parse_args()
 
 
@@ -285,10 +286,94 @@ def run_ours(args, rank, world, local_rank):
                      "launches_timed": len(attn_ms)},
         "clocks": clk,
     }
+    del batch, eng
+    torch.cuda.empty_cache()
+    if not args.no_dense:
+        line["full_model"] = run_dense(args, rank, world, local_rank)
     line.update(trace_replay_metrics(line["value"], local_rank))
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(reqs, budget_s=20.0)
     return line
+
+
+def run_dense(args, rank, world, local_rank):
+    """BASELINE configs[2]: Llama-3-8B-shaped bf16 continuation prefill over
+    8K-32K cached prefixes with random-init weights — the full model per
+    step (embedding, 32 x {RMSNorm, QKV GEMM, RoPE + KV scatter, paged
+    continuation attention, O GEMM, SwiGLU MLP}, LM head + greedy token on
+    each sequence's last token) plus the pool ops (hash, lookup, insert with
+    eviction, release).  GEMMs are cuBLAS; everything else is ours."""
+    import torch
+    import torch.distributed as dist
+    from paper_2601_12967_b200 import workload as W
+    from paper_2601_12967_b200.engine import LLAMA3_8B, LLAMA3_8B_DENSE, ContinuationEngine, DenseModel
+    from paper_2601_12967_b200.kv_cache import TIERED
+
+    dev = torch.device("cuda", local_rank)
+    reqs = W.long_prefix_continuation_batch(8, seed=rank + 1)
+    pre_b, suf_b, cap = capacity_for(reqs, slack=2.5)
+    eng = ContinuationEngine(LLAMA3_8B, cap, TIERED, device=local_rank, seed=rank)
+    model = DenseModel(LLAMA3_8B_DENSE, seed=rank, device=local_rank)
+    handles = [eng.submit_partial_prefill(r.prefix_tokens, r.prefix_tags, now=0) for r in reqs]
+    batch = eng.make_batch(handles, [r.suffix_len for r in reqs])
+    batch.set_model(model)
+    steps, warm = max(2, args.steps), max(3, args.warmup)
+    host = [torch.from_numpy(np.concatenate([W.fresh_suffix_tokens(r, s) for r in reqs]).view(np.int64)).pin_memory()
+            for s in range(warm + 2 * steps)]
+    devs = [h.to(dev) for h in host]
+    now = 10
+    for s in range(warm):
+        now += 1
+        batch.stage_suffix_device(devs[s])
+        batch.run(now, seed=s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for s in range(warm, warm + steps):
+        now += 1
+        batch.stage_suffix_device(devs[s])
+        batch.run(now, seed=s, time_attention=(s == warm + steps - 1))
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    attn_ms = float(np.sum(batch.attention_ms()))
+    # end to end: H2D of the step's tokens, D2H of each sequence's next token
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for s in range(warm + steps, warm + 2 * steps):
+        now += 1
+        batch.stage_suffix_host(host[s])
+        batch.run(now, seed=s)
+        batch.model_result()
+    e1.record()
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1)
+    hits, status, _ = batch.results()
+    assert (status == 0).all()
+    mx, _ = reduce_over_ranks([ms, ms_e2e, attn_ms], dev)
+    ms, ms_e2e, attn_ms = mx
+    tokens = batch.total_q * steps * world
+    step_ms = ms / steps
+    dense = batch.dense_flops()
+    attn = batch.attention_flops() * LLAMA3_8B.n_layers
+    out = {
+        "workload": "configs[2]: Llama-3-8B-shaped bf16 continuation prefill over 8K-32K cached prefix, "
+                    "random-init weights (8 requests, prefixes 8K..32K, 1024 tool-output tokens each)",
+        "tokens_per_s": tokens / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": step_ms,
+        "e2e_tokens_per_s": tokens / (ms_e2e * 1e-3),
+        "suffix_tokens_per_step_per_gpu": batch.total_q, "prefix_tokens_per_step_per_gpu": int(sum(batch.prefix_lens)),
+        "dense_tflop_per_step": dense / 1e12, "attention_tflop_per_step": attn / 1e12,
+        "attention_ms_per_step": attn_ms, "attention_share": attn_ms / step_ms,
+        "attention_tflops": attn / (attn_ms * 1e-3) / 1e12,
+        "rest_tflops": dense / ((step_ms - attn_ms) * 1e-3) / 1e12,
+        "rest": "cuBLAS bf16 GEMMs (QKV/O/gate-up/down/LM head) + our RMSNorm/RoPE/SwiGLU/pool kernels",
+        "first_tokens_sample": batch.model_result()[:4].tolist(),
+    }
+    del batch, eng, model
+    torch.cuda.empty_cache()
+    return out
 
 
 TRACE = dict(n_requests=60, seed=1, capacity_blocks=8192, workload="default")

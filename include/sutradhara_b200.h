@@ -285,6 +285,35 @@ int sb_batch_copy_output(sb_batch* batch, int64_t first_row, int64_t n_rows, voi
 int sb_batch_info(const sb_batch* batch, int64_t* total_q, int64_t* total_blocks,
                   int64_t* prompt_tokens, double* attention_flops, void** out);
 
+/* ---- dense layers around the attention (csrc/model.cu) ----------------
+ * A Llama-3-shaped decoder with seeded random-init bf16 weights (BASELINE
+ * configs[2]); the reference charges this compute as a cost
+ * (CostModel::chunk_ms, engine.cpp:35-39).  d_model = 128 * n_q_heads. */
+typedef struct sb_model sb_model;
+int sb_model_create(int32_t n_layers, int32_t d_model, int32_t n_q_heads, int32_t n_kv_heads,
+                    int32_t d_ff, int64_t vocab, float rope_theta, uint64_t seed, int32_t device,
+                    sb_model** out);
+void sb_model_destroy(sb_model* model);
+void sb_model_shape(const sb_model* model, int32_t* n_layers, int32_t* n_q_heads,
+                    int32_t* n_kv_heads);
+void sb_model_vocab(const sb_model* model, int64_t* vocab);
+/* Device pointer + element count of a weight (bf16, nn.Linear [out, in]
+ * layout).  layer >= 0: which = 0 Wqkv [(Hq+2Hkv)*128, d] (q, k, v rows),
+ * 1 Wo [d, d], 2 Wgate_up [2*d_ff, d] (gate rows then up rows),
+ * 3 Wdown [d, d_ff], 4 attention RMSNorm [d], 5 MLP RMSNorm [d];
+ * layer < 0: 0 embedding [vocab, d], 1 LM head [vocab, d], 2 final norm [d]. */
+int sb_model_weight(sb_model* model, int32_t layer, int32_t which, void** ptr, int64_t* n_elems);
+/* Attach a model to a batch: sb_batch_run then embeds the suffix tokens
+ * (token id mod vocab), runs every layer (RMSNorm, QKV, RoPE at the token's
+ * absolute position, KV append into the pages, continuation attention, O
+ * projection, SwiGLU MLP) and the LM head on each sequence's last token.
+ * NULL detaches (attention-path mode with stand-in projections). */
+int sb_batch_set_model(sb_batch* batch, sb_model* model);
+/* Greedy next token per sequence (int32 [n]) and/or fp32 logits [n, vocab]. */
+int sb_batch_model_result(sb_batch* batch, int32_t* next_tokens, float* logits, void* stream);
+/* Dense-layer FLOPs of one run (2 * tokens * weights of all layers). */
+int sb_batch_dense_flops(const sb_batch* batch, double* flops);
+
 /* ---- agentic trace replay on the B200 pool (FTR / hit rate) ---------- */
 /* Generates the reference's synthetic agent trace (trace_gen.cpp:96-193;
  * workload "default" | "tool_heavy" | "iteration_heavy", gen[8] overrides as

@@ -91,6 +91,15 @@ SIGNATURES = {
     "sb_replay_generated": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), C.c_int32, C.c_uint64, C.c_int32, C.c_int64,
                                       C.c_int64, C.POINTER(C.c_double), C.c_int32, I64P, I64P, I64P, I64P, U64P]),
     "sb_kv_append": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, VP]),
+    "sb_model_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_float,
+                                  C.c_uint64, C.c_int32, C.POINTER(VP)]),
+    "sb_model_destroy": (None, [VP]),
+    "sb_model_shape": (None, [VP, I32P, I32P, I32P]),
+    "sb_model_vocab": (None, [VP, I64P]),
+    "sb_model_weight": (C.c_int, [VP, C.c_int32, C.c_int32, C.POINTER(VP), I64P]),
+    "sb_batch_set_model": (C.c_int, [VP, VP]),
+    "sb_batch_model_result": (C.c_int, [VP, I32P, C.POINTER(C.c_float), VP]),
+    "sb_batch_dense_flops": (C.c_int, [VP, C.POINTER(C.c_double)]),
 }
 
 

@@ -36,6 +36,24 @@ __global__ void k_scatter_suffix(const uint64_t* __restrict__ suffix, const int6
   }
 }
 
+struct ModelWorkspace;
+ModelWorkspace* model_workspace_create(sb_model* m, const std::vector<int64_t>& prefix_len,
+                                       const std::vector<int64_t>& suffix_len);
+void model_workspace_destroy(ModelWorkspace* w);
+void model_embed(sb_model* m, ModelWorkspace* w, const uint64_t* d_suffix, cudaStream_t st);
+void model_layer_pre(sb_model* m, ModelWorkspace* w, int l, void* k_pool, void* v_pool, const int32_t* q_off,
+                     const int32_t* kv_len, const int32_t* table, int32_t n_seqs, int32_t max_blocks,
+                     cudaStream_t st);
+void model_layer_post(sb_model* m, ModelWorkspace* w, int l, cudaStream_t st);
+void model_head(sb_model* m, ModelWorkspace* w, cudaStream_t st);
+double model_flops(const sb_model* m, int64_t rows);
+struct ModelIO {  // the few workspace buffers the engine touches (model.cu)
+  __nv_bfloat16 *q, *a;
+  float* logits;
+  int32_t* next_tok;
+};
+ModelIO model_io(ModelWorkspace* w);
+
 template <class T>
 static T* dmalloc(size_t n) {
   T* p = nullptr;
@@ -94,8 +112,11 @@ struct sb_batch {
   __nv_bfloat16 *q = nullptr, *k_new = nullptr, *v_new = nullptr, *out = nullptr;
   std::vector<cudaEvent_t> ev0, ev1;
   double attn_flops = 0;
+  sb_model* model = nullptr;  // dense layers around the attention (optional)
+  ModelWorkspace* mw = nullptr;
   ~sb_batch() {
     cudaSetDevice(eng->device);
+    model_workspace_destroy(mw);
     void* ptrs[] = {tokens, seq_off, blk_off, tag_off, tags, hashes, ids, status, table, q_off, kv_len, work,
                     hits, suffix_off, slot_off, suffix, q, k_new, v_new, out};
     for (void* p : ptrs)
@@ -315,6 +336,28 @@ int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention
     n_launch += 1;
     const float scale = 1.f / std::sqrt(static_cast<float>(e->hd));
     const int64_t nq = b->total_q * e->hq * e->hd, nkv = b->total_q * e->hkv * e->hd;
+    if (b->model) {  // the real Llama-shaped layers (model.cu) around the attention
+      const ModelIO io = model_io(b->mw);
+      model_embed(b->model, b->mw, b->suffix, st);
+      n_launch += 1;
+      for (int l = 0; l < e->n_layers; ++l) {
+        model_layer_pre(b->model, b->mw, l, e->k_pools[l], e->v_pools[l], b->q_off, b->kv_len, b->table, b->n,
+                        b->max_blocks, st);
+        if (time_attention) SB_CUDA(cudaEventRecord(b->ev0[l], st));
+        chk(sb_continuation_attention(io.q, e->k_pools[l], e->v_pools[l], io.a, b->q_off, b->kv_len, b->table, b->n,
+                                      b->max_blocks, b->max_q, static_cast<int32_t>(b->total_q), e->hq, e->hkv, e->hd,
+                                      16, e->cap, scale, b->work, b->n_work, stream));
+        if (time_attention) SB_CUDA(cudaEventRecord(b->ev1[l], st));
+        model_layer_post(b->model, b->mw, l, st);
+        n_launch += 5;  // rmsnorm, rope+scatter, attention, rmsnorm, swiglu (+ cuBLAS GEMMs)
+      }
+      model_head(b->model, b->mw, st);
+      n_launch += 2;
+      chk(sb_kv_release_batch(e->cache, b->ids, b->total_blocks, nullptr, stream));
+      n_launch += 3;
+      if (launches) *launches = n_launch;
+      return int(SB_OK);
+    }
     for (int l = 0; l < e->n_layers; ++l) {
       const uint64_t base = (seed * 1000003ull + static_cast<uint64_t>(l)) * 3ull;
       chk(sb_fill_random_bf16(b->q, nq, base, 1.f, stream));  // projection outputs (random-init stand-in)
@@ -362,10 +405,50 @@ int sb_batch_copy_output(sb_batch* b, int64_t first_row, int64_t n_rows, void* h
   return guard([&] {
     if (first_row < 0 || first_row + n_rows > b->total_q) throw Error(SB_ERR_INVALID, "row range");
     const size_t row = static_cast<size_t>(b->eng->hq) * b->eng->hd;
-    SB_CUDA(cudaMemcpyAsync(host_dst, b->out + first_row * row, n_rows * row * sizeof(__nv_bfloat16),
+    const __nv_bfloat16* src = b->model ? model_io(b->mw).a : b->out;
+    SB_CUDA(cudaMemcpyAsync(host_dst, src + first_row * row, n_rows * row * sizeof(__nv_bfloat16),
                             cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)));
     return int(SB_OK);
   });
+}
+
+int sb_batch_set_model(sb_batch* b, sb_model* m) {
+  return guard([&] {
+    SB_CUDA(cudaSetDevice(b->eng->device));
+    model_workspace_destroy(b->mw);
+    b->mw = nullptr;
+    b->model = nullptr;
+    if (!m) return int(SB_OK);
+    int32_t nl = 0, hq = 0, hkv = 0;
+    sb_model_shape(m, &nl, &hq, &hkv);
+    if (nl != b->eng->n_layers || hq != b->eng->hq || hkv != b->eng->hkv)
+      throw Error(SB_ERR_INVALID, "model shape differs from the engine's KV shape");
+    b->mw = model_workspace_create(m, b->prefix_len, b->suffix_len);
+    b->model = m;
+    return int(SB_OK);
+  });
+}
+
+int sb_batch_model_result(sb_batch* b, int32_t* next_tokens, float* logits, void* stream) {
+  return guard([&] {
+    if (!b->model) throw Error(SB_ERR_INVALID, "no model attached");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const ModelIO io = model_io(b->mw);
+    if (next_tokens)
+      SB_CUDA(cudaMemcpyAsync(next_tokens, io.next_tok, sizeof(int32_t) * b->n, cudaMemcpyDeviceToHost, st));
+    if (logits) {
+      int64_t vocab = 0;
+      sb_model_vocab(b->model, &vocab);
+      SB_CUDA(cudaMemcpyAsync(logits, io.logits, sizeof(float) * b->n * vocab, cudaMemcpyDeviceToHost, st));
+    }
+    SB_CUDA(cudaStreamSynchronize(st));
+    return int(SB_OK);
+  });
+}
+
+int sb_batch_dense_flops(const sb_batch* b, double* flops) {
+  *flops = b->model ? model_flops(b->model, b->total_q) : 0.0;
+  return SB_OK;
 }
 
 int sb_batch_info(const sb_batch* b, int64_t* total_q, int64_t* total_blocks, int64_t* prompt_tokens,

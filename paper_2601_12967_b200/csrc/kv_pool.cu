@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(32 * kHashWarps, 8)
     __syncwarp();
     seq_b[w][lane] = b;
     seq_e[w][lane] = e;
-    seq_p[w][lane] = tokens + b + k;  // lane k of a half warp loads token k of a block
+    seq_p[w][lane] = tokens + b;
     const int nb_max = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(nblk)));
     // blocks every sequence of the group holds in full (empty lanes hold none)
     const int nb_full = static_cast<int>(
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(32 * kHashWarps, 8)
       if (j < nb_full) {
 #pragma unroll
         for (int r = 0; r < 16; ++r)
-          v[r] = __ldg(reinterpret_cast<const unsigned long long*>(seq_p[w][2 * r + half] + 16 * j));
+          v[r] = __ldg(reinterpret_cast<const unsigned long long*>(seq_p[w][2 * r + half] + 16 * j + k));
       } else {
 #pragma unroll
         for (int r = 0; r < 16; ++r) {

@@ -51,6 +51,54 @@ class ModelShape:
 _DEBUG = os.environ.get("SB_DEBUG", "0") == "1"
 
 LLAMA3_8B = ModelShape(32, 32, 8, 128)
+
+
+@dataclass
+class DenseShape:
+    """Dense layers of a Llama-3-style decoder around the paged attention."""
+    n_layers: int = 32
+    d_model: int = 4096
+    n_q_heads: int = 32
+    n_kv_heads: int = 8
+    d_ff: int = 14336
+    vocab: int = 128256
+    rope_theta: float = 500000.0
+
+
+LLAMA3_8B_DENSE = DenseShape()
+
+
+class DenseModel:
+    """Binding of ``sb_model`` (csrc/model.cu): seeded random-init bf16
+    weights of a Llama-3-shaped decoder; attach it to a ContinuationBatch to
+    run the real layers (QKV/O/MLP GEMMs on cuBLAS, RMSNorm/RoPE/SwiGLU and
+    the paged attention in our kernels) instead of the stand-in projections."""
+
+    def __init__(self, shape: DenseShape, seed: int = 0, device: int = 0):
+        self.shape = shape
+        self._L = _lib.lib()
+        h = C.c_void_p()
+        _lib.check(self._L.sb_model_create(shape.n_layers, shape.d_model, shape.n_q_heads, shape.n_kv_heads,
+                                           shape.d_ff, shape.vocab, shape.rope_theta, seed, device, C.byref(h)),
+                   "model")
+        self._h = h
+
+    def weight(self, layer: int, which: int):
+        """(device pointer, element count) of a bf16 weight (see sb_model_weight)."""
+        ptr, n = C.c_void_p(), C.c_int64()
+        _lib.check(self._L.sb_model_weight(self._h, layer, which, C.byref(ptr), C.byref(n)), "weight")
+        return ptr.value, n.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.sb_model_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 TOY_2L_256 = ModelShape(2, 2, 1, 128)  # configs[0]: 2 layers, d_model = 2 x 128
 
 
@@ -210,3 +258,22 @@ class ContinuationBatch:
 
     def attention_flops(self) -> float:
         return self._flops
+
+    def set_model(self, model: Optional["DenseModel"]):
+        """Run the real dense layers around the attention (None: stand-ins)."""
+        self._model = model  # keep the weights alive while attached
+        _lib.check(self._L.sb_batch_set_model(self._h, model._h if model is not None else None), "set_model")
+
+    def model_result(self, logits: bool = False):
+        """Greedy next token per sequence (and fp32 last-token logits)."""
+        nxt = np.zeros(self.n, np.int32)
+        lg = np.zeros((self.n, self._model.shape.vocab), np.float32) if logits else None
+        _lib.check(self._L.sb_batch_model_result(self._h, nxt.ctypes.data_as(_lib.I32P),
+                                                 lg.ctypes.data_as(C.POINTER(C.c_float)) if logits else None,
+                                                 self._stream()), "model_result")
+        return (nxt, lg) if logits else nxt
+
+    def dense_flops(self) -> float:
+        f = C.c_double()
+        self._L.sb_batch_dense_flops(self._h, C.byref(f))
+        return f.value

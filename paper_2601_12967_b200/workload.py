@@ -119,3 +119,21 @@ def fresh_suffix_tokens(req: ContinuationRequest, step: int) -> np.ndarray:
     step inserts and evicts real blocks."""
     secs = [Section(s.tag, s.length, s.key ^ (0x9E37 * (step + 1)), s.src_iter) for s in req.suffix]
     return build_prompt(secs)[0]
+
+
+def long_prefix_continuation_batch(n_requests: int = 8, prefix_min: int = 8192, prefix_max: int = 32768,
+                                   suffix_len: int = 1024, sys_len: int = 2048,
+                                   seed: int = 1) -> List[ContinuationRequest]:
+    """BASELINE.json configs[2]: continuation prefill of `suffix_len` tool-output
+    tokens over 8K-32K-token cached prefixes (shared system prompt + history),
+    prefix lengths evenly spread and rounded to the 16-token block."""
+    reqs = []
+    for r in range(n_requests):
+        frac = r / max(1, n_requests - 1)
+        plen = 16 * int(round((prefix_min + frac * (prefix_max - prefix_min)) / 16))
+        prefix = [Section(SYS, sys_len, SYSTEM_KEY), Section(HIST, plen - sys_len, 5000 * seed + r)]
+        suffix = [Section(TOOL, suffix_len, 6000 * seed + r, 0)]
+        req = ContinuationRequest(r, 2, 1, prefix, suffix)
+        req.prefix_tokens, req.prefix_tags = build_prompt(prefix)
+        reqs.append(req)
+    return reqs

@@ -1,0 +1,137 @@
+"""GPU numerics of the dense layers around the continuation attention
+(csrc/model.cu, attached to a ContinuationBatch): the engine's continuation
+step — embed, per layer RMSNorm / QKV / RoPE + KV scatter into the pool pages
+/ paged continuation attention / O projection / SwiGLU MLP, final norm + LM
+head on each sequence's last token — against a torch fp32 restatement that
+uses the same weights (read back from the device) and the same cached prefix
+pages, rounding activations to bf16 where the device path stores them.
+
+Tolerance (bf16 activations, fp32 accumulation): last-token logits within
+2e-2 of the reference's max |logit|; greedy tokens equal wherever the
+reference's top-2 gap exceeds that tolerance."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+BS = 16
+
+
+def _bf(x):
+    import torch
+
+    return x.to(torch.bfloat16).float()
+
+
+class _DevBuf:
+    """A raw device pointer exposed through __cuda_array_interface__."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i2", "data": (ptr, False), "version": 3}
+
+
+def _dev_tensor(ptr, n, shape):
+    """fp32 copy of a bf16 device buffer owned by the library."""
+    import torch
+
+    t = torch.as_tensor(_DevBuf(ptr, n), device="cuda").view(torch.bfloat16)
+    return t.float().reshape(shape).clone()
+
+
+def _rope(x, pos, theta):
+    """x [T, H, 128] fp32, rotate-half RoPE at absolute positions pos [T]."""
+    import torch
+
+    f = torch.arange(64, dtype=torch.float64, device=x.device)
+    inv = theta ** (-2.0 * f / 128.0)
+    ang = pos.double()[:, None] * inv[None, :]
+    c, s = torch.cos(ang).float()[:, None, :], torch.sin(ang).float()[:, None, :]
+    x1, x2 = x[..., :64], x[..., 64:]
+    return torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], -1)
+
+
+def _rms(x, w, eps=1e-5):
+    return x * (x.pow(2).mean(-1, keepdim=True) + eps).rsqrt() * w
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prefix_lens,suffix_lens", [([48, 96, 16], [37, 70, 1]), ([256], [130])])
+def test_dense_step_matches_torch_reference(prefix_lens, suffix_lens):
+    import torch
+    import torch.nn.functional as F
+    from paper_2601_12967_b200.engine import ContinuationEngine, DenseModel, DenseShape, ModelShape
+
+    hq, hkv, d, dff, vocab, nl = 4, 2, 512, 1024, 1000, 2
+    ds = DenseShape(n_layers=nl, d_model=d, n_q_heads=hq, n_kv_heads=hkv, d_ff=dff, vocab=vocab, rope_theta=10000.0)
+    cap = sum((p + s + 15) // 16 for p, s in zip(prefix_lens, suffix_lens)) + 4
+    eng = ContinuationEngine(ModelShape(nl, hq, hkv, 128), cap, policy=1, seed=7)
+    model = DenseModel(ds, seed=3)
+    handles = []
+    for i, p in enumerate(prefix_lens):
+        toks = O.materialize(0, p, 100 + i)
+        handles.append(eng.submit_partial_prefill(toks, [(0, p, 3)], now=0))
+    batch = eng.make_batch(handles, suffix_lens)
+    batch.set_model(model)
+    rng = np.random.default_rng(1)
+    suffix = rng.integers(0, 2**62, sum(suffix_lens), dtype=np.int64)
+    batch.stage_suffix_device(torch.from_numpy(suffix).cuda())
+    batch.run(now=5, seed=0)
+    nxt, logits = batch.model_result(logits=True)
+    hits, status, ids = batch.results()
+    assert (status == 0).all()
+
+    # ---- torch restatement
+    W = {}
+    for l in range(nl):
+        for which, shp in ((0, ((hq + 2 * hkv) * 128, d)), (1, (d, d)), (2, (2 * dff, d)), (3, (d, dff)), (4, (d,)),
+                           (5, (d,))):
+            ptr, n = model.weight(l, which)
+            W[l, which] = _dev_tensor(ptr, n, shp)
+    emb = _dev_tensor(*model.weight(-1, 0), (vocab, d))
+    lm = _dev_tensor(*model.weight(-1, 1), (vocab, d))
+    fnorm = _dev_tensor(*model.weight(-1, 2), (d,))
+    pools = [(_dev_tensor(eng.k_pool(l), cap * hkv * 16 * 128, (cap, hkv, 16, 128)),
+              _dev_tensor(eng.v_pool(l), cap * hkv * 16 * 128, (cap, hkv, 16, 128))) for l in range(nl)]
+    blk = np.cumsum([0] + [(p + s + 15) // 16 for p, s in zip(prefix_lens, suffix_lens)])
+    ref_logits = []
+    off = 0
+    for si, (p, s) in enumerate(zip(prefix_lens, suffix_lens)):
+        tok = torch.from_numpy(suffix[off:off + s].view(np.uint64) % np.uint64(vocab)).long().cuda()
+        off += s
+        x = emb[tok]  # bf16 values already
+        pos = torch.arange(p, p + s, device="cuda")
+        pages = torch.from_numpy(ids[blk[si]:blk[si] + p // 16]).long().cuda()
+        for l in range(nl):
+            xn = _bf(_rms(x, W[l, 4]))
+            qkv = _bf(xn @ W[l, 0].t()).reshape(s, hq + 2 * hkv, 128)
+            q = _bf(_rope(qkv[:, :hq], pos, ds.rope_theta))
+            k = _bf(_rope(qkv[:, hq:hq + hkv], pos, ds.rope_theta))
+            v = qkv[:, hq + hkv:]
+            kp, vp = pools[l]
+            kpre = kp[pages].permute(1, 0, 2, 3).reshape(hkv, -1, 128)  # [hkv, p, 128]
+            vpre = vp[pages].permute(1, 0, 2, 3).reshape(hkv, -1, 128)
+            K = torch.cat([kpre, k.permute(1, 0, 2)], 1).repeat_interleave(hq // hkv, 0)
+            V = torch.cat([vpre, v.permute(1, 0, 2)], 1).repeat_interleave(hq // hkv, 0)
+            sc = q.permute(1, 0, 2) @ K.transpose(1, 2) / math.sqrt(128)
+            mask = torch.arange(p + s, device="cuda")[None, :] > (p + torch.arange(s, device="cuda"))[:, None]
+            a = _bf((torch.softmax(sc.masked_fill(mask, float("-inf")), -1) @ V).permute(1, 0, 2).reshape(s, d))
+            x = _bf(x + a @ W[l, 1].t())
+            xn = _bf(_rms(x, W[l, 5]))
+            gu = _bf(xn @ W[l, 2].t())
+            h = _bf(F.silu(gu[:, :dff]) * gu[:, dff:])
+            x = _bf(x + h @ W[l, 3].t())
+        xl = _bf(_rms(x[-1:], fnorm))
+        ref_logits.append((xl @ lm.t())[0])
+    ref = torch.stack(ref_logits).cpu()
+    got = torch.from_numpy(logits)
+    tol = 2e-2 * ref.abs().max().item()
+    err = (got - ref).abs().max().item()
+    print(f"dense step: max |logit err| {err:.3e} vs tol {tol:.3e} (max |logit| {ref.abs().max().item():.3f})")
+    assert ref.abs().max().item() > 0
+    assert err <= tol, (err, tol)
+    top2 = ref.topk(2, -1).values
+    for i in range(len(prefix_lens)):
+        if (top2[i, 0] - top2[i, 1]).item() > 2 * tol:
+            assert nxt[i] == int(ref[i].argmax()), i
