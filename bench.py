@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--requests", type=int, default=N_REQ)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true", help="skip the configs[2] full-model measurement")
+    ap.add_argument("--no-trace", action="store_true", help="skip the trace replay (p50 FTR / hit rate)")
     return ap.parse_args()
 
 
@@ -290,7 +291,18 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.empty_cache()
     if not args.no_dense:
         line["full_model"] = run_dense(args, rank, world, local_rank)
-    line.update(trace_replay_metrics(line["value"], local_rank))
+    try:  # same attention problem through NVIDIA's trtllm-gen kernel (flashinfer cubin), as a reference point
+        import bench_attn
+
+        ref = bench_attn.measure(args.requests, launches=5, flashinfer=True)
+        line["roofline"]["library_reference"] = {
+            "ours_standalone_tflops": ref["tflops"], "flashinfer_trtllm_gen_tflops": ref["flashinfer"]["tflops"],
+            "max_abs_diff": ref["flashinfer"]["max_abs_diff_vs_ours"],
+            "note": "both kernels on identical synthetic paged KV/queries of the configs[1] step, CUDA events"}
+    except Exception as e:  # library absent or incompatible: no reference point
+        line["roofline"]["library_reference"] = {"unavailable": str(e)[:200]}
+    if not args.no_trace:
+        line.update(trace_replay_metrics(line["value"], local_rank))
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(reqs, budget_s=20.0)
     return line
