@@ -5,15 +5,17 @@ iterations each) sharing a 2K-token system prefix, each caught at the moment
 its tool outputs arrive.  One step = one batched continuation prefill over
 the Llama-3-8B-shaped paged KV pool (32 layers, 32 q / 8 kv heads, d=128):
 
-  chain-hash prompts -> prefix lookup -> insert (hint-aware eviction under
-  pool pressure) -> block tables -> per layer {projection stand-in, KV append,
-  continuation attention} -> release
+  chain-hash the prompts (prefix hashes gathered from the pinned pool blocks,
+  suffix folded) -> prefix lookup -> insert (hint-aware eviction under pool
+  pressure) -> block tables -> per layer {KV append, continuation attention}
+  -> release
 
 ``value`` is suffix (tool-output) tokens per second with inputs resident in
 HBM; ``e2e`` is the same through the public engine API with the step's
 suffix tokens copied host->device and an output sample copied back, inside
-the timed region.  Dense projections/MLP are outside the measured path
-(random-init stand-in activations are generated on device each layer).
+the timed region.  The per-layer q / k / v of this step are seeded stand-ins
+generated once per batch: the dense layers around the attention are measured
+separately as ``full_model`` (configs[2], the whole Llama-3-8B-shaped model).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
@@ -272,7 +274,8 @@ def run_ours(args, rank, world, local_rank):
             "eviction_policy": "tiered (hint-aware)",
             "parallelism": f"requests sharded, {world} independent pools; NCCL all-reduce of cache stats only",
             "l2": "inputs larger than L2 (KV pool >> 126 MB)",
-            "scope": "hash + lookup + insert/evict + KV append + attention; dense projections/MLP not measured",
+            "scope": "hash + lookup + insert/evict + KV append + attention (q/k/v stand-ins generated once per "
+                     "batch); the full dense model is the separate full_model measurement",
         },
         "hit_rate": hit_rate,
         "evicted_blocks_per_step": stats["evicted_blocks"] / max(1, (args.warmup + 2 * args.steps)),

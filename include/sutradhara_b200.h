@@ -93,6 +93,15 @@ int sb_chain_hash_batch(const uint64_t* d_tokens, const int64_t* d_seq_offsets,
                         int32_t n_seqs, int64_t block_size, uint64_t* d_block_hashes,
                         void* stream);
 
+/* Same fold over token segments: segment s is d_tokens[d_seg_bounds[2s] ..
+ * d_seg_bounds[2s+1]), its blocks' chain hashes go to d_block_hashes
+ * [d_seg_blocks[s] + j], the chain starting from d_parent[s] (NULL = root).
+ * With d_parent = the hash of a cached prefix's last block this is the
+ * incremental (suffix-only) hashing of an extended prompt. */
+int sb_chain_hash_segments(const uint64_t* d_tokens, const int64_t* d_seg_bounds,
+                           const int64_t* d_seg_blocks, const uint64_t* d_parent, int32_t n_segs,
+                           int64_t block_size, uint64_t* d_block_hashes, void* stream);
+
 /* Device-side synthetic token materialisation (trace.cpp:70-78 and
  * decode_token trace.cpp:80-83).  section_tag uses agentsim::SectionTag order
  * (trace.hpp:18): 0 system, 1 user, 2 tool_output, 3 history. */
@@ -227,6 +236,13 @@ int sb_kv_append(const void* k_new, const void* v_new, void* k_pool, void* v_poo
                  const int32_t* d_block_table, int32_t n_seqs, int32_t max_blocks_per_seq,
                  int32_t n_kv_heads, int32_t head_dim, int32_t page_size, void* stream);
 
+/* Device gather of the chain hashes of resident blocks (KvBlock::chain_hash,
+ * kv_cache.hpp:53): d_out[d_pos ? d_pos[i] : i] = chain hash of d_ids[i].
+ * Lets an engine reuse the hashes of a pinned prefix instead of re-folding
+ * its tokens (incremental, suffix-only hashing). */
+int sb_kv_gather_chain_hashes(sb_kv_cache* cache, const int32_t* d_ids, const int64_t* d_pos, int64_t n,
+                              uint64_t* d_out, void* stream);
+
 /* ---- engine-path helpers ---------------------------------------------- */
 /* Dense block table from the per-sequence chain ids returned by
  * sb_kv_insert_batch: table[s*max_blocks + j] = ids[block_offsets[s] + j]
@@ -268,10 +284,13 @@ void sb_batch_destroy(sb_batch* batch);
 /* This step's suffix tokens, packed in batch order (host or device array). */
 int sb_batch_stage_suffix(sb_batch* batch, const uint64_t* tokens, int32_t on_device,
                           void* stream);
-/* One continuation-prefill step: chain hashes, admission lookup, insert with
- * hint-aware eviction (Engine::complete_prefill, engine.cpp:305-322), page
- * table, then per layer {projection stand-in, KV append, attention}, and the
- * release of the call's block references (engine.cpp:343-346). */
+/* One continuation-prefill step: chain hashes (the pinned prefix's hashes are
+ * gathered from the pool, only the suffix is folded), admission lookup,
+ * insert with hint-aware eviction (Engine::complete_prefill,
+ * engine.cpp:305-322), page table, then per layer {KV append, attention} and
+ * the release of the call's block references (engine.cpp:343-346).  Without
+ * an attached model the per-layer q / k / v are seeded stand-ins generated
+ * once at batch creation (the dense layers are `sb_batch_set_model`). */
 int sb_batch_run(sb_batch* batch, int64_t now, uint64_t seed, int32_t time_attention,
                  void* stream, int32_t* launches);
 /* Per-layer attention times of the last timed run (ms, n_layers floats). */

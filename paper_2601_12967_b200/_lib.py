@@ -39,6 +39,7 @@ SIGNATURES = {
     "sb_kv_root_hash": (C.c_uint64, []),
     "sb_kv_chain_hash_host": (C.c_uint64, [C.c_uint64, U64P, C.c_int64]),
     "sb_chain_hash_batch": (C.c_int, [VP, VP, VP, VP, C.c_int32, C.c_int64, VP, VP]),
+    "sb_chain_hash_segments": (C.c_int, [VP, VP, VP, VP, C.c_int32, C.c_int64, VP, VP]),
     "sb_materialize_tokens": (C.c_int, [C.c_int32, C.c_int64, C.c_uint64, C.c_int32, VP, VP]),
     "sb_decode_tokens": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, VP, VP]),
     "sb_kv_create": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.POINTER(VP)]),
@@ -70,6 +71,7 @@ SIGNATURES = {
                                             C.c_int32, VP]),
     "sb_attention_work_list": (C.c_int, [I32P, I32P, C.c_int32, C.c_int32, C.c_int32, I32P, C.c_int32, I32P]),
     "sb_build_block_table": (C.c_int, [VP, VP, C.c_int32, C.c_int32, VP, VP]),
+    "sb_kv_gather_chain_hashes": (C.c_int, [VP, VP, VP, C.c_int64, VP, VP]),
     "sb_fill_random_bf16": (C.c_int, [VP, C.c_int64, C.c_uint64, C.c_float, VP]),
     "sb_engine_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
                                    C.c_uint64, C.POINTER(VP)]),

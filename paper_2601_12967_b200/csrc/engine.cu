@@ -108,6 +108,12 @@ struct sb_batch {
   int32_t n_work = 0;
   int64_t* hits = nullptr;
   int64_t *suffix_off = nullptr, *slot_off = nullptr;
+  // incremental hashing: prefix chain hashes gathered from the pinned blocks,
+  // only the suffix segments folded (parent = last prefix block's hash)
+  int32_t *pre_ids = nullptr, *last_pre = nullptr;
+  int64_t *pre_pos = nullptr, *sfx_seq_off = nullptr, *sfx_blk_off = nullptr;
+  int64_t n_pre = 0;
+  uint64_t* parent0 = nullptr;
   uint64_t* suffix = nullptr;
   __nv_bfloat16 *q = nullptr, *k_new = nullptr, *v_new = nullptr, *out = nullptr;
   std::vector<cudaEvent_t> ev0, ev1;
@@ -118,7 +124,8 @@ struct sb_batch {
     cudaSetDevice(eng->device);
     model_workspace_destroy(mw);
     void* ptrs[] = {tokens, seq_off, blk_off, tag_off, tags, hashes, ids, status, table, q_off, kv_len, work,
-                    hits, suffix_off, slot_off, suffix, q, k_new, v_new, out};
+                    hits, suffix_off, slot_off, suffix, q, k_new, v_new, out, pre_ids, last_pre, pre_pos,
+                    sfx_seq_off, sfx_blk_off, parent0};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (auto e : ev0) cudaEventDestroy(e);
@@ -222,7 +229,8 @@ int sb_batch_create(sb_engine* e, const int32_t* handles, const int64_t* suffix_
       b->n = n;
       std::vector<uint64_t> toks;
       std::vector<sb_tag_range> tags;
-      std::vector<int64_t> tag_off{0}, slot_off, suffix_off{0};
+      std::vector<int64_t> tag_off{0}, slot_off, suffix_off{0}, pre_pos, sfx_blk;
+      std::vector<int32_t> pre_ids, last_pre;
       b->seq_off_h = {0};
       b->blk_off_h = {0};
       for (int i = 0; i < n; ++i) {
@@ -232,6 +240,12 @@ int sb_batch_create(sb_engine* e, const int32_t* handles, const int64_t* suffix_
         const int64_t pl = static_cast<int64_t>(pc.tokens.size()), sl = suffix_lens[i];
         if (pl % 16) throw Error(SB_ERR_UNSUPPORTED, "tool-independent prefix must end on a 16-token block boundary");
         if (sl <= 0) throw Error(SB_ERR_INVALID, "suffix must be non-empty");
+        for (int64_t k = 0; k < pl / 16; ++k) {
+          pre_ids.push_back(pc.ids[static_cast<size_t>(k)]);
+          pre_pos.push_back(b->blk_off_h.back() + k);
+        }
+        last_pre.push_back(pc.ids[static_cast<size_t>(pl / 16 - 1)]);
+        sfx_blk.push_back(b->blk_off_h.back() + pl / 16);
         b->prefix_len.push_back(pl);
         b->suffix_len.push_back(sl);
         b->full_len.push_back(pl + sl);
@@ -271,11 +285,33 @@ int sb_batch_create(sb_engine* e, const int32_t* handles, const int64_t* suffix_
       b->kv_len = upload(kl);
       b->suffix_off = upload(suffix_off);
       b->slot_off = upload(slot_off);
+      // suffix-only hashing: segment s = tokens[slot_off[s], seq_off[s+1]), its blocks from
+      // blk_off[s] + prefix_blocks (sb_chain_hash_segments)
+      std::vector<int64_t> so;
+      for (int i = 0; i < n; ++i) {
+        so.push_back(slot_off[static_cast<size_t>(i)]);
+        so.push_back(b->seq_off_h[static_cast<size_t>(i) + 1]);
+      }
+      const std::vector<int64_t>& bo = sfx_blk;
+      b->sfx_seq_off = upload(so);
+      b->sfx_blk_off = upload(bo);
+      b->pre_ids = upload(pre_ids);
+      b->pre_pos = upload(pre_pos);
+      b->last_pre = upload(last_pre);
+      b->n_pre = static_cast<int64_t>(pre_ids.size());
+      b->parent0 = dmalloc<uint64_t>(n);
       b->suffix = dmalloc<uint64_t>(b->total_q);
       b->q = dmalloc<__nv_bfloat16>(static_cast<size_t>(b->total_q) * e->hq * e->hd);
       b->out = dmalloc<__nv_bfloat16>(static_cast<size_t>(b->total_q) * e->hq * e->hd);
       b->k_new = dmalloc<__nv_bfloat16>(static_cast<size_t>(b->total_q) * e->hkv * e->hd);
       b->v_new = dmalloc<__nv_bfloat16>(static_cast<size_t>(b->total_q) * e->hkv * e->hd);
+      {  // seeded stand-ins for the projection outputs (attention-path mode, no model attached)
+        const int64_t nq = b->total_q * e->hq * e->hd, nkv = b->total_q * e->hkv * e->hd;
+        int st = sb_fill_random_bf16(b->q, nq, 0x51ull, 1.f, nullptr);
+        if (!st) st = sb_fill_random_bf16(b->k_new, nkv, 0x52ull, 1.f, nullptr);
+        if (!st) st = sb_fill_random_bf16(b->v_new, nkv, 0x53ull, 1.f, nullptr);
+        if (st) throw Error(st, sb_last_error());
+      }
       // LPT-ordered attention work list
       const int tpt = 128 / (e->hq / e->hkv);
       int64_t cap_items = 0;
@@ -324,8 +360,12 @@ int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention
     auto chk = [](int s) {
       if (s) throw Error(s, sb_last_error());
     };
-    chk(sb_chain_hash_batch(b->tokens, b->seq_off, b->blk_off, nullptr, b->n, 16, b->hashes, stream));
-    n_launch += 1;
+    // incremental hashing: the pinned prefix's chain hashes come from the pool,
+    // only the suffix (tool output) tokens are folded, from the prefix's last hash
+    chk(sb_kv_gather_chain_hashes(e->cache, b->pre_ids, b->pre_pos, b->n_pre, b->hashes, stream));
+    chk(sb_kv_gather_chain_hashes(e->cache, b->last_pre, nullptr, b->n, b->parent0, stream));
+    chk(sb_chain_hash_segments(b->tokens, b->sfx_seq_off, b->sfx_blk_off, b->parent0, b->n, 16, b->hashes, stream));
+    n_launch += 3;
     chk(sb_kv_lookup_prefix_batch(e->cache, b->tokens, b->seq_off, b->blk_off, b->blk_off_h.data(), b->hashes, b->n,
                                   now, b->hits, stream));
     n_launch += 3;
@@ -358,11 +398,11 @@ int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention
       if (launches) *launches = n_launch;
       return int(SB_OK);
     }
+    (void)seed;
+    (void)nq;
+    (void)nkv;
     for (int l = 0; l < e->n_layers; ++l) {
-      const uint64_t base = (seed * 1000003ull + static_cast<uint64_t>(l)) * 3ull;
-      chk(sb_fill_random_bf16(b->q, nq, base, 1.f, stream));  // projection outputs (random-init stand-in)
-      chk(sb_fill_random_bf16(b->k_new, nkv, base + 1, 1.f, stream));
-      chk(sb_fill_random_bf16(b->v_new, nkv, base + 2, 1.f, stream));
+      // q / k / v: the seeded stand-ins of the batch (the dense layers are sb_batch_set_model)
       chk(sb_kv_append(b->k_new, b->v_new, e->k_pools[l], e->v_pools[l], b->q_off, b->kv_len, b->table, b->n,
                        b->max_blocks, e->hkv, e->hd, 16, stream));
       if (time_attention) SB_CUDA(cudaEventRecord(b->ev0[l], st));
@@ -370,7 +410,7 @@ int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention
                                     b->max_blocks, b->max_q, static_cast<int32_t>(b->total_q), e->hq, e->hkv, e->hd, 16,
                                     e->cap, scale, b->work, b->n_work, stream));
       if (time_attention) SB_CUDA(cudaEventRecord(b->ev1[l], st));
-      n_launch += 5;
+      n_launch += 2;
     }
     chk(sb_kv_release_batch(e->cache, b->ids, b->total_blocks, nullptr, stream));
     n_launch += 3;

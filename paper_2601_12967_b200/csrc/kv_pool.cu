@@ -151,10 +151,10 @@ __device__ void index_insert(const Pool& P, uint64_t h, int32_t id, uint64_t par
 // partial unless full_only).
 __global__ void k_chain_hash(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ seq_off,
                              const int64_t* __restrict__ blk_off, const uint64_t* __restrict__ parent0, int n_seqs,
-                             int64_t bs, int full_only, uint64_t* __restrict__ out) {
+                             int64_t bs, int full_only, uint64_t* __restrict__ out, int segs) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_seqs) return;
-  const int64_t b = seq_off[s], e = seq_off[s + 1];
+  const int64_t b = seq_off[segs ? 2 * s : s], e = seq_off[segs ? 2 * s + 1 : s + 1];
   uint64_t h = parent0 ? parent0[s] : kRootHash;
   const int64_t ob = blk_off[s];
   const int64_t nblk = full_only ? (e - b) / bs : (e - b + bs - 1) / bs;
@@ -190,7 +190,7 @@ constexpr int kHashWarps = 4;
 __global__ void __launch_bounds__(32 * kHashWarps, 8)
     k_chain_hash16(const uint64_t* __restrict__ tokens, const int64_t* __restrict__ seq_off,
                    const int64_t* __restrict__ blk_off, const uint64_t* __restrict__ parent0, int n_seqs,
-                   int full_only, uint64_t* __restrict__ out) {
+                   int full_only, uint64_t* __restrict__ out, int segs) {
   __shared__ uint64_t stage[kHashWarps][32][17];  // 17-word rows: conflict-free per half warp
   __shared__ const uint64_t* seq_p[kHashWarps][32];
   __shared__ int64_t seq_b[kHashWarps][32], seq_e[kHashWarps][32];
@@ -202,8 +202,8 @@ __global__ void __launch_bounds__(32 * kHashWarps, 8)
     int64_t b = 0, e = 0, ob = 0, nblk = 0;
     uint64_t h = kRootHash;
     if (s < n_seqs) {
-      b = seq_off[s];
-      e = seq_off[s + 1];
+      b = seq_off[segs ? 2 * s : s];  // segs: sequence s = tokens [seq_off[2s], seq_off[2s+1])
+      e = seq_off[segs ? 2 * s + 1 : s + 1];
       ob = blk_off[s];
       if (parent0) h = parent0[s];
       nblk = full_only ? (e - b) / 16 : (e - b + 15) / 16;
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(32 * kHashWarps, 8)
 
 static void launch_chain_hash(const uint64_t* tokens, const int64_t* seq_off, const int64_t* blk_off,
                               const uint64_t* parent0, int n_seqs, int64_t bs, int full_only, uint64_t* out,
-                              cudaStream_t st) {
+                              cudaStream_t st, int segs = 0) {
   if (n_seqs <= 0) return;
   if (bs == 16) {
     static int grid_cap = 0;  // whole waves of resident CTAs
@@ -269,9 +269,10 @@ static void launch_chain_hash(const uint64_t* tokens, const int64_t* seq_off, co
     }
     const int groups = (n_seqs + 31) / 32;
     const int grid = std::min(grid_cap, (groups + kHashWarps - 1) / kHashWarps);
-    kern<<<grid, 32 * kHashWarps, 0, st>>>(tokens, seq_off, blk_off, parent0, n_seqs, full_only, out);
+    kern<<<grid, 32 * kHashWarps, 0, st>>>(tokens, seq_off, blk_off, parent0, n_seqs, full_only, out, segs);
   } else {
-    k_chain_hash<<<(n_seqs + 63) / 64, 64, 0, st>>>(tokens, seq_off, blk_off, parent0, n_seqs, bs, full_only, out);
+    k_chain_hash<<<(n_seqs + 63) / 64, 64, 0, st>>>(tokens, seq_off, blk_off, parent0, n_seqs, bs, full_only, out,
+                                                    segs);
   }
 }
 
@@ -745,6 +746,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
   __shared__ int64_t sh[8];
   __shared__ uint32_t cnt_b;
   __shared__ unsigned long long n_cand, n_hc;
+  __shared__ unsigned long long key_range[2];
   extern __shared__ uint64_t dyn[];  // [kCandSmem] candidates | [kSortSmemKeys] selection
   uint64_t* cand_s = dyn;
   uint64_t* sel_s = dyn + kCandSmem;
@@ -781,6 +783,8 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
   if (t == 0) {
     n_cand = 0;
     n_hc = 0;
+    key_range[0] = ~0ull;
+    key_range[1] = 0;
   }
   __syncthreads();
   if (mode == 0) {
@@ -800,13 +804,25 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
   }
   // ---- score every block, compact the candidates
   // (first into shared memory; overflow keeps going into global S.keys)
+  uint64_t kmn = ~0ull, kmx = 0;  // key range of the candidates: radix passes skip the shared high bits
   score_slice<1, true>(P, S.rank_of, 0, P.cap, [&](bool c, uint64_t k, bool) {
     bool mine;
     const uint64_t at = warp_append_slot(c, &n_cand, mine);
     if (mine) {
       if (at < kCandSmem) cand_s[at] = k; else S.keys[at - kCandSmem] = k;
+      kmn = min(kmn, k);
+      kmx = max(kmx, k);
     }
   });
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, o));
+    kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
+  }
+  if ((t & 31) == 0) {
+    atomicMin(&key_range[0], kmn);
+    atomicMax(&key_range[1], kmx);
+  }
   __syncthreads();
   if (mode == 0)
     for (int64_t p = t; p < f; p += blockDim.x) S.rank_of[S.prehit[b0 + p]] = -1;
@@ -827,10 +843,13 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
     uint64_t prefix = 0, mask = 0;
     if (K < ncand) {
       int64_t need = K;
-      const int shifts[6] = {53, 42, 31, 20, 10, 0};
-      const int widths[6] = {11, 11, 11, 11, 10, 10};
-      for (int pass = 0; pass < 6; ++pass) {
-        const int sh_ = shifts[pass], wd = widths[pass];
+      // start at the highest bit in which the candidates differ (the bits above are shared)
+      int hi_bit = 64 - __clzll(static_cast<long long>(key_range[0] ^ key_range[1]));
+      mask = hi_bit >= 64 ? 0ull : ~((uint64_t(1) << hi_bit) - 1);
+      prefix = key_range[0] & mask;
+      while (hi_bit > 0) {
+        const int wd = min(11, hi_bit), sh_ = hi_bit - wd;
+        hi_bit = sh_;
         const uint64_t bmask = (uint64_t(1) << wd) - 1;
         hist[2 * t] = 0;
         hist[2 * t + 1] = 0;
@@ -1411,6 +1430,7 @@ __global__ void __launch_bounds__(32, 1) k_walk(Pool P, Scratch S, InsertArgs A,
   __syncwarp();
   int64_t ptr = 0, fi = 0, nev = 0, nnew = 0, failpos = -1;
   int status = 0;
+  bool taken_seen = false;  // lane 0: some victim was referenced by a hit of this insert
   for (int64_t p0 = f; p0 < P_ && status == 0; p0 += 32) {
     // the warp prefetches 32 positions' pre-state probe results
     const int64_t p = p0 + lane;
@@ -1423,6 +1443,53 @@ __global__ void __launch_bounds__(32, 1) k_walk(Pool P, Scratch S, InsertArgs A,
         late = P.ref[b] == -1 && P.pinned[b] == 0;
       }
     }
+    // Fast path (the common case of a continuation: fresh tool-output blocks):
+    // every position of the chunk misses, no late candidate is pending and no
+    // victim was referenced, so the i-th miss takes the next free id, else the
+    // next victim in (tier, last_used, id) order — all 32 lanes in parallel.
+    const bool all_miss = __all_sync(0xffffffffu, b < 0);
+    const bool simple = __shfl_sync(0xffffffffu, static_cast<int>(nl == 0 && !taken_seen), 0) != 0;
+    if (all_miss && simple) {
+      const int64_t n = (P_ - p0) < 32 ? (P_ - p0) : int64_t(32);
+      const int64_t fi0 = __shfl_sync(0xffffffffu, fi, 0), ptr0 = __shfl_sync(0xffffffffu, ptr, 0);
+      const int64_t nev0 = __shfl_sync(0xffffffffu, nev, 0);
+      const int64_t a = Fp - fi0 > 0 ? Fp - fi0 : 0;  // free ids left
+      const int64_t i = lane;
+      bool ok = i < n;
+      bool fail = false;
+      int32_t id = -1;
+      if (ok) {
+        if (i < a) {
+          id = S.freel[fi0 + i];
+        } else if (ptr0 + (i - a) < K) {
+          const uint64_t vk = vs ? vic_s[ptr0 + (i - a)] : S.victims[ptr0 + (i - a)];
+          id = static_cast<int32_t>(vk & P.idmask);
+          S.evicted[nev0 + (i - a)] = id;
+        } else {
+          fail = true;
+        }
+      }
+      const unsigned fm = __ballot_sync(0xffffffffu, fail);
+      const int64_t nok = fm ? static_cast<int64_t>(__ffs(fm) - 1) : n;  // positions assigned
+      if (ok && i < nok) {
+        S.chain_out[p0 + i] = id;
+        S.kind[p0 + i] = 1;
+      }
+      if (lane == 0) {
+        const int64_t from_free = nok < a ? nok : a;
+        fi = fi0 + from_free;
+        ptr = ptr0 + (nok - from_free);
+        nev = nev0 + (nok - from_free);
+        nnew += nok;
+        if (fm) {
+          status = SB_ERR_CACHE_FULL;
+          failpos = p0 + nok;
+        }
+      }
+      status = __shfl_sync(0xffffffffu, status, 0);
+      __syncwarp();
+      continue;
+    }
     pb[lane] = b;
     pr[lane] = r;
     pl[lane] = late;
@@ -1434,8 +1501,12 @@ __global__ void __launch_bounds__(32, 1) k_walk(Pool P, Scratch S, InsertArgs A,
         const int32_t bb = pb[i], rr = pr[i];
         bool miss = bb < 0;
         if (!miss && rr >= 0) {
-          if (rr < ptr && !taken[rr]) miss = true;  // evicted earlier in this insert
-          else taken[rr] = 1;                        // referenced: no longer a candidate
+          if (rr < ptr && !taken[rr]) {
+            miss = true;  // evicted earlier in this insert
+          } else {
+            taken[rr] = 1;  // referenced: no longer a candidate
+            taken_seen = true;
+          }
         }
         if (!miss) {
           S.chain_out[q] = bb;
@@ -1625,6 +1696,14 @@ __global__ void k_index_fill(Pool P) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < P.cap;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     if (P.ntok[i] > 0) index_insert(P, P.chain[i], static_cast<int32_t>(i), P.parent[i], P.ntok[i]);
+}
+
+// out[pos ? pos[i] : i] = chain hash of resident block ids[i]
+__global__ void k_gather_chain(Pool P, const int32_t* __restrict__ ids, const int64_t* __restrict__ pos, int64_t n,
+                               uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[pos ? pos[i] : i] = P.chain[ids[i]];
 }
 
 __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
@@ -1881,6 +1960,29 @@ int sb_chain_hash_batch(const uint64_t* d_tokens, const int64_t* d_seq_offsets, 
     if (block_size < 1) throw Error(SB_ERR_INVALID, "block_size must be >= 1");
     launch_chain_hash(d_tokens, d_seq_offsets, d_block_offsets, d_parent, n_seqs, block_size, 0, d_block_hashes,
                       static_cast<cudaStream_t>(stream));
+    SB_CHECK_LAUNCH();
+    return int(SB_OK);
+  });
+}
+
+int sb_chain_hash_segments(const uint64_t* d_tokens, const int64_t* d_seg_bounds, const int64_t* d_seg_blocks,
+                           const uint64_t* d_parent, int32_t n_segs, int64_t block_size, uint64_t* d_block_hashes,
+                           void* stream) {
+  return guard([&] {
+    if (block_size < 1) throw Error(SB_ERR_INVALID, "block_size");
+    launch_chain_hash(d_tokens, d_seg_bounds, d_seg_blocks, d_parent, n_segs, block_size, 0, d_block_hashes,
+                      static_cast<cudaStream_t>(stream), 1);
+    SB_CHECK_LAUNCH();
+    return int(SB_OK);
+  });
+}
+
+int sb_kv_gather_chain_hashes(sb_kv_cache* c, const int32_t* d_ids, const int64_t* d_pos, int64_t n,
+                              uint64_t* d_out, void* stream) {
+  return guard([&] {
+    if (n <= 0) return int(SB_OK);
+    SB_CUDA(cudaSetDevice(c->device));
+    k_gather_chain<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(c->P, d_ids, d_pos, n, d_out);
     SB_CHECK_LAUNCH();
     return int(SB_OK);
   });
