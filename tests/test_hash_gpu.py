@@ -51,3 +51,46 @@ def test_chain_hash_batch_matches_oracle(bs, lens):
     got = _gpu_hashes(seqs, bs, parents)
     for i, s in enumerate(seqs):
         assert got[i] == _cpu_hashes(s, bs, parents[i]), (i, len(s))
+
+
+@pytest.mark.gpu
+def test_chain_hash_segments_and_prefix_gather():
+    """Incremental hashing: the suffix segments of prompts whose prefixes are
+    cached fold from the prefix's last chain hash (sb_chain_hash_segments);
+    the prefix hashes come from the pool (sb_kv_gather_chain_hashes).  Both
+    must equal the oracle's full-prompt chain."""
+    import torch
+    from paper_2601_12967_b200 import _lib
+    from paper_2601_12967_b200.kv_cache import CacheConfig, KvCache
+
+    L = _lib.lib()
+    rng = np.random.default_rng(9)
+    bs = 16
+    pre_lens, suf_lens = [32, 160, 16 * 37, 64], [5, 16, 700, 33]
+    cache = KvCache(CacheConfig(bs, 512, 1))
+    prompts, pre_ids = [], []
+    for pl, sl in zip(pre_lens, suf_lens):
+        t = rng.integers(0, 2**63, pl + sl, dtype=np.uint64)
+        prompts.append(t)
+        pre_ids.append(cache.insert(t[:pl], [(0, pl, 3)], 1))
+    toks = np.concatenate(prompts)
+    off = np.concatenate([[0], np.cumsum([len(t) for t in prompts])])
+    nblk = [(len(t) + bs - 1) // bs for t in prompts]
+    boff = np.concatenate([[0], np.cumsum(nblk)])
+    seg = np.array([[off[i] + pre_lens[i], off[i + 1]] for i in range(len(prompts))], dtype=np.int64).ravel()
+    segblk = np.array([boff[i] + pre_lens[i] // bs for i in range(len(prompts))], dtype=np.int64)
+    ids = np.concatenate([np.array(x, dtype=np.int32) for x in pre_ids])
+    pos = np.concatenate([boff[i] + np.arange(pre_lens[i] // bs) for i in range(len(prompts))]).astype(np.int64)
+    last = np.array([x[-1] for x in pre_ids], dtype=np.int32)
+    d = lambda a: torch.from_numpy(a).cuda()
+    out = torch.zeros(int(boff[-1]), dtype=torch.int64, device="cuda")
+    par = torch.zeros(len(prompts), dtype=torch.int64, device="cuda")
+    p = lambda t: C.c_void_p(t.data_ptr())
+    dt, dseg, dsb, dids, dpos, dlast = d(toks.view(np.int64)), d(seg), d(segblk), d(ids), d(pos), d(last)
+    _lib.check(L.sb_kv_gather_chain_hashes(cache.handle, p(dids), p(dpos), len(ids), p(out), None))
+    _lib.check(L.sb_kv_gather_chain_hashes(cache.handle, p(dlast), None, len(last), p(par), None))
+    _lib.check(L.sb_chain_hash_segments(p(dt), p(dseg), p(dsb), p(par), len(prompts), bs, p(out), None))
+    torch.cuda.synchronize()
+    h = out.cpu().numpy().view(np.uint64)
+    for i, t in enumerate(prompts):
+        assert h[boff[i]:boff[i + 1]].tolist() == _cpu_hashes(t, bs, O.root_hash()), i
