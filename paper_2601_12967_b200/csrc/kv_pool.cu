@@ -2310,6 +2310,7 @@ int sb_kv_touch(sb_kv_cache* c, const int32_t* ids, int64_t n, int64_t now) {
   return guard([&] {
     std::lock_guard<std::mutex> lk(c->mu);
     SB_CUDA(cudaSetDevice(c->device));
+    check_now(c->P, now);
     return run_validated(c, ids, n, 0, 1, 0, 0, now);
   });
 }

@@ -217,3 +217,23 @@ def test_huge_pool_keys_read_in_place():
         assert o.evict(needed) == c.evict(needed), needed
     assert o.dump() == c.dump()
     c.audit()
+
+
+@pytest.mark.gpu
+def test_time_range_guard():
+    """Victim keys hold last_used in 61 - idb bits: times outside +-2^(60-idb)
+    are rejected loudly (never silently wrapped) by every call that stores
+    a time."""
+    from paper_2601_12967_b200 import errors
+    from paper_2601_12967_b200.kv_cache import CacheConfig, KvCache
+
+    c = KvCache(CacheConfig(16, 64, 1))
+    t = O.materialize(0, 32, 1)
+    ids = c.insert(t, [(0, 32, 3)], (1 << 39) - 1)
+    for bad in (1 << 39, -(1 << 39) - 1):
+        with pytest.raises(errors.Unsupported):
+            c.insert(t, [(0, 32, 3)], bad)
+        with pytest.raises(errors.Unsupported):
+            c.lookup_prefix(t, bad)
+        with pytest.raises(errors.Unsupported):
+            c.touch(ids, bad)
