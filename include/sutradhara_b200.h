@@ -87,7 +87,7 @@ uint64_t sb_kv_chain_hash_host(uint64_t parent, const uint64_t* tokens, int64_t 
  * d_block_hashes[d_block_offsets[s] + j].  The chain for sequence s starts
  * from d_parent[s] (NULL = kv_root_hash()).  Replaces the per-block
  * kv_chain_hash loop inside KvCache::lookup_prefix / insert
- * (kv_cache.cpp:90-98, 471-475). */
+ * (kv_cache.cpp:90-98, 138-141). */
 int sb_chain_hash_batch(const uint64_t* d_tokens, const int64_t* d_seq_offsets,
                         const int64_t* d_block_offsets, const uint64_t* d_parent,
                         int32_t n_seqs, int64_t block_size, uint64_t* d_block_hashes,
@@ -121,7 +121,7 @@ int sb_kv_lookup_prefix(sb_kv_cache* cache, const uint64_t* tokens, int64_t n_to
                         int64_t now, int64_t* hit_tokens);
 /* KvCache::insert(tokens, tags, now)             kv_cache.cpp:103
  * out_ids must hold ceil(n_tokens / block_size) entries.  On CacheFull the
- * reference's rollback is reproduced (kv_cache.cpp:130-136, 481-487). */
+ * reference's rollback is reproduced (kv_cache.cpp:130-136, 148-154). */
 int sb_kv_insert(sb_kv_cache* cache, const uint64_t* tokens, int64_t n_tokens,
                  const sb_tag_range* tags, int64_t n_tags, int64_t now, int32_t* out_ids,
                  int64_t* n_out);
