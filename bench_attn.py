@@ -45,7 +45,7 @@ def measure(n_requests: int = 64, launches: int = 6, flashinfer: bool = False) -
     work = torch.from_numpy(attention_work_list(q_lens, kv_lens, hq, hkv)).cuda()
     flops = attention_flops(q_lens, kv_lens, hq)
     out = torch.empty_like(q)
-    for _ in range(2):
+    for _ in range(8):
         continuation_attention(q, kp, vp, q_off, kvl, table, max(q_lens), out=out, work=work)
     torch.cuda.synchronize()
     ts = []
