@@ -146,6 +146,8 @@ def reduce_over_ranks(values, device=None):
     import torch
     import torch.distributed as dist
 
+    if dist.is_available() and dist.is_initialized() and dist.get_backend() == "gloo":
+        device = None  # the CPU test backend reduces host tensors
     v = torch.tensor(values, dtype=torch.float64, device=device)
     mx, sm = v.clone(), v.clone()
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
@@ -155,6 +157,15 @@ def reduce_over_ranks(values, device=None):
 
 
 # ---------------------------------------------------------------- our arm
+def gpu_of(local_rank: int) -> int:
+    """This rank's GPU: one per rank (the driver's torchrun layout); ranks
+    beyond the visible GPU count share them (functional tests of the N>1 path
+    on a single GPU, with SB_DIST_BACKEND=gloo)."""
+    import torch
+
+    return local_rank % max(1, torch.cuda.device_count())
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -162,6 +173,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2601_12967_b200.engine import LLAMA3_8B, ContinuationEngine
     from paper_2601_12967_b200.kv_cache import TIERED
 
+    local_rank = gpu_of(local_rank)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     reqs = setup_workload(rank, args.requests)
@@ -242,6 +254,11 @@ def run_ours(args, rank, world, local_rank):
                                 float(stats["evicted_blocks"]), attn_avg_ms], dev)
     ms, ms_e2e, attn_avg_ms = mx[0], mx[1], mx[5]
     hit_rate = sm[2] / sm[3]
+    prefix_tokens = int(sum(batch.prefix_lens))
+    del batch, eng
+    torch.cuda.empty_cache()
+    # configs[2] on every rank (weak scaling; its timing is max-reduced over ranks)
+    full_model = None if args.no_dense else run_dense(args, rank, world, local_rank)
     if rank != 0:
         return None
 
@@ -268,7 +285,7 @@ def run_ours(args, rank, world, local_rank):
             "model_shape": "Llama-3-8B attention: 32 layers x 32 q / 8 kv heads x 128, 16-token KV pages",
             "requests_per_gpu": args.requests,
             "suffix_tokens_per_step_per_gpu": tokens_per_step,
-            "prefix_tokens_per_step_per_gpu": int(sum(batch.prefix_lens)),
+            "prefix_tokens_per_step_per_gpu": prefix_tokens,
             "kv_pool_blocks_per_gpu": cap,
             "kv_pool_gib_per_gpu": round(cap * LLAMA3_8B.kv_bytes_per_token * 16 / 2**30, 1),
             "eviction_policy": "tiered (hint-aware)",
@@ -290,10 +307,8 @@ def run_ours(args, rank, world, local_rank):
                      "launches_timed": len(attn_ms)},
         "clocks": clk,
     }
-    del batch, eng
-    torch.cuda.empty_cache()
-    if not args.no_dense:
-        line["full_model"] = run_dense(args, rank, world, local_rank)
+    if full_model is not None:
+        line["full_model"] = full_model
     try:  # same attention problem through NVIDIA's trtllm-gen kernel (flashinfer cubin), as a reference point
         import bench_attn
 
@@ -325,6 +340,7 @@ def run_dense(args, rank, world, local_rank):
     from paper_2601_12967_b200.engine import LLAMA3_8B, LLAMA3_8B_DENSE, ContinuationEngine, DenseModel
     from paper_2601_12967_b200.kv_cache import TIERED
 
+    local_rank = gpu_of(local_rank)
     dev = torch.device("cuda", local_rank)
     reqs = W.long_prefix_continuation_batch(8, seed=rank + 1)
     pre_b, suf_b, cap = capacity_for(reqs, slack=2.5)
@@ -566,8 +582,8 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(gpu_of(local_rank))
+        dist.init_process_group(os.environ.get("SB_DIST_BACKEND", "nccl"))
     line = run_ours(args, rank, world, local_rank)
     if line is not None:
         print(json.dumps(line))
