@@ -259,6 +259,11 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.empty_cache()
     # configs[2] on every rank (weak scaling; its timing is max-reduced over ranks)
     full_model = None if args.no_dense else run_dense(args, rank, world, local_rank)
+    trace = None
+    if not args.no_trace:  # sharded over the ranks, gathered on rank 0
+        per_gpu = tokens_per_step / (ms / args.steps) * 1e3
+        per_gpu_full = full_model["tokens_per_s"] / world if full_model else None
+        trace = trace_replay_metrics(per_gpu, local_rank, per_gpu_full, rank, world, dev)
     if rank != 0:
         return None
 
@@ -319,9 +324,8 @@ def run_ours(args, rank, world, local_rank):
             "note": "both kernels on identical synthetic paged KV/queries of the configs[1] step, CUDA events"}
     except Exception as e:  # library absent or incompatible: no reference point
         line["roofline"]["library_reference"] = {"unavailable": str(e)[:200]}
-    if not args.no_trace:
-        fm = line.get("full_model", {}).get("tokens_per_s")
-        line.update(trace_replay_metrics(line["value"], local_rank, fm))
+    if trace is not None:
+        line.update(trace)
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(reqs, budget_s=20.0)
     return line
@@ -411,43 +415,77 @@ def run_dense(args, rank, world, local_rank):
 TRACE = dict(n_requests=60, seed=1, capacity_blocks=8192, workload="default")
 
 
-def trace_replay_metrics(tokens_per_s: float, device: int, full_model_tokens_per_s=None):
+def trace_replay_metrics(tokens_per_s: float, device: int, full_model_tokens_per_s=None, rank: int = 0,
+                         world: int = 1, dev=None):
     """p50 FTR and hint-aware hit rate on the reference's synthetic agent
-    trace (trace_gen default workload, 60 requests, 8192-block pool),
-    replayed with every KV decision on the B200 pool (csrc/replay.cu):
+    trace (trace_gen default workload, 60 requests per GPU, 8192-block pool per
+    GPU), replayed with every KV decision on the B200 pool (csrc/replay.cu):
     - reference cost model: identical to the reference simulator's numbers
       (tests/test_replay_gpu.py), for the Sutradhara and Baseline presets;
-    - B200-calibrated: prefill charged at the measured full-model
+    - B200-calibrated: prefill charged at the measured per-GPU full-model
       continuation-prefill rate (configs[2], all dense layers + attention) when
       available, else at the attention-path rate, instead of the reference's
-      0.05 ms/token (decode model unchanged)."""
+      0.05 ms/token (decode model unchanged).
+    With N GPUs the trace is sharded: rank r replays its own 60 requests (seed
+    1 + r) on its own pool, and the per-request FTRs and the hit / prompt /
+    eviction counters are gathered over NCCL for the job-wide p50 and hit rate
+    (the only cross-GPU traffic)."""
+    import torch
     from paper_2601_12967_b200.replay import replay
 
-    out = {}
+    cfg = dict(TRACE)
+    cfg["seed"] = TRACE["seed"] + rank
     t0 = time.perf_counter()
-    sut = replay(preset="sutradhara", device=device, **TRACE)
+    runs = {"sutradhara": replay(preset="sutradhara", device=device, **cfg)}
     wall = time.perf_counter() - t0
-    base = replay(preset="baseline", device=device, **TRACE)
+    runs["baseline"] = replay(preset="baseline", device=device, **cfg)
     rate = full_model_tokens_per_s or tokens_per_s
     cal_cost = [1000.0 / rate, 20.0, 2.0, 256]
-    sut_cal = replay(preset="sutradhara", device=device, cost=cal_cost, **TRACE)
-    base_cal = replay(preset="baseline", device=device, cost=cal_cost, **TRACE)
-    out["p50_ftr_ms"] = sut.p50()
+    runs["sutradhara_cal"] = replay(preset="sutradhara", device=device, cost=cal_cost, **cfg)
+    runs["baseline_cal"] = replay(preset="baseline", device=device, cost=cal_cost, **cfg)
+
+    def gathered(r):
+        """(all ranks' FTRs, e2e times, hit tokens, prompt tokens, evictions)"""
+        row = np.concatenate([r.ftr_ms, r.e2e_ms, [r.hit_tokens.sum(), r.prompt_tokens.sum(), r.evictions]])
+        t = torch.tensor(row, dtype=torch.float64, device=dev)
+        import torch.distributed as dist
+
+        if world > 1 and dist.is_initialized():
+            if dist.get_backend() == "gloo":
+                t = t.cpu()
+            parts = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(parts, t)
+            t = torch.stack(parts)
+        else:
+            t = t[None]
+        a = t.cpu().numpy()
+        n = len(r.ftr_ms)
+        return a[:, :n].ravel(), a[:, n:2 * n].ravel(), a[:, 2 * n].sum(), a[:, 2 * n + 1].sum(), a[:, 2 * n + 2].sum()
+
+    def p50(v):
+        v = np.sort(v)
+        return float(v[max(1, int(np.ceil(0.5 * len(v)))) - 1])
+
+    g = {k: gathered(r) for k, r in runs.items()}
+    if rank != 0:
+        return None
+    summ = {k: {"p50_ftr_ms": p50(v[0]), "p50_e2e_ms": p50(v[1]), "hit_rate": float(v[2] / max(1.0, v[3])),
+                "evictions": int(v[4])} for k, v in g.items()}
+    out = {"p50_ftr_ms": summ["sutradhara"]["p50_ftr_ms"]}
     out["trace"] = {
-        "workload": "reference trace_gen default workload, 60 requests, seed 1, pool 8192 x 16-token blocks",
-        "sutradhara": {"p50_ftr_ms": sut.p50(), "p50_e2e_ms": sut.p50(sut.e2e_ms), "hit_rate": sut.hit_rate,
-                       "evictions": sut.evictions},
-        "baseline": {"p50_ftr_ms": base.p50(), "p50_e2e_ms": base.p50(base.e2e_ms), "hit_rate": base.hit_rate,
-                     "evictions": base.evictions},
+        "workload": f"reference trace_gen default workload, 60 requests per GPU (seeds 1..{world}), "
+                    f"pool 8192 x 16-token blocks per GPU, {world} GPU(s)",
+        "sutradhara": summ["sutradhara"],
+        "baseline": summ["baseline"],
         "b200_calibrated": {"prefill_ms_per_token": cal_cost[0],
-                            "prefill_rate_source": "full_model (configs[2])" if full_model_tokens_per_s
-                            else "attention path (configs[1])",
-                            "sutradhara_p50_ftr_ms": sut_cal.p50(),
-                            "baseline_p50_ftr_ms": base_cal.p50(),
-                            "sutradhara_hit_rate": sut_cal.hit_rate},
+                            "prefill_rate_source": "full_model (configs[2]), per GPU" if full_model_tokens_per_s
+                            else "attention path (configs[1]), per GPU",
+                            "sutradhara_p50_ftr_ms": summ["sutradhara_cal"]["p50_ftr_ms"],
+                            "baseline_p50_ftr_ms": summ["baseline_cal"]["p50_ftr_ms"],
+                            "sutradhara_hit_rate": summ["sutradhara_cal"]["hit_rate"]},
         "replay_wall_s": wall,
     }
-    out["hint_aware_hit_rate"] = sut.hit_rate
+    out["hint_aware_hit_rate"] = summ["sutradhara"]["hit_rate"]
     return out
 
 
