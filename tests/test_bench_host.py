@@ -1,0 +1,75 @@
+"""CPU: host-side pieces of bench.py and the workloads — pool sizing, the
+configs[2] request shape, the committed ncu evidence the bench line cites,
+and the stats all-gather used by the sharded trace metrics (world_size 2,
+gloo)."""
+import json
+import os
+import socket
+
+import numpy as np
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import bench
+from paper_2601_12967_b200 import workload as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_configs2_requests():
+    reqs = W.long_prefix_continuation_batch(8)
+    lens = [r.prefix_len for r in reqs]
+    assert lens[0] == 8192 and lens[-1] == 32768 and lens == sorted(lens)
+    assert all(l % 16 == 0 for l in lens) and all(r.suffix_len == 1024 for r in reqs)
+    # shared system prompt: identical first 2048 tokens
+    assert all(np.array_equal(r.prefix_tokens[:2048], reqs[0].prefix_tokens[:2048]) for r in reqs)
+    assert len({int(r.prefix_tokens[2048]) for r in reqs}) == len(reqs)
+
+
+def test_capacity_for_counts_shared_prefix_once():
+    reqs = W.agentic_continuation_batch(4, seed=1)
+    pre, suf, cap = bench.capacity_for(reqs)
+    assert pre == sum(r.prefix_len // 16 for r in reqs) - 3 * (2048 // 16)
+    assert suf == sum((r.suffix_len + 15) // 16 for r in reqs)
+    assert cap == pre + int(1.25 * suf) + 1
+
+
+def test_attention_traffic_from_committed_ncu():
+    t = bench.ncu_traffic(bench.ATTN_NCU)
+    m = json.load(open(bench.ATTN_NCU))
+    assert "continuation_attention" in m["kernel"]
+    assert 1e9 < t < 1e10  # bytes per launch, read + write
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # the gather pattern of bench.trace_replay_metrics: fixed-size rows per rank
+    row = torch.tensor([10.0 * rank + i for i in range(5)], dtype=torch.float64)
+    parts = [torch.empty_like(row) for _ in range(world)]
+    dist.all_gather(parts, row)
+    q.put((rank, torch.stack(parts).numpy().tolist()))
+    dist.destroy_process_group()
+
+
+def test_trace_stats_gather_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][1] == res[1][1] == [[0.0, 1.0, 2.0, 3.0, 4.0], [10.0, 11.0, 12.0, 13.0, 14.0]]
