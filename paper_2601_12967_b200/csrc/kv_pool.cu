@@ -742,6 +742,7 @@ struct InsertArgs {
 __global__ void __launch_bounds__(kSelectThreads, 1)
     k_select(Pool P, Scratch S, InsertArgs A, int s, int mode, int64_t needed) {
   __shared__ uint32_t hist[2048];
+  __shared__ uint32_t bmin[2048], bmax[2048];  // per bin: min / max of the 32 key bits below the digit
   __shared__ uint32_t warp_sums[33];
   __shared__ int64_t sh[8];
   __shared__ uint32_t cnt_b;
@@ -851,12 +852,28 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
         const int wd = min(11, hi_bit), sh_ = hi_bit - wd;
         hi_bit = sh_;
         const uint64_t bmask = (uint64_t(1) << wd) - 1;
+        const int s2 = sh_ > 32 ? sh_ - 32 : 0;  // the 32 key bits below the digit: [s2, s2 + 32)
         hist[2 * t] = 0;
         hist[2 * t + 1] = 0;
+        bmin[2 * t] = bmin[2 * t + 1] = ~0u;
+        bmax[2 * t] = bmax[2 * t + 1] = 0u;
         __syncthreads();
-        for (int64_t i = t; i < ncand; i += blockDim.x) {
-          const uint64_t k = key_at(i);
-          if ((k & mask) == prefix) atomicAdd(&hist[(k >> sh_) & bmask], 1u);
+        // warp-aggregated: the keys of one pass crowd into a few bins (same
+        // tier / last_used high bits), so lanes with equal digits combine
+        // first and one lane per distinct digit updates shared memory
+        for (int64_t i0 = 0; i0 < ncand; i0 += blockDim.x) {
+          const int64_t i = i0 + t;
+          const uint64_t k = i < ncand ? key_at(i) : 0;
+          const bool part = i < ncand && (k & mask) == prefix;
+          const uint32_t d = part ? static_cast<uint32_t>((k >> sh_) & bmask) : 0xFFFFFFFFu;
+          const uint32_t low = static_cast<uint32_t>(k >> s2);
+          const unsigned peers = __match_any_sync(0xffffffffu, d);
+          const uint32_t mn = __reduce_min_sync(peers, low), mxv = __reduce_max_sync(peers, low);
+          if (part && (t & 31) == __ffs(peers) - 1) {
+            atomicAdd(&hist[d], static_cast<uint32_t>(__popc(peers)));
+            atomicMin(&bmin[d], mn);
+            atomicMax(&bmax[d], mxv);
+          }
         }
         __syncthreads();
         const uint32_t a0 = hist[2 * t], a1 = hist[2 * t + 1];
@@ -877,6 +894,22 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
         prefix |= static_cast<uint64_t>(sh[4]) << sh_;
         mask |= bmask << sh_;
         const bool done = (static_cast<int64_t>(cnt_b) == need);
+        if (!done && sh_ > 0) {
+          // skip the bits below the digit that every key of the chosen bin
+          // shares (tiered keys: same tier and last_used high bits)
+          const uint32_t lo = bmin[sh[4]], hi = bmax[sh[4]];
+          const int top = sh_ - s2;                           // valid bits of lo/hi: [0, top)
+          const uint32_t vmask = top >= 32 ? ~0u : ((1u << top) - 1);
+          const uint32_t diff = (lo ^ hi) & vmask;
+          const int nb = diff ? 32 - __clz(diff) : 0;         // differing bits are [0, nb)
+          const int new_hi = s2 + nb;                         // next digit starts below new_hi
+          if (new_hi < sh_) {
+            const uint64_t shared_bits = (((uint64_t(1) << (sh_ - new_hi)) - 1)) << new_hi;
+            prefix |= (static_cast<uint64_t>(lo) << s2) & shared_bits;
+            mask |= shared_bits;
+            hi_bit = new_hi;
+          }
+        }
         __syncthreads();
         if (done) break;
       }
