@@ -53,7 +53,7 @@ constexpr uint64_t kNoKey = ~uint64_t(0);
 constexpr int kSelectThreads = 1024;
 constexpr int kSortSmemKeys = 8192;
 constexpr int kCandSmem = 16384;  // candidate keys staged in shared memory (128 KB)
-constexpr int64_t kCoopMinCap = 65536;  // pools at least this large use the all-SM scorer
+constexpr int64_t kCoopMinCap = 16384;  // pools at least this large use the all-SM scorer
 
 enum Ctr { C_NRES = 0, C_EVICTED, C_LOOKUPS, C_HIT_TOK, C_LOOK_TOK, C_INS_BLOCKS, C_EV_BLOCKS, C_FULL, C_N };
 enum Scal { S_F = 0, S_K, S_FREE, S_NEV, S_STATUS, S_FAILPOS, S_NNEW, S_NCAND, S_ERRIDX, S_NLATE, S_N };

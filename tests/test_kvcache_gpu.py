@@ -169,7 +169,7 @@ def test_batch_apis_match_sequential_oracle():
 
 @pytest.mark.gpu
 def test_large_pool_cooperative_scorer():
-    """Pools of >= 65536 blocks use the all-SM cooperative scorer
+    """Pools of >= 16384 blocks use the all-SM cooperative scorer
     (k_select_coop): eviction order, insert ids under pressure and the full
     dump must still equal the oracle."""
     bs, cap = 1, 70000
