@@ -64,6 +64,7 @@ CASES = [
     ([257, 64], [2048, 4095], 32, 8),         # Llama-3-8B heads, multi-tile
     ([130], [70], 2, 2),                      # MHA (group 1): 128 tokens per tile
     ([96, 200], [500, 33], 16, 8),            # group 2
+    ([40, 17], [32768, 20000], 32, 8),        # configs[2]-long cached prefixes (2K+ pages per sequence)
 ]
 
 
@@ -117,3 +118,28 @@ def test_kv_append_then_attend():
     out = continuation_attention(q, kp, vp, qo, kl, tb, max(q_lens))
     ref = ref_attention(q, kp, vp, qo.cpu(), kl.cpu(), tb, 1 / math.sqrt(128))
     assert (out.float() - ref).abs().max().item() <= REL_TOL_BF16 * ref.abs().max().item() + 1e-3
+
+
+@pytest.mark.gpu
+def test_running_max_keeps_growing():
+    """Scores that rise along the key axis force the online softmax to raise
+    its running max (and lazily rescale O in TMEM) again and again."""
+    import torch
+    from paper_2601_12967_b200.attention import continuation_attention
+
+    q_lens, prefix = [70, 33], [3000, 1200]
+    q, kp, vp, qo, kl, tb = make_case(q_lens, prefix, 8, 2, seed=5)
+    # key position p of sequence s gets dim 0 = p / 64 (bf16-exact multiples), queries dim 0 = 2:
+    # the logit grows by ~0.25 nats per 16 keys -> a new max far above the old one every few tiles
+    for s, k in enumerate([p + ql for p, ql in zip(prefix, q_lens)]):
+        for pos in range(k):
+            kp[tb[s, pos // 16], :, pos % 16, 0] = pos / 64.0
+    q[:, :, 0] = 2.0
+    dev = torch.device("cuda")
+    q, kp, vp, qo, kl, tb = (x.to(dev) for x in (q, kp, vp, qo, kl, tb))
+    out = continuation_attention(q, kp, vp, qo, kl, tb, max(q_lens))
+    torch.cuda.synchronize()
+    ref = ref_attention(q, kp, vp, qo.cpu(), kl.cpu(), tb, 1 / math.sqrt(128))
+    assert torch.isfinite(out.float()).all()
+    err = (out.float() - ref).abs().max().item()
+    assert err <= REL_TOL_BF16 * ref.abs().max().item() + 1e-3, err
