@@ -220,6 +220,16 @@ int sb_continuation_attention(const void* q, const void* k_pool, const void* v_p
                               int64_t n_pool_blocks, float softmax_scale, const int32_t* d_work,
                               int32_t n_work, void* stream);
 
+/* The same op in fp32 on CUDA cores (fp32 q / pages / out; outputs within
+ * 1e-5 of an fp32 reference): the precision contract of fp32 pipelines such
+ * as the toy model of BASELINE configs[0].  Same layouts and arguments. */
+int sb_continuation_attention_f32(const float* q, const float* k_pool, const float* v_pool, float* out,
+                                  const int32_t* d_q_offsets, const int32_t* d_kv_lens,
+                                  const int32_t* d_block_table, int32_t n_seqs,
+                                  int32_t max_blocks_per_seq, int32_t total_q, int32_t n_q_heads,
+                                  int32_t n_kv_heads, int32_t head_dim, int32_t page_size,
+                                  float softmax_scale, void* stream);
+
 /* Work list for sb_continuation_attention (host): one item per (sequence, kv
  * head, pair of 128-row query tiles) that has queries, longest first (LPT),
  * as int32 pairs {seq, kv_head << 16 | pair}.  out holds 2*cap ints; returns

@@ -69,6 +69,8 @@ SIGNATURES = {
     "sb_continuation_attention": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                             C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_float, VP,
                                             C.c_int32, VP]),
+    "sb_continuation_attention_f32": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                                C.c_int32, C.c_int32, C.c_int32, C.c_float, VP]),
     "sb_attention_work_list": (C.c_int, [I32P, I32P, C.c_int32, C.c_int32, C.c_int32, I32P, C.c_int32, I32P]),
     "sb_build_block_table": (C.c_int, [VP, VP, C.c_int32, C.c_int32, VP, VP]),
     "sb_kv_gather_chain_hashes": (C.c_int, [VP, VP, VP, C.c_int64, VP, VP]),

@@ -53,8 +53,19 @@ def continuation_attention(q, k_pool, v_pool, q_offsets, kv_lens, block_table, m
     """work: optional device int32 tensor from attention_work_list (LPT order)."""
     import torch
 
-    assert q.dtype == torch.bfloat16 and k_pool.dtype == torch.bfloat16 and v_pool.dtype == torch.bfloat16
     assert q.is_contiguous() and k_pool.is_contiguous() and v_pool.is_contiguous()
+    if q.dtype == torch.float32:  # fp32 contract (CUDA-core kernel, 1e-5 of an fp32 reference)
+        assert k_pool.dtype == torch.float32 and v_pool.dtype == torch.float32
+        total_q, n_q_heads, head_dim = q.shape
+        n_blocks, n_kv_heads, page, _ = k_pool.shape
+        out = torch.empty_like(q) if out is None else out
+        scale = 1.0 / math.sqrt(head_dim) if softmax_scale is None else softmax_scale
+        _lib.check(_lib.lib().sb_continuation_attention_f32(
+            _ptr(q), _ptr(k_pool), _ptr(v_pool), _ptr(out), _ptr(q_offsets), _ptr(kv_lens), _ptr(block_table),
+            kv_lens.numel(), block_table.shape[1], total_q, n_q_heads, n_kv_heads, head_dim, page,
+            C.c_float(scale), _stream_ptr(stream)), "continuation_attention_f32")
+        return out
+    assert q.dtype == torch.bfloat16 and k_pool.dtype == torch.bfloat16 and v_pool.dtype == torch.bfloat16
     total_q, n_q_heads, head_dim = q.shape
     n_blocks, n_kv_heads, page, hd2 = k_pool.shape
     assert hd2 == head_dim and tuple(v_pool.shape) == tuple(k_pool.shape)

@@ -394,6 +394,85 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// fp32 continuation attention (CUDA cores): the same op on fp32 pages, for
+// the fp32 precision contract (outputs within 1e-5 of an fp32 reference) —
+// e.g. the toy 2-layer model of BASELINE configs[0] whose reference path is
+// fp32.  One warp per (query token, q head); 32 keys per step, one per lane:
+// lane l folds q . k_l over the 128 dims (q broadcast from shared memory),
+// the warp runs the online softmax, and each lane accumulates 4 of the 128
+// output dims (coalesced V rows).
+constexpr int kF32Warps = 8;
+__global__ void __launch_bounds__(32 * kF32Warps) k_continuation_attention_f32(
+    const float* __restrict__ q, const float* __restrict__ k_pool, const float* __restrict__ v_pool,
+    float* __restrict__ out, const int32_t* __restrict__ q_off, const int32_t* __restrict__ kv_len,
+    const int32_t* __restrict__ table, int32_t n_seqs, int32_t max_blocks, int32_t n_q_heads, int32_t n_kv_heads,
+    float scale) {
+  __shared__ float4 qs[kF32Warps][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = blockIdx.x * static_cast<int64_t>(kF32Warps) + w;  // (token, head)
+  const int64_t total = static_cast<int64_t>(q_off[n_seqs]) * n_q_heads;
+  if (row >= total) return;
+  const int64_t tok = row / n_q_heads;
+  const int hq = static_cast<int>(row % n_q_heads), kvh = hq / (n_q_heads / n_kv_heads);
+  int lo = 0, hi = n_seqs;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (q_off[mid] <= tok) lo = mid; else hi = mid;
+  }
+  const int sq = lo;
+  const int q_len = q_off[sq + 1] - q_off[sq];
+  const int n_keys = kv_len[sq] - q_len + static_cast<int>(tok - q_off[sq]) + 1;  // causal
+  qs[w][lane] = reinterpret_cast<const float4*>(q + row * 128)[lane];
+  __syncwarp();
+  const int32_t* trow = table + static_cast<int64_t>(sq) * max_blocks;
+  float m = -INFINITY, l = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k0 = 0; k0 < n_keys; k0 += 32) {
+    const int key = k0 + lane;
+    float sc = -INFINITY;
+    if (key < n_keys) {
+      const int64_t page = trow[key / 16];
+      const float4* kr = reinterpret_cast<const float4*>(k_pool + ((page * n_kv_heads + kvh) * 16 + key % 16) * 128);
+      float d = 0.f;
+#pragma unroll 8
+      for (int c = 0; c < 32; ++c) {
+        const float4 kv = kr[c], qv = qs[w][c];
+        d = fmaf(qv.x, kv.x, fmaf(qv.y, kv.y, fmaf(qv.z, kv.z, fmaf(qv.w, kv.w, d))));
+      }
+      sc = d * scale;
+    }
+    float mx = sc;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float m_new = fmaxf(m, mx);
+    const float corr = expf(m - m_new);  // 0 on the first step
+    const float pr = key < n_keys ? expf(sc - m_new) : 0.f;
+    float ps = pr;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    l = l * corr + ps;
+    acc.x *= corr;
+    acc.y *= corr;
+    acc.z *= corr;
+    acc.w *= corr;
+    const int n_here = min(32, n_keys - k0);
+    for (int i = 0; i < n_here; ++i) {
+      const float pi = __shfl_sync(0xffffffffu, pr, i);
+      const int ki = k0 + i;
+      const int64_t page = trow[ki / 16];
+      const float4 vv =
+          reinterpret_cast<const float4*>(v_pool + ((page * n_kv_heads + kvh) * 16 + ki % 16) * 128)[lane];
+      acc.x = fmaf(pi, vv.x, acc.x);
+      acc.y = fmaf(pi, vv.y, acc.y);
+      acc.z = fmaf(pi, vv.z, acc.z);
+      acc.w = fmaf(pi, vv.w, acc.w);
+    }
+    m = m_new;
+  }
+  const float inv = 1.f / l;
+  reinterpret_cast<float4*>(out + row * 128)[lane] = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+}
+
 // KV append: write the suffix K/V rows into their pool pages.
 __global__ void k_kv_append(const __nv_bfloat16* __restrict__ k_new, const __nv_bfloat16* __restrict__ v_new,
                             __nv_bfloat16* __restrict__ k_pool, __nv_bfloat16* __restrict__ v_pool,
@@ -481,6 +560,25 @@ extern "C" int sb_continuation_attention(const void* q, const void* k_pool, cons
     if (grid <= 0) return int(SB_OK);
     kern<<<static_cast<unsigned>(grid), attn::kThreads, attn::kSmemBytes, static_cast<cudaStream_t>(stream)>>>(
         tm_q, tm_k, tm_v, prm);
+    SB_CHECK_LAUNCH();
+    return int(SB_OK);
+  });
+}
+
+extern "C" int sb_continuation_attention_f32(const float* q, const float* k_pool, const float* v_pool, float* out,
+                                             const int32_t* d_q_offsets, const int32_t* d_kv_lens,
+                                             const int32_t* d_block_table, int32_t n_seqs, int32_t max_blocks_per_seq,
+                                             int32_t total_q, int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim,
+                                             int32_t page_size, float softmax_scale, void* stream) {
+  return guard([&] {
+    if (head_dim != 128 || page_size != 16) throw Error(SB_ERR_UNSUPPORTED, "head_dim must be 128 and page_size 16");
+    if (n_kv_heads <= 0 || n_q_heads % n_kv_heads) throw Error(SB_ERR_INVALID, "n_q_heads % n_kv_heads != 0");
+    if (n_seqs <= 0 || total_q <= 0) return int(SB_OK);
+    const int64_t rows = static_cast<int64_t>(total_q) * n_q_heads;
+    attn::k_continuation_attention_f32<<<static_cast<unsigned>((rows + attn::kF32Warps - 1) / attn::kF32Warps),
+                                         32 * attn::kF32Warps, 0, static_cast<cudaStream_t>(stream)>>>(
+        q, k_pool, v_pool, out, d_q_offsets, d_kv_lens, d_block_table, n_seqs, max_blocks_per_seq, n_q_heads,
+        n_kv_heads, softmax_scale);
     SB_CHECK_LAUNCH();
     return int(SB_OK);
   });

@@ -13,7 +13,8 @@ def ref_attention(q, k_pool, v_pool, q_off, kv_lens, table, scale):
     """fp32 reference: gather pages, causal over the suffix, full over the prefix."""
     import torch
 
-    out = torch.zeros_like(q, dtype=torch.float32)
+    dt = torch.float64 if q.dtype == torch.float64 else torch.float32
+    out = torch.zeros_like(q, dtype=dt)
     n_kv = k_pool.shape[1]
     group = q.shape[1] // n_kv
     for s in range(len(kv_lens)):
@@ -22,9 +23,9 @@ def ref_attention(q, k_pool, v_pool, q_off, kv_lens, table, scale):
         if ql == 0:
             continue
         pages = table[s, : (kl + 15) // 16].long()
-        k = k_pool[pages].float().permute(1, 0, 2, 3).reshape(n_kv, -1, 128)[:, :kl]  # [kvh, kl, d]
-        v = v_pool[pages].float().permute(1, 0, 2, 3).reshape(n_kv, -1, 128)[:, :kl]
-        qs = q[a:b].float().permute(1, 0, 2)  # [hq, ql, d]
+        k = k_pool[pages].to(dt).permute(1, 0, 2, 3).reshape(n_kv, -1, 128)[:, :kl]  # [kvh, kl, d]
+        v = v_pool[pages].to(dt).permute(1, 0, 2, 3).reshape(n_kv, -1, 128)[:, :kl]
+        qs = q[a:b].to(dt).permute(1, 0, 2)  # [hq, ql, d]
         k = k.repeat_interleave(group, 0)
         v = v.repeat_interleave(group, 0)
         sc = qs @ k.transpose(1, 2) * scale  # [hq, ql, kl]
@@ -143,3 +144,27 @@ def test_running_max_keeps_growing():
     assert torch.isfinite(out.float()).all()
     err = (out.float() - ref).abs().max().item()
     assert err <= REL_TOL_BF16 * ref.abs().max().item() + 1e-3, err
+
+
+REL_TOL_F32 = 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [([64], [0], 4, 1), ([100, 37, 1], [300, 0, 1000], 8, 2), ([33], [2000], 2, 1)])
+def test_continuation_attention_f32_matches_fp32(case):
+    """fp32 contract (north star: 1e-5 in fp32), e.g. the toy 2-layer d=256
+    model of configs[0] (2 q heads x 128)."""
+    import torch
+    from paper_2601_12967_b200.attention import continuation_attention
+
+    q_lens, prefix, hq, hkv = case
+    q, kp, vp, qo, kl, tb = make_case(q_lens, prefix, hq, hkv, seed=11)
+    dev = torch.device("cuda")
+    q, kp, vp = (x.float().to(dev) for x in (q, kp, vp))
+    qo, kl, tb = (x.to(dev) for x in (qo, kl, tb))
+    out = continuation_attention(q, kp, vp, qo, kl, tb, max(q_lens))
+    torch.cuda.synchronize()
+    # float64 reference of the same op (so the tolerance measures our fp32 error)
+    ref = ref_attention(q.double(), kp.double(), vp.double(), qo.cpu(), kl.cpu(), tb, 1 / math.sqrt(128))
+    err = ((out.double() - ref).abs().max() / ref.abs().max()).item()
+    assert err <= REL_TOL_F32, err
