@@ -317,11 +317,12 @@ def run_ours(args, rank, world, local_rank):
     try:  # same attention problem through NVIDIA's trtllm-gen kernel (flashinfer cubin), as a reference point
         import bench_attn
 
-        ref = bench_attn.measure(args.requests, launches=5, flashinfer=True)
+        ref = bench_attn.measure(args.requests, launches=6, flashinfer=True)
         line["roofline"]["library_reference"] = {
             "ours_standalone_tflops": ref["tflops"], "flashinfer_trtllm_gen_tflops": ref["flashinfer"]["tflops"],
             "max_abs_diff": ref["flashinfer"]["max_abs_diff_vs_ours"],
-            "note": "both kernels on identical synthetic paged KV/queries of the configs[1] step, CUDA events"}
+            "note": "both kernels on identical synthetic paged KV/queries of the configs[1] step, CUDA events, "
+                    "3 alternating rounds of 6 launches each (median)"}
     except Exception as e:  # library absent or incompatible: no reference point
         line["roofline"]["library_reference"] = {"unavailable": str(e)[:200]}
     if trace is not None:

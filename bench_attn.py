@@ -45,19 +45,11 @@ def measure(n_requests: int = 64, launches: int = 6, flashinfer: bool = False) -
     work = torch.from_numpy(attention_work_list(q_lens, kv_lens, hq, hkv)).cuda()
     flops = attention_flops(q_lens, kv_lens, hq)
     out = torch.empty_like(q)
-    for _ in range(8):
+
+    def run_ours():
         continuation_attention(q, kp, vp, q_off, kvl, table, max(q_lens), out=out, work=work)
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(launches):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        continuation_attention(q, kp, vp, q_off, kvl, table, max(q_lens), out=out, work=work)
-        b.record()
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    ms = float(np.median(ts))
-    fi = None
+
+    run_fi = None
     if flashinfer:
         import flashinfer.prefill as FP
 
@@ -70,17 +62,31 @@ def measure(n_requests: int = 64, launches: int = 6, flashinfer: bool = False) -
             return FP.trtllm_batch_context_with_kv_cache(q, (kp, vp), ws, table, seq_lens, max(q_lens), max(kv_lens),
                                                          1.0 / np.sqrt(128), 1.0, len(reqs), q_off, cum_kv, out=fo,
                                                          kv_layout="HND", causal=True)
-        for _ in range(2):
-            run_fi()
-        torch.cuda.synchronize()
-        fts = []
-        for _ in range(launches):
+
+    def timed(fn, n):
+        ts = []
+        for _ in range(n):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            run_fi()
+            fn()
             b.record()
             torch.cuda.synchronize()
-            fts.append(a.elapsed_time(b))
+            ts.append(a.elapsed_time(b))
+        return ts
+
+    # warm both, then alternate rounds so both kernels see the same clock /
+    # power-cap state (short single runs of either are boost-clock biased)
+    for fn in (run_ours, run_fi):
+        if fn is not None:
+            timed(fn, 4)
+    ts, fts = [], []
+    for _ in range(3):
+        ts += timed(run_ours, launches)
+        if run_fi is not None:
+            fts += timed(run_fi, launches)
+    ms = float(np.median(ts))
+    fi = None
+    if run_fi is not None:
         fms = float(np.median(fts))
         fi = {"kernel": "flashinfer trtllm_batch_context_with_kv_cache (trtllm-gen cubin)", "ms": fms,
               "tflops": flops / fms / 1e9,
