@@ -338,6 +338,17 @@ int sb_model_weight(sb_model* model, int32_t layer, int32_t which, void** ptr, i
  * projection, SwiGLU MLP) and the LM head on each sequence's last token.
  * NULL detaches (attention-path mode with stand-in projections). */
 int sb_batch_set_model(sb_batch* batch, sb_model* model);
+/* The partial prefill itself (paper §4.2: the tool-independent prompt is
+ * prefilled while the tool runs; Engine::start_step charges it,
+ * engine.cpp:424-427): for each partial call, the prefix tokens not cached at
+ * submit (sb_engine_submit_partial records the admission lookup,
+ * engine.cpp:170) run through the model, their K/V written into the call's
+ * pinned pages.  A later continuation batch then attends over a prefix whose
+ * KV is the model's own. */
+int sb_engine_prefill_partials(sb_engine* engine, sb_model* model, const int32_t* handles, int32_t n,
+                               void* stream);
+/* Prefix tokens of a partial call that were already cached at submit. */
+int sb_engine_partial_cached(sb_engine* engine, int32_t handle, int64_t* cached_tokens);
 /* Greedy next token per sequence (int32 [n]) and/or fp32 logits [n, vocab]. */
 int sb_batch_model_result(sb_batch* batch, int32_t* next_tokens, float* logits, void* stream);
 /* Dense-layer FLOPs of one run (2 * tokens * weights of all layers). */

@@ -102,6 +102,8 @@ SIGNATURES = {
     "sb_model_vocab": (None, [VP, I64P]),
     "sb_model_weight": (C.c_int, [VP, C.c_int32, C.c_int32, C.POINTER(VP), I64P]),
     "sb_batch_set_model": (C.c_int, [VP, VP]),
+    "sb_engine_prefill_partials": (C.c_int, [VP, VP, I32P, C.c_int32, VP]),
+    "sb_engine_partial_cached": (C.c_int, [VP, C.c_int32, I64P]),
     "sb_batch_model_result": (C.c_int, [VP, I32P, C.POINTER(C.c_float), VP]),
     "sb_batch_dense_flops": (C.c_int, [VP, C.POINTER(C.c_double)]),
 }

@@ -76,6 +76,7 @@ struct PartialCall {
   std::vector<uint64_t> tokens;
   std::vector<sb_tag_range> tags;
   std::vector<int32_t> ids;
+  int64_t cached = 0;  // prefix tokens already in the pool at submit (engine.cpp:170)
   bool live = true;
 };
 
@@ -184,8 +185,13 @@ int sb_engine_submit_partial(sb_engine* e, const uint64_t* tokens, int64_t n, co
     pc.tokens.assign(tokens, tokens + n);
     pc.tags.assign(tags, tags + n_tags);
     pc.ids.resize(static_cast<size_t>((n + 15) / 16));
+    // admission lookup (engine.cpp:170): the prefix tokens whose KV is already
+    // cached; the partial prefill computes the rest (the insert below touches
+    // the same blocks at the same time, so the pool state is unchanged by it)
+    int st = sb_kv_lookup_prefix(e->cache, tokens, n, now, &pc.cached);
+    if (st) return st;
     int64_t n_out = 0;
-    int st = sb_kv_insert(e->cache, tokens, n, tags, n_tags, now, pc.ids.data(), &n_out);
+    st = sb_kv_insert(e->cache, tokens, n, tags, n_tags, now, pc.ids.data(), &n_out);
     if (st) return st;
     // pinned at the PARTIAL_PREFILL tier until extended or abandoned (engine.cpp:280-281)
     st = sb_kv_set_reuse_priority(e->cache, pc.ids.data(), n_out, 1, SB_TAG_PARTIAL_PREFILL);
@@ -215,6 +221,88 @@ int sb_engine_partial_blocks(sb_engine* e, int32_t handle, int32_t* out, int64_t
     const auto& ids = it->second.ids;
     *n_out = static_cast<int64_t>(ids.size());
     for (int64_t i = 0; i < std::min<int64_t>(cap, *n_out); ++i) out[i] = ids[i];
+    return int(SB_OK);
+  });
+}
+
+int sb_engine_prefill_partials(sb_engine* e, sb_model* m, const int32_t* handles, int32_t n, void* stream) {
+  return guard([&] {
+    SB_CUDA(cudaSetDevice(e->device));
+    int32_t nl = 0, hq = 0, hkv = 0;
+    sb_model_shape(m, &nl, &hq, &hkv);
+    if (nl != e->n_layers || hq != e->hq || hkv != e->hkv)
+      throw Error(SB_ERR_INVALID, "model shape differs from the engine's KV shape");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // per partial: tokens [cached, P) are computed, attending to [0, P)
+    std::vector<int64_t> pre, suf;
+    std::vector<int32_t> qo{0}, kl, table;
+    std::vector<uint64_t> toks;
+    int32_t max_blocks = 1, max_q = 0;
+    for (int i = 0; i < n; ++i) {
+      auto it = e->partials.find(handles[i]);
+      if (it == e->partials.end() || !it->second.live) throw Error(SB_ERR_INVALID, "stale continuation handle");
+      max_blocks = std::max<int32_t>(max_blocks, static_cast<int32_t>(it->second.ids.size()));
+    }
+    for (int i = 0; i < n; ++i) {
+      const PartialCall& pc = e->partials.find(handles[i])->second;
+      const int64_t P = static_cast<int64_t>(pc.tokens.size()), H = std::min(pc.cached, P);
+      pre.push_back(H);
+      suf.push_back(P - H);
+      toks.insert(toks.end(), pc.tokens.begin() + H, pc.tokens.end());
+      qo.push_back(qo.back() + static_cast<int32_t>(P - H));
+      kl.push_back(static_cast<int32_t>(P));
+      max_q = std::max<int32_t>(max_q, static_cast<int32_t>(P - H));
+      for (int32_t j = 0; j < max_blocks; ++j)
+        table.push_back(j < static_cast<int32_t>(pc.ids.size()) ? pc.ids[static_cast<size_t>(j)] : -1);
+    }
+    const int64_t T = qo.back();
+    if (T == 0) return int(SB_OK);
+    ModelWorkspace* mw = model_workspace_create(m, pre, suf);
+    uint64_t* d_tok = upload(toks);
+    int32_t *d_qo = upload(qo), *d_kl = upload(kl), *d_tb = upload(table), *d_work = nullptr;
+    int32_t n_work = 0;
+    try {
+      const int tpt = 128 / (e->hq / e->hkv);
+      int64_t cap_items = 0;
+      for (int i = 0; i < n; ++i) cap_items += (suf[static_cast<size_t>(i)] + 2 * tpt - 1) / (2 * tpt) * e->hkv;
+      std::vector<int32_t> work(static_cast<size_t>(2 * cap_items + 2));
+      int stt = sb_attention_work_list(qo.data(), kl.data(), n, e->hq, e->hkv, work.data(),
+                                       static_cast<int32_t>(cap_items + 1), &n_work);
+      if (stt) throw Error(stt, sb_last_error());
+      work.resize(static_cast<size_t>(2 * n_work));
+      d_work = upload(work);
+      const ModelIO io = model_io(mw);
+      const float scale = 1.f / std::sqrt(static_cast<float>(e->hd));
+      model_embed(m, mw, d_tok, st);
+      for (int l = 0; l < e->n_layers; ++l) {
+        model_layer_pre(m, mw, l, e->k_pools[l], e->v_pools[l], d_qo, d_kl, d_tb, n, max_blocks, st);
+        stt = sb_continuation_attention(io.q, e->k_pools[l], e->v_pools[l], io.a, d_qo, d_kl, d_tb, n, max_blocks,
+                                        max_q, static_cast<int32_t>(T), e->hq, e->hkv, e->hd, 16, e->cap, scale,
+                                        d_work, n_work, stream);
+        if (stt) throw Error(stt, sb_last_error());
+        model_layer_post(m, mw, l, st);
+      }
+      SB_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+      model_workspace_destroy(mw);
+      for (void* p : {static_cast<void*>(d_tok), static_cast<void*>(d_qo), static_cast<void*>(d_kl),
+                      static_cast<void*>(d_tb), static_cast<void*>(d_work)})
+        if (p) cudaFree(p);
+      throw;
+    }
+    model_workspace_destroy(mw);
+    for (void* p : {static_cast<void*>(d_tok), static_cast<void*>(d_qo), static_cast<void*>(d_kl),
+                    static_cast<void*>(d_tb), static_cast<void*>(d_work)})
+      if (p) cudaFree(p);
+    return int(SB_OK);
+  });
+}
+
+int sb_engine_partial_cached(sb_engine* e, int32_t handle, int64_t* cached_tokens) {
+  return guard([&] {
+    auto it = e->partials.find(handle);
+    if (it == e->partials.end()) throw Error(SB_ERR_INVALID, "unknown handle");
+    *cached_tokens = it->second.cached;
     return int(SB_OK);
   });
 }

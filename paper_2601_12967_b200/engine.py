@@ -169,6 +169,19 @@ class ContinuationEngine:
                                                     C.byref(n)))
         return PartialHandle(hid.value, t, list(tags), ids[: n.value].tolist())
 
+    def prefill_partials(self, handles: Sequence[PartialHandle], model: "DenseModel"):
+        """Run the model over the uncached part of each partial prefix (the
+        prefill that overlaps the tool call), writing its K/V into the pinned
+        pages (``sb_engine_prefill_partials``)."""
+        hid = np.array([h.call_id for h in handles], dtype=np.int32)
+        _lib.check(self._L.sb_engine_prefill_partials(self._h, model._h, hid.ctypes.data_as(_lib.I32P), len(hid),
+                                                      ContinuationBatch._stream()), "prefill_partials")
+
+    def cached_at_submit(self, handle: PartialHandle) -> int:
+        n = C.c_int64(0)
+        _lib.check(self._L.sb_engine_partial_cached(self._h, handle.call_id, C.byref(n)), "partial_cached")
+        return n.value
+
     def abandon_partial(self, handle: PartialHandle):
         _lib.check(self._L.sb_engine_abandon_partial(self._h, handle.call_id), "abandon_partial")
 

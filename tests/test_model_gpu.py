@@ -135,3 +135,95 @@ def test_dense_step_matches_torch_reference(prefix_lens, suffix_lens):
     for i in range(len(prefix_lens)):
         if (top2[i, 0] - top2[i, 1]).item() > 2 * tol:
             assert nxt[i] == int(ref[i].argmax()), i
+
+
+def _torch_forward_logits(tok_ids, W, emb, lm, fnorm, nl, hq, hkv, d, dff, theta):
+    """Monolithic fp32 forward (bf16 rounding where the device stores) of one
+    whole prompt: last-token logits."""
+    import torch
+    import torch.nn.functional as F
+
+    s = len(tok_ids)
+    x = emb[tok_ids]
+    pos = torch.arange(0, s, device="cuda")
+    mask = torch.arange(s, device="cuda")[None, :] > torch.arange(s, device="cuda")[:, None]
+    for l in range(nl):
+        xn = _bf(_rms(x, W[l, 4]))
+        qkv = _bf(xn @ W[l, 0].t()).reshape(s, hq + 2 * hkv, 128)
+        q = _bf(_rope(qkv[:, :hq], pos, theta))
+        k = _bf(_rope(qkv[:, hq:hq + hkv], pos, theta))
+        v = qkv[:, hq + hkv:]
+        K = k.permute(1, 0, 2).repeat_interleave(hq // hkv, 0)
+        V = v.permute(1, 0, 2).repeat_interleave(hq // hkv, 0)
+        sc = q.permute(1, 0, 2) @ K.transpose(1, 2) / math.sqrt(128)
+        a = _bf((torch.softmax(sc.masked_fill(mask, float("-inf")), -1) @ V).permute(1, 0, 2).reshape(s, d))
+        x = _bf(x + a @ W[l, 1].t())
+        xn = _bf(_rms(x, W[l, 5]))
+        gu = _bf(xn @ W[l, 2].t())
+        h = _bf(F.silu(gu[:, :dff]) * gu[:, dff:])
+        x = _bf(x + h @ W[l, 3].t())
+    return (_bf(_rms(x[-1:], fnorm)) @ lm.t())[0]
+
+
+@pytest.mark.gpu
+def test_split_prefill_equals_monolithic_prefill():
+    """Prompt splitting (paper §4.2) is exact: prefill the tool-independent
+    prefix (its uncached part, while the tool runs), then the continuation of
+    the tool output over the cached pages, gives the same last-token logits as
+    one prefill of the whole prompt.  Request B shares A's system prompt, so
+    its prefix prefill starts at A's cached blocks."""
+    import torch
+    from paper_2601_12967_b200.engine import ContinuationEngine, DenseModel, DenseShape, ModelShape
+
+    hq, hkv, d, dff, vocab, nl = 4, 2, 512, 1024, 1000, 2
+    ds = DenseShape(n_layers=nl, d_model=d, n_q_heads=hq, n_kv_heads=hkv, d_ff=dff, vocab=vocab, rope_theta=10000.0)
+    eng = ContinuationEngine(ModelShape(nl, hq, hkv, 128), 256, policy=1, seed=9)
+    model = DenseModel(ds, seed=4)
+    rng = np.random.default_rng(3)
+    system = rng.integers(0, 2**62, 64, dtype=np.int64).view(np.uint64)
+    pre_a = np.concatenate([system, rng.integers(0, 2**62, 96, dtype=np.int64).view(np.uint64)])
+    pre_b = np.concatenate([system, rng.integers(0, 2**62, 80, dtype=np.int64).view(np.uint64)])
+    ha = eng.submit_partial_prefill(pre_a, [(0, 64, 3), (64, 160, 2)], now=0)
+    hb = eng.submit_partial_prefill(pre_b, [(0, 64, 3), (64, 144, 2)], now=1)
+    assert eng.cached_at_submit(ha) == 0 and eng.cached_at_submit(hb) == 64
+    eng.prefill_partials([ha, hb], model)          # while the tools run
+    sfx = [37, 50]
+    batch = eng.make_batch([ha, hb], sfx)           # the tool outputs arrive
+    batch.set_model(model)
+    suffix = rng.integers(0, 2**62, sum(sfx), dtype=np.int64)
+    batch.stage_suffix_device(torch.from_numpy(suffix).cuda())
+    batch.run(now=5, seed=0)
+    _, logits = batch.model_result(logits=True)
+    assert (batch.results()[1] == 0).all()
+
+    W = {}
+    for l in range(nl):
+        for which, shp in ((0, ((hq + 2 * hkv) * 128, d)), (1, (d, d)), (2, (2 * dff, d)), (3, (d, dff)), (4, (d,)),
+                           (5, (d,))):
+            W[l, which] = _dev_tensor(*model.weight(l, which), shp)
+    emb = _dev_tensor(*model.weight(-1, 0), (vocab, d))
+    lm = _dev_tensor(*model.weight(-1, 1), (vocab, d))
+    fnorm = _dev_tensor(*model.weight(-1, 2), (d,))
+    refs = []
+    for pre, (o, n) in zip((pre_a, pre_b), ((0, sfx[0]), (sfx[0], sfx[1]))):
+        whole = np.concatenate([pre, suffix[o:o + n].view(np.uint64)])
+        ids = torch.from_numpy((whole % np.uint64(vocab)).astype(np.int64)).cuda()
+        refs.append(_torch_forward_logits(ids, W, emb, lm, fnorm, nl, hq, hkv, d, dff, ds.rope_theta))
+    ref = torch.stack(refs).cpu()
+    got = torch.from_numpy(logits)
+    tol = 2e-2 * ref.abs().max().item()
+    err = (got - ref).abs().max().item()
+    print(f"split vs monolithic prefill: max |logit err| {err:.3e} vs tol {tol:.3e}")
+    assert err <= tol, (err, tol)
+
+    # negative control: without the partial prefill the prefix pages hold the
+    # engine's stand-in KV, and the same check must fail
+    eng2 = ContinuationEngine(ModelShape(nl, hq, hkv, 128), 256, policy=1, seed=9)
+    h2 = [eng2.submit_partial_prefill(pre_a, [(0, 64, 3), (64, 160, 2)], now=0),
+          eng2.submit_partial_prefill(pre_b, [(0, 64, 3), (64, 144, 2)], now=1)]
+    b2 = eng2.make_batch(h2, sfx)
+    b2.set_model(model)
+    b2.stage_suffix_device(torch.from_numpy(suffix).cuda())
+    b2.run(now=5, seed=0)
+    _, lg2 = b2.model_result(logits=True)
+    assert (torch.from_numpy(lg2) - ref).abs().max().item() > tol
