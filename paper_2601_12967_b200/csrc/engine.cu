@@ -4,9 +4,12 @@
 //   Engine::extend_prefill + complete_prefill     engine.cpp:184-223, 305-322
 //   Engine::abandon_partial                       engine.cpp:234-248
 // where the reference only charges a prefill cost (engine.cpp:35-39), this
-// engine runs the continuation: chain hashes -> admission lookup -> insert
-// (hint-aware eviction) -> page table -> per layer {projection stand-in, KV
-// append, tcgen05 attention} -> release, all stream-ordered on one stream.
+// engine runs the computation: the partial prefill of a prefix's uncached
+// tokens (sb_engine_prefill_partials, while the tool runs) and the
+// continuation step: chain hashes -> admission lookup -> insert (hint-aware
+// eviction) -> page table -> per layer {KV append, tcgen05 attention} (or the
+// full dense layers with an attached model, csrc/model.cu) -> release, all
+// stream-ordered on one stream.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -157,7 +160,8 @@ int sb_engine_create(int32_t n_layers, int32_t n_q_heads, int32_t n_kv_heads, in
       for (int l = 0; l < n_layers; ++l) {
         e->k_pools.push_back(dmalloc<__nv_bfloat16>(elems));
         e->v_pools.push_back(dmalloc<__nv_bfloat16>(elems));
-        // stand-in for the KV written by the eager prefill of a random-init model
+        // seeded KV for pages never prefilled here (sb_engine_prefill_partials overwrites
+        // the pages of the prefixes it computes)
         st = sb_fill_random_bf16(e->k_pools.back(), elems, seed * 131 + 2 * l, 1.f, nullptr);
         if (!st) st = sb_fill_random_bf16(e->v_pools.back(), elems, seed * 131 + 2 * l + 1, 1.f, nullptr);
         if (st) throw Error(st, sb_last_error());
