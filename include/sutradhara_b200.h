@@ -152,6 +152,10 @@ int sb_kv_contains(const sb_kv_cache* cache, int32_t id);
 int sb_kv_resident_ids(const sb_kv_cache* cache, int32_t* out, int64_t* n_out);
 /* KvCache::block(id); tokens_out may be NULL, else holds block_size u64. */
 int sb_kv_block(const sb_kv_cache* cache, int32_t id, sb_block_info* info, uint64_t* tokens_out);
+/* Batched KvCache::contains / KvCache::block (kv_cache.hpp:106-107): one
+ * record per id in a single device round trip; a record with n_tokens == 0
+ * means the id is not resident (block() would throw for it). */
+int sb_kv_blocks(sb_kv_cache* cache, const int32_t* ids, int64_t n, sb_block_info* infos);
 /* KvCache::audit()                                kv_cache.cpp:242 */
 int sb_kv_audit(const sb_kv_cache* cache);
 /* KvCache::dump() — byte-identical text; *len receives the full length

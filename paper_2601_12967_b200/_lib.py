@@ -60,6 +60,7 @@ SIGNATURES = {
     "sb_kv_contains": (C.c_int, [VP, C.c_int32]),
     "sb_kv_resident_ids": (C.c_int, [VP, I32P, I64P]),
     "sb_kv_block": (C.c_int, [VP, C.c_int32, C.POINTER(BlockInfo), U64P]),
+    "sb_kv_blocks": (C.c_int, [VP, I32P, C.c_int64, C.POINTER(BlockInfo)]),
     "sb_kv_audit": (C.c_int, [VP]),
     "sb_kv_dump": (C.c_int, [VP, C.c_char_p, C.c_int64, I64P]),
     "sb_kv_lookup_prefix_batch": (C.c_int, [VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int64, VP, VP]),

@@ -1700,6 +1700,27 @@ __global__ void k_release_apply(Pool P, const int32_t* ids, int64_t n, const int
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     if (ids[i] >= 0) atomicSub(&P.ref[ids[i]], 1);
 }
+// Batched KvCache::block(id) read-back: one record per id, n_tokens == 0 for
+// an id that is out of range or not resident.
+__global__ void k_block_info(Pool P, const int32_t* ids, int64_t n, sb_block_info* out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t id = ids[i];
+    sb_block_info b{};
+    b.block_id = id;
+    if (id >= 0 && id < P.cap && P.ntok[id] > 0) {
+      b.tag = P.tag[id];
+      b.tier = tier_of(b.tag);
+      b.ref_count = P.ref[id];
+      b.last_used = P.last[id];
+      b.chain_hash = P.chain[id];
+      b.parent_hash = P.parent[id];
+      b.pinned = P.pinned[id];
+      b.n_tokens = P.ntok[id];
+    }
+    out[i] = b;
+  }
+}
 __global__ void k_touch_apply(Pool P, const int32_t* ids, int64_t n, int64_t now, const int64_t* scal) {
   const int64_t lim = min(n, scal[S_ERRIDX]);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < lim;
@@ -2406,24 +2427,37 @@ int sb_kv_resident_ids(const sb_kv_cache* c, int32_t* out, int64_t* n_out) {
 }
 
 int sb_kv_block(const sb_kv_cache* c, int32_t id, sb_block_info* info, uint64_t* tokens_out) {
+  // logical constness: the read-back only uses the pool's staging buffers
+  sb_kv_cache* m = const_cast<sb_kv_cache*>(c);
+  const int st = sb_kv_blocks(m, &id, 1, info);
+  if (st != SB_OK) return st;
   return guard([&] {
-    if (id < 0 || id >= c->P.cap || !sb_kv_contains(c, id)) {
+    if (info->n_tokens == 0) {
       set_last_error("block " + std::to_string(id) + " not resident");
       return int(SB_ERR_UNKNOWN_BLOCK);
     }
-    const Pool& P = c->P;
-    info->block_id = id;
-    SB_CUDA(cudaMemcpy(&info->tag, P.tag + id, 4, cudaMemcpyDeviceToHost));
-    SB_CUDA(cudaMemcpy(&info->ref_count, P.ref + id, 4, cudaMemcpyDeviceToHost));
-    SB_CUDA(cudaMemcpy(&info->pinned, P.pinned + id, 4, cudaMemcpyDeviceToHost));
-    SB_CUDA(cudaMemcpy(&info->n_tokens, P.ntok + id, 4, cudaMemcpyDeviceToHost));
-    SB_CUDA(cudaMemcpy(&info->last_used, P.last + id, 8, cudaMemcpyDeviceToHost));
-    SB_CUDA(cudaMemcpy(&info->chain_hash, P.chain + id, 8, cudaMemcpyDeviceToHost));
-    SB_CUDA(cudaMemcpy(&info->parent_hash, P.parent + id, 8, cudaMemcpyDeviceToHost));
-    info->tier = tier_of(info->tag);
     if (tokens_out)
-      SB_CUDA(cudaMemcpy(tokens_out, P.tok + int64_t(id) * P.bs, sizeof(uint64_t) * info->n_tokens,
+      SB_CUDA(cudaMemcpy(tokens_out, c->P.tok + int64_t(id) * c->P.bs, sizeof(uint64_t) * info->n_tokens,
                          cudaMemcpyDeviceToHost));
+    return int(SB_OK);
+  });
+}
+
+int sb_kv_blocks(sb_kv_cache* c, const int32_t* ids, int64_t n, sb_block_info* infos) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(c->mu);
+    SB_CUDA(cudaSetDevice(c->device));
+    if (n <= 0) return int(SB_OK);
+    c->ensure_ids(n);
+    // the token staging buffer holds the records (48 B = 6 u64 each)
+    static_assert(sizeof(sb_block_info) == 6 * sizeof(uint64_t), "sb_block_info layout");
+    c->ensure_tokens(6 * n);
+    sb_block_info* d_out = reinterpret_cast<sb_block_info*>(c->d_tok);
+    SB_CUDA(cudaMemcpyAsync(c->d_ids, ids, sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+    k_block_info<<<grid_for(n), 256, 0, c->stream>>>(c->P, c->d_ids, n, d_out);
+    SB_CHECK_LAUNCH();
+    SB_CUDA(cudaMemcpyAsync(infos, d_out, sizeof(sb_block_info) * n, cudaMemcpyDeviceToHost, c->stream));
+    SB_CUDA(cudaStreamSynchronize(c->stream));
     return int(SB_OK);
   });
 }

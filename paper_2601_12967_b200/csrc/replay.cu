@@ -589,13 +589,21 @@ struct Sim {
       return;
     }
     c.chain_refs = ids;
-    for (size_t i = 0; i < ids.size(); ++i) {
-      const int32_t id = ids[i];
-      if (pin_count[id]++ == 0) {
-        sb_block_info info;
-        Pool::ok(sb_kv_block(pool.c, id, &info, nullptr));
-        real_tag[id] = info.tag != SB_TAG_PARTIAL_PREFILL ? info.tag : tag_at(c, static_cast<int64_t>(i) * bs);
+    // first pins remember the block's real tag (one batched read-back)
+    std::vector<int32_t> first;
+    std::vector<size_t> pos;
+    for (size_t i = 0; i < ids.size(); ++i)
+      if (pin_count[ids[i]]++ == 0) {
+        first.push_back(ids[i]);
+        pos.push_back(i);
       }
+    std::vector<sb_block_info> info(first.size());
+    if (!first.empty())
+      Pool::ok(sb_kv_blocks(pool.c, first.data(), static_cast<int64_t>(first.size()), info.data()));
+    for (size_t k = 0; k < first.size(); ++k) {
+      if (info[k].n_tokens == 0) throw Error(SB_ERR_UNKNOWN_BLOCK, "pinned block not resident");
+      real_tag[first[k]] =
+          info[k].tag != SB_TAG_PARTIAL_PREFILL ? info[k].tag : tag_at(c, static_cast<int64_t>(pos[k]) * bs);
     }
     Pool::ok(sb_kv_set_reuse_priority(pool.c, ids.data(), static_cast<int64_t>(ids.size()), 1,
                                       SB_TAG_PARTIAL_PREFILL));
@@ -603,13 +611,20 @@ struct Sim {
     c.state = kAwaiting;
   }
   void release_pins(Call& c) {
-    std::vector<int32_t> unpin;
+    std::vector<int32_t> last, unpin;
     std::map<int32_t, std::vector<int32_t>> by_tag;
     for (int32_t id : c.pinned_ids) {
       auto it = pin_count.find(id);
       if (it == pin_count.end() || --it->second > 0) continue;
       pin_count.erase(it);
-      if (sb_kv_contains(pool.c, id)) {
+      last.push_back(id);
+    }
+    // residency of the blocks whose last pin goes (one batched read-back)
+    std::vector<sb_block_info> info(last.size());
+    if (!last.empty()) Pool::ok(sb_kv_blocks(pool.c, last.data(), static_cast<int64_t>(last.size()), info.data()));
+    for (size_t k = 0; k < last.size(); ++k) {
+      const int32_t id = last[k];
+      if (info[k].n_tokens > 0) {
         unpin.push_back(id);
         auto t = real_tag.find(id);
         if (t != real_tag.end()) by_tag[t->second].push_back(id);

@@ -158,6 +158,16 @@ class KvCache:
         return KvBlock(info.block_id, info.chain_hash, info.parent_hash, info.tag, info.tier, info.ref_count,
                        info.last_used, bool(info.pinned), toks[: info.n_tokens].copy())
 
+    def blocks(self, block_ids) -> list:
+        """Batched contains()/block() metadata: one device round trip; None
+        for an id that is not resident (block() would raise for it)."""
+        ids = np.ascontiguousarray(block_ids, dtype=np.int32)
+        infos = (_lib.BlockInfo * max(len(ids), 1))()
+        _lib.check(self._L.sb_kv_blocks(self._h, ids.ctypes.data_as(_lib.I32P), len(ids), infos), "blocks")
+        return [None if b.n_tokens == 0 else
+                KvBlock(b.block_id, b.chain_hash, b.parent_hash, b.tag, b.tier, b.ref_count, b.last_used,
+                        bool(b.pinned), None) for b in infos[: len(ids)]]
+
     def audit(self):
         _lib.check(self._L.sb_kv_audit(self._h), "audit")
 

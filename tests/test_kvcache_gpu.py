@@ -237,3 +237,30 @@ def test_time_range_guard():
             c.lookup_prefix(t, bad)
         with pytest.raises(errors.Unsupported):
             c.touch(ids, bad)
+
+
+@pytest.mark.gpu
+def test_batched_block_readback_matches_block():
+    """blocks(ids) (one round trip) == contains()/block() per id, including
+    out-of-range and evicted ids."""
+    from paper_2601_12967_b200.kv_cache import CacheConfig, KvCache
+
+    c = KvCache(CacheConfig(16, 96, 1))
+    ids = []
+    for k in range(6):
+        t = O.materialize(k % 4, 100 + 37 * k, k)
+        ids += list(c.insert(t, [(0, 50, k % 6), (50, len(t), (k + 2) % 6)], 10 + k))
+    c.set_reuse_priority(ids[:5], pinned=True, tier_override=4)
+    c.release(ids[5:20])
+    c.evict(4)
+    probe = list(range(-2, 99))
+    got = c.blocks(probe)
+    for i, b in zip(probe, got):
+        if not c.contains(i):
+            assert b is None, i
+            continue
+        ref = c.block(i)
+        assert b is not None
+        for f in ("block_id", "chain_hash", "parent_hash", "tag", "tier", "ref_count", "last_used", "pinned"):
+            assert getattr(b, f) == getattr(ref, f), (i, f)
+    assert c.blocks([]) == []
