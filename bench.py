@@ -83,7 +83,7 @@ class ClockSampler:
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.limit")
 
     def __init__(self, index: int):
         self.index = index
@@ -121,8 +121,15 @@ class ClockSampler:
             for k, nm in enumerate(names):
                 if len(r) > 5 + k and r[5 + k].lower().startswith("active"):
                     reasons.add(nm)
+        def num(i):
+            return [float(r[i]) for r in self.rows if len(r) > i and r[i].replace(".", "").isdigit()]
+
+        pw, lim = num(3), num(9)
+        # power.draw next to the board limit: the attention-dominated step runs
+        # at the power cap (sw_power_cap), i.e. energy per FLOP sets its speed
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w": statistics.median(pw) if pw else None, "power_limit_w": max(lim) if lim else None}
 
 
 def setup_workload(rank: int, n_req: int):

@@ -115,10 +115,11 @@ def lib():
     global _lib
     with _lock:
         if _lib is None:
-            if not os.path.exists(LIB_PATH):
-                raise RuntimeError(f"{LIB_PATH} missing — build it with `python -m paper_2601_12967_b200.build` "
+            path = os.environ.get("SB_LIB_PATH", LIB_PATH)  # A/B runs load an alternative build
+            if not os.path.exists(path):
+                raise RuntimeError(f"{path} missing — build it with `python -m paper_2601_12967_b200.build` "
                                    "(no CPU fallback exists)")
-            L = C.CDLL(LIB_PATH)
+            L = C.CDLL(path)
             for name, (res, args) in SIGNATURES.items():
                 fn = getattr(L, name)
                 fn.restype = res
