@@ -66,6 +66,10 @@ CASES = [
     ([130], [70], 2, 2),                      # MHA (group 1): 128 tokens per tile
     ([96, 200], [500, 33], 16, 8),            # group 2
     ([40, 17], [32768, 20000], 32, 8),        # configs[2]-long cached prefixes (2K+ pages per sequence)
+    ([50, 300], [1000, 16], 64, 8),           # group 8 (Llama-3-70B heads): 16 tokens per tile
+    ([20, 9], [77, 0], 16, 1),                # group 16
+    ([0, 45, 0], [100, 60, 7], 8, 2),         # sequences without suffix tokens in the batch
+    ([256], [256], 4, 4),                     # group 1, exactly one tile pair, block-aligned prefix
 ]
 
 
@@ -150,7 +154,8 @@ REL_TOL_F32 = 1e-5
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", [([64], [0], 4, 1), ([100, 37, 1], [300, 0, 1000], 8, 2), ([33], [2000], 2, 1)])
+@pytest.mark.parametrize("case", [([64], [0], 4, 1), ([100, 37, 1], [300, 0, 1000], 8, 2), ([33], [2000], 2, 1),
+                                  ([0, 50], [10, 300], 64, 8)])
 def test_continuation_attention_f32_matches_fp32(case):
     """fp32 contract (north star: 1e-5 in fp32), e.g. the toy 2-layer d=256
     model of configs[0] (2 q heads x 128)."""
