@@ -319,6 +319,11 @@ def run_ours(args, rank, world, local_rank):
                      "launches_timed": len(attn_ms)},
         "clocks": clk,
     }
+    pw, lim = clk.get("power_w"), clk.get("power_limit_w")
+    if pw and lim and "sw_power_cap" in clk.get("reasons", []) and pw >= 0.95 * lim:
+        # the step ran at the board power limit: energy per FLOP, not a pipe,
+        # sets the attention speed (profiles/README.md "Power")
+        line["roofline"]["limiter"] = f"board power cap ({pw:.0f} W of {lim:.0f} W, sw_power_cap)"
     if full_model is not None:
         line["full_model"] = full_model
     try:  # same attention problem through NVIDIA's trtllm-gen kernel (flashinfer cubin), as a reference point
