@@ -81,13 +81,16 @@ def timed(fn, reps=10, warm=3, kernels=(), flush=False):
     return api, dev
 
 
-def emit(kernel, config, bytes_, api_s, dev_s, hbm, launches=1):
+def emit(kernel, config, bytes_, api_s, dev_s, hbm, launches=1, parts=None):
     """frac uses the kernel's own device time when the profiler saw it."""
     sec = dev_s * launches if dev_s else api_s
     gbs = bytes_ / sec / 1e9
-    print(json.dumps({"kernel": kernel, "config": config, "seconds": sec, "api_seconds": api_s,
-                      "timing": "kernel (CUPTI)" if dev_s else "api (CUDA events)", "algorithmic_bytes": bytes_,
-                      "achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm}), flush=True)
+    row = {"kernel": kernel, "config": config, "seconds": sec, "api_seconds": api_s,
+           "timing": "kernel (CUPTI)" if dev_s else "api (CUDA events)", "algorithmic_bytes": bytes_,
+           "achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm}
+    if parts:
+        row["parts_us"] = {k: round(v * 1e6, 2) for k, v in parts.items() if v}
+    print(json.dumps(row), flush=True)
 
 
 def fill_pool(L, cache, dev, n_seqs, toks, st):
@@ -129,7 +132,8 @@ def evict_bench(L, cache, cap, hbm):
         # scoring: 24 B of metadata read per pool block (ntok/ref/pinned/tag + last) + one 8 B key per candidate
         emit("k_score (hint-aware eviction scoring)", cfg, cap * 24 + res * 8, api, kt.get("k_score"), hbm)
         tot = sum(kt.get(k, 0.0) for k in ("k_plan", "k_score", "k_select_coop"))
-        emit("evict total (k_plan + k_score + k_select_coop)", cfg, cap * 24 + res * 8, api, tot or None, hbm)
+        emit("evict total (k_plan + k_score + k_select_coop)", cfg, cap * 24 + res * 8, api, tot or None, hbm,
+             parts={k: kt.get(k) for k in ("k_plan", "k_score", "k_select_coop")})
 
 
 def main():

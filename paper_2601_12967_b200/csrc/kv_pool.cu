@@ -616,23 +616,77 @@ __device__ uint32_t block_scan_2048(uint32_t* hist, uint32_t* warp_sums) {
   return total;
 }
 
-// Bitonic sort of n (power of two) keys in shared memory.
+// Bitonic sort of n (power of two) keys in shared memory, block-wide.
+// Stages with a compare distance j >= 64 run over shared memory, indexed by
+// compare-exchange pair (q -> i = 2j*(q/j) + q%j, partner i + j) so every
+// thread works; the stages with j <= 32 of each merge run in registers: a
+// warp loads a 64-key segment (two keys per lane), does them with shuffles
+// (j = 32 inside the lane) and writes the segment back — one block barrier
+// per shared-memory stage and per register phase instead of one per stage.
+__device__ __forceinline__ uint64_t cx_keep(uint64_t v, uint64_t p, bool keep_min) {
+  return keep_min ? (v < p ? v : p) : (v > p ? v : p);
+}
+__device__ void bitonic_warp_stages(uint64_t* a, int n, int k_lo, int k_hi) {
+  // merges k_lo..k_hi (powers of two, k_hi <= 64 or k_lo == k_hi), stages j <= min(k/2, 32)
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int seg = (threadIdx.x >> 5) * 64; seg < n; seg += nw * 64) {
+    const int i0 = seg + lane, i1 = i0 + 32;
+    uint64_t v0 = a[i0], v1 = a[i1];
+    for (int k = k_lo; k <= k_hi; k <<= 1) {
+      for (int j = min(k >> 1, 32); j > 0; j >>= 1) {
+        const bool up0 = (i0 & k) == 0, up1 = (i1 & k) == 0;
+        if (j == 32) {  // both keys of the pair sit in this lane
+          const uint64_t lo = v0 < v1 ? v0 : v1, hi = v0 < v1 ? v1 : v0;
+          v0 = up0 ? lo : hi;
+          v1 = up0 ? hi : lo;
+        } else {
+          const bool lower = (lane & j) == 0;
+          const uint64_t p0 = __shfl_xor_sync(0xffffffffu, v0, j);
+          const uint64_t p1 = __shfl_xor_sync(0xffffffffu, v1, j);
+          v0 = cx_keep(v0, p0, lower == up0);
+          v1 = cx_keep(v1, p1, lower == up1);
+        }
+      }
+    }
+    a[i0] = v0;
+    a[i1] = v1;
+  }
+}
 __device__ void bitonic_smem(uint64_t* a, int n) {
-  for (int k = 2; k <= n; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
+  if (n < 64) {  // tiny: plain network
+    for (int k = 2; k <= n; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int q = threadIdx.x; q < (n >> 1); q += blockDim.x) {
+          const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1));
+          const int ixj = i | j;
           const uint64_t x = a[i], y = a[ixj];
-          const bool up = (i & k) == 0;
-          if ((x > y) == up) {
+          if ((x > y) == ((i & k) == 0)) {
             a[i] = y;
             a[ixj] = x;
           }
         }
+        __syncthreads();
+      }
+    return;
+  }
+  const int half = n >> 1;
+  bitonic_warp_stages(a, n, 2, 64);
+  __syncthreads();
+  for (int k = 128; k <= n; k <<= 1) {
+    for (int j = k >> 1; j >= 64; j >>= 1) {
+      for (int q = threadIdx.x; q < half; q += blockDim.x) {
+        const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1));
+        const int ixj = i | j;
+        const uint64_t x = a[i], y = a[ixj];
+        if ((x > y) == ((i & k) == 0)) {
+          a[i] = y;
+          a[ixj] = x;
+        }
       }
       __syncthreads();
     }
+    bitonic_warp_stages(a, n, k, k);
+    __syncthreads();
   }
 }
 
@@ -1255,7 +1309,14 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
         mn = min(mn, static_cast<unsigned long long>(G.kmin[i]));
         mx = max(mx, static_cast<unsigned long long>(G.kmax[i]));
       }
-    if (c) {
+    // warp reduction first: 64-bit shared atomics are CAS loops on sm_100a
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if ((t & 31) == 0 && c) {
       atomicAdd(&red[0], c);
       atomicMin(&red[1], mn);
       atomicMax(&red[2], mx);
@@ -1392,10 +1453,21 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
       if (done) break;
     }
   }
-  if (K > 0)
+  if (K > 0) {
+    // gather the selected keys: one global atomic per warp (ballot + popc)
+    const int lane = t & 31;
     for_keys([&](uint64_t k) {
-      if (K == ncand || (k & mask) <= prefix) S.sortbuf[atomicAdd(&G.ctr[1], 1ull)] = k;
+      const bool sel = K == ncand || (k & mask) <= prefix;
+      const unsigned am = __activemask();
+      const unsigned b = __ballot_sync(am, sel);
+      if (!b) return;
+      const int leader = __ffs(am) - 1;
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(&G.ctr[1], static_cast<unsigned long long>(__popc(b)));
+      base = __shfl_sync(am, base, leader);
+      if (sel) S.sortbuf[base + __popc(b & ((1u << lane) - 1u))] = k;
     });
+  }
   grid.sync();
   if (cta != 0) return;
   // ---- CTA 0: sort the K selected keys, publish them with their ranks
