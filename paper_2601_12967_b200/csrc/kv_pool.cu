@@ -1066,6 +1066,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
 struct CoopBuf {
   uint32_t* hist;            // [6][2048]
   unsigned long long* ctr;   // [0] candidates [1] selected [2] pre-hit candidates [3] min key [4] max key
+                             // [5] keys compacted from the chosen radix bin
   uint64_t* keys;            // candidate keys, slice sl at [sl * slice, + ncnt[sl])
   uint32_t* fcnt;            // free blocks per score slice, [n_slices]
   uint32_t* ncnt;            // candidates per score slice, [n_slices]
@@ -1093,7 +1094,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
   for (int i = t; i < 6 * 2048; i += blockDim.x) G.hist[i] = 0;
   if (t < 3) G.ctr[t] = 0;
   if (t == 3) G.ctr[3] = ~0ull;
-  if (t == 4) G.ctr[4] = 0;
+  if (t == 4 || t == 5) G.ctr[t] = 0;
   if (mode != 0) {
     if (t == 0) {
       S.scal[S_F] = 0;
@@ -1394,14 +1395,38 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
       nl += c;
     }
   }
+  // Large pools (keys read in place): after the first radix pass the keys of
+  // the chosen bin are compacted into S.keys (unused by this path) and the
+  // lower bins' keys go straight to the victim list, so the later passes and
+  // the final gather touch only the bin instead of every candidate.
+  bool compacted = false;
+  int64_t n_bin = 0;
   auto for_keys = [&](auto&& f) {
-    if (G.keys_in_smem) {
+    if (compacted) {
+      for (int64_t i = static_cast<int64_t>(cta) * blockDim.x + t; i < n_bin;
+           i += static_cast<int64_t>(n_cta) * blockDim.x)
+        f(S.keys[i]);
+    } else if (G.keys_in_smem) {
       for (int64_t i = t; i < nl; i += blockDim.x) f(local_keys[i]);
     } else {
+      // in place (L2/HBM): eight loads in flight per thread before the
+      // keys are consumed, so a pass streams instead of waiting one load
+      // latency per key
+      constexpr int kU = 8;
       for (int sl = cta; sl < G.n_slices; sl += n_cta) {
         const int64_t c = G.ncnt[sl];
         const uint64_t* src = G.keys + sl * G.slice;
-        for (int64_t i = t; i < c; i += blockDim.x) f(src[i]);
+        for (int64_t i0 = t; i0 < c; i0 += kU * static_cast<int64_t>(blockDim.x)) {
+          uint64_t v[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int64_t i = i0 + static_cast<int64_t>(u) * blockDim.x;
+            v[u] = i < c ? __ldcg(src + i) : 0;
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u)
+            if (i0 + static_cast<int64_t>(u) * blockDim.x < c) f(v[u]);
+        }
       }
     }
   };
@@ -1451,10 +1476,32 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
       const bool done = static_cast<int64_t>(cnt_b) == need;
       __syncthreads();
       if (done) break;
+      if (!G.keys_in_smem && !compacted && hi_bit > 0) {
+        const int lane = t & 31;
+        auto append = [&](bool take, uint64_t k, unsigned long long* ctr, uint64_t* dst) {
+          const unsigned am = __activemask();
+          const unsigned b = __ballot_sync(am, take);
+          if (!b) return;
+          const int leader = __ffs(am) - 1;
+          unsigned long long base = 0;
+          if (lane == leader) base = atomicAdd(ctr, static_cast<unsigned long long>(__popc(b)));
+          base = __shfl_sync(am, base, leader);
+          if (take) dst[base + __popc(b & ((1u << lane) - 1u))] = k;
+        };
+        for_keys([&](uint64_t k) {
+          const uint64_t km = k & mask;
+          append(km < prefix, k, &G.ctr[1], S.sortbuf);  // lower bins: selected
+          append(km == prefix, k, &G.ctr[5], S.keys);    // the chosen bin
+        });
+        grid.sync();
+        n_bin = static_cast<int64_t>(*reinterpret_cast<volatile unsigned long long*>(&G.ctr[5]));
+        compacted = true;
+      }
     }
   }
   if (K > 0) {
-    // gather the selected keys: one global atomic per warp (ballot + popc)
+    // gather the selected keys (after a compaction only the chosen bin's:
+    // the lower bins are listed already): one global atomic per warp
     const int lane = t & 31;
     for_keys([&](uint64_t k) {
       const bool sel = K == ncand || (k & mask) <= prefix;
