@@ -626,15 +626,17 @@ __device__ uint32_t block_scan_2048(uint32_t* hist, uint32_t* warp_sums) {
 __device__ __forceinline__ uint64_t cx_keep(uint64_t v, uint64_t p, bool keep_min) {
   return keep_min ? (v < p ? v : p) : (v > p ? v : p);
 }
-__device__ void bitonic_warp_stages(uint64_t* a, int n, int k_lo, int k_hi) {
-  // merges k_lo..k_hi (powers of two, k_hi <= 64 or k_lo == k_hi), stages j <= min(k/2, 32)
+__device__ void bitonic_warp_stages(uint64_t* a, int n, int k_lo, int k_hi, bool all_ascending = false) {
+  // merges k_lo..k_hi (powers of two, k_hi <= 64 or k_lo == k_hi), stages j <= min(k/2, 32);
+  // all_ascending: the k = 64 merge sorts every 64-key segment ascending
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int seg = (threadIdx.x >> 5) * 64; seg < n; seg += nw * 64) {
     const int i0 = seg + lane, i1 = i0 + 32;
     uint64_t v0 = a[i0], v1 = a[i1];
     for (int k = k_lo; k <= k_hi; k <<= 1) {
       for (int j = min(k >> 1, 32); j > 0; j >>= 1) {
-        const bool up0 = (i0 & k) == 0, up1 = (i1 & k) == 0;
+        const bool asc = all_ascending && k == 64;
+        const bool up0 = asc || (i0 & k) == 0, up1 = asc || (i1 & k) == 0;
         if (j == 32) {  // both keys of the pair sit in this lane
           const uint64_t lo = v0 < v1 ? v0 : v1, hi = v0 < v1 ? v1 : v0;
           v0 = up0 ? lo : hi;
@@ -688,6 +690,42 @@ __device__ void bitonic_smem(uint64_t* a, int n) {
     bitonic_warp_stages(a, n, k, k);
     __syncthreads();
   }
+}
+
+// Merge sort of n keys (power of two, 128 <= n, 2n keys of shared memory):
+// 64-key segments sorted ascending per warp in registers, then merge passes
+// in which each thread emits n / blockDim.x consecutive outputs of a merged
+// run, located by a merge-path binary search (A before B on ties).  Every
+// pass moves the keys through shared memory once — the bitonic network moves
+// them once per stage.  Returns the buffer holding the sorted keys.
+__device__ uint64_t* merge_sort_smem(uint64_t* a, uint64_t* tmp, int n) {
+  bitonic_warp_stages(a, n, 2, 64, true);
+  __syncthreads();
+  const int per = max(1, n / static_cast<int>(blockDim.x));
+  uint64_t *src = a, *dst = tmp;
+  for (int w = 64; w < n; w <<= 1) {
+    for (int o = threadIdx.x * per; o < n; o += blockDim.x * per) {
+      const int base = o & ~(2 * w - 1), d = o - base;
+      const uint64_t* A = src + base;
+      const uint64_t* B = A + w;
+      int lo = max(0, d - w), hi = min(d, w);
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (A[mid] <= B[d - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+      }
+      int ia = lo, ib = d - lo;
+      for (int e = 0; e < per; ++e) {
+        const bool take_a = ib >= w || (ia < w && A[ia] <= B[ib]);
+        dst[base + d + e] = take_a ? A[ia++] : B[ib++];
+      }
+    }
+    __syncthreads();
+    uint64_t* t = src;
+    src = dst;
+    dst = t;
+  }
+  return src;
 }
 
 // Same network in global memory (fallback for very large victim lists).
@@ -1526,8 +1564,12 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
     if (in_smem) {
       for (int64_t i = t; i < n2; i += blockDim.x) local_keys[i] = i < K ? S.sortbuf[i] : kNoKey;
       __syncthreads();
-      bitonic_smem(local_keys, static_cast<int>(n2));
-      dst = local_keys;
+      if (n2 >= 1024 && 2 * n2 <= kSortSmemKeys) {  // merge sort (faster from 1K keys), scratch after the keys
+        dst = merge_sort_smem(local_keys, local_keys + n2, static_cast<int>(n2));
+      } else {
+        bitonic_smem(local_keys, static_cast<int>(n2));
+        dst = local_keys;
+      }
     } else {
       for (int64_t i = K + t; i < n2; i += blockDim.x) S.sortbuf[i] = kNoKey;
       __syncthreads();
