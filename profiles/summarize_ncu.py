@@ -2,7 +2,9 @@
 <name>_details.csv (the details page) and <name>_metrics.json (duration,
 DRAM bytes, pipe utilisation, occupancy, top stall reasons).
 
-    python profiles/summarize_ncu.py gpurun_out/x.ncu-rep profiles/r01/x
+    python profiles/summarize_ncu.py gpurun_out/x.ncu-rep profiles/r01/x [launch index]
+
+The launch index selects one kernel of a multi-kernel report (default 0).
 """
 import csv
 import io
@@ -23,12 +25,12 @@ KEYS = [
 ]
 
 
-def main(rep, out):
+def main(rep, out, idx=0):
     det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     open(out + "_details.csv", "w").write(det)
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    h, u, v = rows[0], rows[1], rows[2]
+    h, u, v = rows[0], rows[1], rows[2 + idx]
     m = {"kernel": v[h.index("Kernel Name")]}
     for k in KEYS:
         if k in h:
@@ -47,4 +49,4 @@ def main(rep, out):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 0)
