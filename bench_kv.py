@@ -144,7 +144,7 @@ def main():
     from paper_2601_12967_b200.kv_cache import CacheConfig, KvCache
 
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="hash,probe,probe_big,evict,evict_big,append")
+    ap.add_argument("--only", default="hash,probe,probe_big,evict_small,evict,evict_big,append")
     only = set(ap.parse_args().only.split(","))
     L = _lib.lib()
     hbm = float(peaks()["hbm_gbs"])
@@ -170,6 +170,11 @@ def main():
     if "probe_big" in only:
         probe_bench(L, dev, st, hbm, 1 << 22, 4096, 8192, evict=False)
     # ---- eviction at pool scale: evict() = k_plan + k_score (HBM pass) + k_select_coop
+    if "evict_small" in only:  # the engine step's pool size class (27K blocks)
+        cache3 = KvCache(CacheConfig(16, 1 << 15, 1))
+        fill_pool(L, cache3, dev, 28, 16384, st)
+        evict_bench(L, cache3, 1 << 15, hbm)
+        del cache3
     for big, n_fill in ((1 << 22, 2048), (1 << 24, 8192)):
         if ("evict" if big == 1 << 22 else "evict_big") in only:
             cache2 = KvCache(CacheConfig(16, big, 1))
