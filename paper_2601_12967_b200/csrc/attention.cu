@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < 2 * n_kv; ++i) {
         const int j = i >> 1, which = i & 1, stage = i % kStages;
         if (which == 0 && j + 1 < n_kv) fetch_rows(j + 1, next_rows);  // page ids one tile ahead
-        mbar_wait(&ss.kv_empty[stage], ((i / kStages) & 1) ^ 1);
+        mbar_wait_suspend(&ss.kv_empty[stage], ((i / kStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&ss.kv_full[stage], kTileBytes);
         uint8_t* dst = sKV + stage * kTileBytes;
         const void* tm = which ? static_cast<const void*>(&tm_v) : static_cast<const void*>(&tm_k);
@@ -219,8 +219,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
       const uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
       const uint32_t sq = smem_u32(sQ), skv = smem_u32(sKV);
-      mbar_wait(&ss.q_full, 0);
-      auto wait_stage = [&](int i) { mbar_wait(&ss.kv_full[i % kStages], (i / kStages) & 1); };
+      mbar_wait_suspend(&ss.q_full, 0);
+      auto wait_stage = [&](int i) { mbar_wait_suspend(&ss.kv_full[i % kStages], (i / kStages) & 1); };
       auto qk = [&](int t, int j) {
         const uint32_t kb = skv + ((2 * j) % kStages) * kTileBytes;
         const uint32_t qb = sq + t * kTileBytes;
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t vb = skv + ((2 * j + 1) % kStages) * kTileBytes;
 #pragma unroll
         for (int part = 0; part < kPSplit; ++part) {
-          mbar_wait(&ss.p_part[t][part], j & 1);
+          mbar_wait_suspend(&ss.p_part[t][part], j & 1);
           tc_fence_after();
 #pragma unroll
           for (int kk = part * (8 / kPSplit); kk < (part + 1) * (8 / kPSplit); ++kk)
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int qpos = prefix + qidx;  // absolute key position of this query
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kv; ++j) {
-      mbar_wait(&ss.s_full[t], j & 1);
+      mbar_wait_suspend(&ss.s_full[t], j & 1);
       tc_fence_after();
       // raw scores: four TMEM loads in flight, one wait
       uint32_t sv[128];
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (j > 0 && __any_sync(0xffffffffu, need)) {
         // rescale this warp's rows of O in TMEM once PV_{j-1} has landed
-        mbar_wait(&ss.o_done[t], (j - 1) & 1);
+        mbar_wait_suspend(&ss.o_done[t], (j - 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       l += acc[0] + acc[1];
     }
     // ---- epilogue: O / l -> bf16 -> global
-    mbar_wait(&ss.o_done[t], (n_kv - 1) & 1);
+    mbar_wait_suspend(&ss.o_done[t], (n_kv - 1) & 1);
     tc_fence_after();
     const bool valid = qidx < q_len;
     const float inv = (valid && l > 0.f) ? 1.f / l : 0.f;

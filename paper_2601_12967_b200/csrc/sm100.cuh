@@ -42,6 +42,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Same wait with a suspend-time hint: the warp stays suspended in hardware
+// until the phase completes (or the hint, in ns, expires) instead of
+// re-issuing try_wait — fewer spin instructions on long waits.
+__device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+        : "memory");
+  } while (!ok);
+}
 
 // ----------------------------------------------------------------------- TMA
 // 1-D bulk copy global -> shared (16 B aligned, bytes % 16 == 0), completion
