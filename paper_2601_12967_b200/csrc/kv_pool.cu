@@ -1240,7 +1240,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) k_score(Pool P, Scratch S, C
     int64_t lo, n;
     range(c, lo, n);
     const int sl = slice_of(static_cast<int>(c / chunks_per_slice));
-    mbar_wait(&full[c % kScoreStages], static_cast<uint32_t>((c / kScoreStages) & 1));
+    mbar_wait_suspend(&full[c % kScoreStages], static_cast<uint32_t>((c / kScoreStages) & 1));
     const uint8_t* st = stage_mem + (c % kScoreStages) * kScoreStageBytes;
     // thread t scores blocks 4t .. 4t+3 of the chunk: 16 B shared loads
     const int i0 = 4 * t;
