@@ -73,3 +73,23 @@ def test_trace_stats_gather_world2():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res[0][1] == res[1][1] == [[0.0, 1.0, 2.0, 3.0, 4.0], [10.0, 11.0, 12.0, 13.0, 14.0]]
+
+
+def test_clock_sampler_parses_power_and_reasons():
+    """nvidia-smi rows -> median SM clock, power draw and limit, the throttle
+    reasons the timing rules reject or note (no GPU needed)."""
+    s = bench.ClockSampler(0)
+    s.proc = type("P", (), {"terminate": lambda self: None, "wait": lambda self, timeout=None: 0})()
+    # index, clocks.sm, clocks.max.sm, power.draw, active, hw_slow, hw_thermal, sw_thermal, sw_power_cap, power.limit
+    s.rows = [["0", "1520", "1965", "990.5", "0x4", "Not Active", "Not Active", "Not Active", "Active", "1000.00"],
+              ["0", "1540", "1965", "985.0", "0x4", "Not Active", "Not Active", "Not Active", "Active", "1000.00"],
+              ["0", "1530", "1965", "995.0", "0x0", "Not Active", "Not Active", "Not Active", "Not Active", "1000.00"]]
+    import time as _t
+    sleep, _t.sleep = _t.sleep, lambda x: None
+    try:
+        c = s.stop()
+    finally:
+        _t.sleep = sleep
+    assert c["sm_mhz"] == 1530.0 and c["sm_max_mhz"] == 1965.0 and c["samples"] == 3
+    assert c["power_w"] == 990.5 and c["power_limit_w"] == 1000.0
+    assert c["reasons"] == ["sw_power_cap"]
