@@ -140,9 +140,11 @@ def setup_workload(rank: int, n_req: int):
 
 
 def capacity_for(reqs, bs=16, slack=1.25):
+    """Pool size for a step: every prefix block, plus `slack` x the blocks a
+    step adds (tool outputs + one response block per call)."""
     sys_blocks = 2048 // bs
     prefix_blocks = sum(r.prefix_len // bs for r in reqs) - (len(reqs) - 1) * sys_blocks
-    suffix_blocks = sum((r.suffix_len + bs - 1) // bs for r in reqs)
+    suffix_blocks = sum((r.suffix_len + bs - 1) // bs for r in reqs) + len(reqs)
     return prefix_blocks, suffix_blocks, prefix_blocks + int(slack * suffix_blocks) + 1
 
 
@@ -186,9 +188,8 @@ def run_ours(args, rank, world, local_rank):
     reqs = setup_workload(rank, args.requests)
     pre_b, suf_b, cap = capacity_for(reqs)
     eng = ContinuationEngine(LLAMA3_8B, cap, TIERED, device=local_rank, seed=rank)
-    handles = [eng.submit_partial_prefill(r.prefix_tokens, r.prefix_tags, now=0) for r in reqs]
-    assert eng.cache.resident_blocks() == pre_b, (eng.cache.resident_blocks(), pre_b)
-    batch = eng.make_batch(handles, [r.suffix_len for r in reqs])
+    batch = eng.make_batch([r.prefix_tokens for r in reqs], [r.prefix_tags for r in reqs],
+                           [r.suffix_len for r in reqs])
     n_steps = args.warmup + 2 * args.steps
     suffix_host = []
     for s in range(n_steps):
@@ -363,7 +364,10 @@ def run_dense(args, rank, world, local_rank):
     pre_b, suf_b, cap = capacity_for(reqs, slack=2.5)
     eng = ContinuationEngine(LLAMA3_8B, cap, TIERED, device=local_rank, seed=rank)
     model = DenseModel(LLAMA3_8B_DENSE, seed=rank, device=local_rank)
-    handles = [eng.submit_partial_prefill(r.prefix_tokens, r.prefix_tags, now=0) for r in reqs]
+    handles = []
+    for r in reqs:  # the partial calls; their prefix pages are admitted (pinned) when their prefill is done
+        handles.append(eng.submit_partial_prefill(r.prefix_tokens, r.prefix_tags, now=0))
+        assert eng.prefill_done(handles[-1], now=0) == eng.PINNED
     # the tool-independent prefixes are prefilled through the model (the work
     # prompt splitting hides behind the tool calls), timed once
     pe0, pe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -374,7 +378,8 @@ def run_dense(args, rank, world, local_rank):
     torch.cuda.synchronize()
     prefix_ms = pe0.elapsed_time(pe1)
     prefix_tokens = sum(r.prefix_len - eng.cached_at_submit(h) for r, h in zip(reqs, handles))
-    batch = eng.make_batch(handles, [r.suffix_len for r in reqs])
+    batch = eng.make_batch([r.prefix_tokens for r in reqs], [r.prefix_tags for r in reqs],
+                           [r.suffix_len for r in reqs])
     batch.set_model(model)
     steps, warm = max(2, args.steps), max(3, args.warmup)
     host = [torch.from_numpy(np.concatenate([W.fresh_suffix_tokens(r, s) for r in reqs]).view(np.int64)).pin_memory()

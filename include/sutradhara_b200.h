@@ -32,7 +32,10 @@ enum {
   SB_ERR_CONFIG = 5,           /* ConfigError      common.hpp:25  */
   SB_ERR_CUDA = 6,             /* CUDA runtime / launch failure   */
   SB_ERR_INVALID = 7,          /* bad argument to this C-ABI      */
-  SB_ERR_UNSUPPORTED = 8       /* shape/config outside the kernels' range */
+  SB_ERR_UNSUPPORTED = 8,      /* shape/config outside the kernels' range */
+  SB_ERR_STALE_HANDLE = 9,     /* StaleHandle      common.hpp:102 */
+  SB_ERR_INVALID_STATE = 10,   /* InvalidState     common.hpp:107 */
+  SB_ERR_UNKNOWN_CALL = 11     /* UnknownCall      common.hpp:112 */
 };
 
 /* ---- semantic tags (order == agentsim::KvTag, kv_cache.hpp:21-28) ---- */
@@ -281,36 +284,84 @@ void sb_engine_destroy(sb_engine* engine);
 sb_kv_cache* sb_engine_cache(sb_engine* engine);
 void* sb_engine_k_pool(sb_engine* engine, int32_t layer);
 void* sb_engine_v_pool(sb_engine* engine, int32_t layer);
-/* Engine::submit_partial_prefill + pin_partial (engine.cpp:153-182, 250-286):
- * insert the tool-independent prefix and pin it at PARTIAL_PREFILL. */
+/* Engine lifecycle, one call at a time (engine.hpp:104-111, engine.cpp).
+ * Calls are engine-owned records; each KV transition is one op of the pool's
+ * op program, with the reference's exact block-pool effects.  All run on the
+ * pool's stream and return when done.  Errors mirror the reference's
+ * exceptions: SB_ERR_STALE_HANDLE, SB_ERR_INVALID_STATE, SB_ERR_UNKNOWN_CALL.
+ *
+ * Engine::submit_call (engine.cpp:128-151): admission lookup_prefix at now. */
+int sb_engine_submit_call(sb_engine* engine, const uint64_t* tokens, int64_t n,
+                          const sb_tag_range* tags, int64_t n_tags, int64_t decode_length,
+                          int64_t now, int32_t* call);
+/* Engine::submit_partial_prefill (engine.cpp:153-182): admission lookup of the
+ * tool-independent prefix; returns the continuation handle (= call id). */
 int sb_engine_submit_partial(sb_engine* engine, const uint64_t* tokens, int64_t n,
                              const sb_tag_range* tags, int64_t n_tags, int64_t now,
                              int32_t* handle);
-/* Engine::abandon_partial (engine.cpp:234-248): unpin and drop the refs. */
+/* The call's prefill finished (Engine::complete_prefill, engine.cpp:305-322):
+ * a partial not yet extended is pinned (pin_partial, engine.cpp:250-286:
+ * insert at PARTIAL_PREFILL, pin counts, remembered real tags) -> outcome 1,
+ * or fails to pin (CacheFull, the call is aborted) -> outcome 2; otherwise the
+ * prompt is inserted with its tags (CacheFull: proceed uncached), the partial
+ * pins released (engine.cpp:288-303) and the old refs dropped -> outcome 3. */
+int sb_engine_prefill_done(sb_engine* engine, int32_t call, int64_t now, int32_t* outcome);
+/* Engine::extend_prefill (engine.cpp:184-223).  *completed = 1 when an empty
+ * suffix completed the prefill at once. */
+int sb_engine_extend(sb_engine* engine, int32_t handle, const uint64_t* suffix, int64_t n,
+                     const sb_tag_range* tags, int64_t n_tags, int64_t decode_length, int64_t now,
+                     int32_t* completed);
+/* Engine::abandon_partial (engine.cpp:234-248): release pins (restoring real
+ * tags), drop the chain refs. */
 int sb_engine_abandon_partial(sb_engine* engine, int32_t handle);
+/* Engine::finish_decode (engine.cpp:324-347): insert prompt + response
+ * (RESPONSE tag), release it, release the chain refs. */
+int sb_engine_finish(sb_engine* engine, int32_t call, const uint64_t* response, int64_t n_response,
+                     int64_t now);
+/* CallRecord view: state (agentsim::CallState order), cached prefix at
+ * admission, prompt tokens, chain refs held, partial pins held. */
+int sb_engine_call_info(sb_engine* engine, int32_t call, int32_t* state, int64_t* cached_prefix,
+                        int64_t* prompt_tokens, int32_t* n_chain, int32_t* n_pinned);
+/* which = 0: the chain refs; 1: the partial-prefill pins. */
+int sb_engine_call_blocks(sb_engine* engine, int32_t call, int32_t which, int32_t* out, int64_t cap,
+                          int64_t* n_out);
 int sb_engine_partial_blocks(sb_engine* engine, int32_t handle, int32_t* out, int64_t cap,
                              int64_t* n_out);
-/* A batch of extend_prefill continuations (engine.cpp:184-223) with fixed
- * suffix (tool-output) lengths. */
-int sb_batch_create(sb_engine* engine, const int32_t* handles, const int64_t* suffix_lens,
-                    int32_t n, sb_batch** out);
+
+/* ---- the batched engine step ------------------------------------------
+ * n continuations per step, slot i with a fixed tool-independent prefix
+ * (tokens prefix_tokens[prefix_off[i] .. prefix_off[i+1]), tags
+ * prefix_tags[tag_off[i] .. tag_off[i+1]) in prefix-local positions) and a
+ * fixed tool-output length.  One sb_batch_run is the engine-side lifecycle of
+ * n new calls at `now`, each transition for all n calls as one op program
+ * (same semantics as the per-call API applied in slot order):
+ *   submit_partial_prefill (prefix hashes + admission lookups) -> pin_partial
+ *   -> extend_prefill (the staged tool-output tokens, suffix-only hashing)
+ *   -> complete_prefill (insert with hint-aware eviction, release pins and
+ *   partial refs) -> per layer {KV append, continuation attention} (or the
+ *   dense model) -> finish_decode with one response token (the model's greedy
+ *   token, else decode_token(stream_keys[i], 0)).
+ * Without an attached model the per-layer q / k / v are seeded stand-ins
+ * generated once at batch creation (the dense layers are sb_batch_set_model). */
+int sb_batch_create(sb_engine* engine, int32_t n, const uint64_t* prefix_tokens,
+                    const int64_t* prefix_off, const sb_tag_range* prefix_tags,
+                    const int64_t* tag_off, const int64_t* suffix_lens,
+                    const uint64_t* stream_keys, sb_batch** out);
 void sb_batch_destroy(sb_batch* batch);
-/* This step's suffix tokens, packed in batch order (host or device array). */
+/* This step's tool-output tokens, packed in slot order (host or device array). */
 int sb_batch_stage_suffix(sb_batch* batch, const uint64_t* tokens, int32_t on_device,
                           void* stream);
-/* One continuation-prefill step: chain hashes (the pinned prefix's hashes are
- * gathered from the pool, only the suffix is folded), admission lookup,
- * insert with hint-aware eviction (Engine::complete_prefill,
- * engine.cpp:305-322), page table, then per layer {KV append, attention} and
- * the release of the call's block references (engine.cpp:343-346).  Without
- * an attached model the per-layer q / k / v are seeded stand-ins generated
- * once at batch creation (the dense layers are `sb_batch_set_model`). */
 int sb_batch_run(sb_batch* batch, int64_t now, uint64_t seed, int32_t time_attention,
                  void* stream, int32_t* launches);
 /* Per-layer attention times of the last timed run (ms, n_layers floats). */
 int sb_batch_attention_ms(sb_batch* batch, float* out);
+/* Last step: admission-lookup hits (tokens per call), complete_prefill
+ * statuses, and the chains the continuation attended over (ceil(full/16)
+ * ids per call, packed). */
 int sb_batch_results(sb_batch* batch, int64_t* hits, int32_t* status, int32_t* block_ids,
                      void* stream);
+/* Last step's pin_partial outcomes (1 pinned, 2 pin failed). */
+int sb_batch_pin_outcomes(sb_batch* batch, int32_t* outcomes);
 /* Async D2H of query rows [first_row, first_row+n_rows) of the last layer's
  * attention output (bf16) into host_dst. */
 int sb_batch_copy_output(sb_batch* batch, int64_t first_row, int64_t n_rows, void* host_dst,
@@ -344,10 +395,10 @@ int sb_model_weight(sb_model* model, int32_t layer, int32_t which, void** ptr, i
 int sb_batch_set_model(sb_batch* batch, sb_model* model);
 /* The partial prefill itself (paper §4.2: the tool-independent prompt is
  * prefilled while the tool runs; Engine::start_step charges it,
- * engine.cpp:424-427): for each partial call, the prefix tokens not cached at
- * submit (sb_engine_submit_partial records the admission lookup,
- * engine.cpp:170) run through the model, their K/V written into the call's
- * pinned pages.  A later continuation batch then attends over a prefix whose
+ * engine.cpp:424-427): for each pinned partial call (sb_engine_prefill_done
+ * allocated its pages), the prefix tokens not cached at submit (the
+ * admission lookup, engine.cpp:170) run through the model, their K/V written
+ * into the call's pinned pages.  A later continuation batch then attends over a prefix whose
  * KV is the model's own. */
 int sb_engine_prefill_partials(sb_engine* engine, sb_model* model, const int32_t* handles, int32_t n,
                                void* stream);

@@ -190,6 +190,20 @@ def main():
     with open(os.path.join(OUT, "manifest.json"), "w") as f:
         json.dump(manifest, f, indent=1)
     print(json.dumps(manifest, indent=1))
+    engine_events()
+
+
+def engine_events():
+    """Golden engine event lists: the reference engine (oracle/ref_engine.cpp)
+    driven by the scripts of tests/engine_scripts.py."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(HERE))
+    from tests import engine_scripts as S
+
+    for name, mk in S.SCRIPTS.items():
+        ev, _, _ = S.run_reference(mk())
+        write_gz(f"engine_{name}.jsonl.gz", "\n".join(json.dumps(e) for e in ev) + "\n")
 
 
 if __name__ == "__main__":

@@ -394,6 +394,16 @@ class RefCache:
     def contains(self, block_id):
         return bool(self.L.ref_kv_contains(self._h, block_id))
 
+    def block(self, block_id):
+        f = np.zeros(6, np.int64)
+        h = np.zeros(2, np.uint64)
+        toks = np.zeros(self.block_size, np.uint64)
+        st = self.L.ref_kv_block(self._h, block_id, _i64(f), _u64(h), _u64(toks))
+        if st:
+            return st, None
+        return 0, dict(tag=int(f[0]), tier=int(f[1]), ref=int(f[2]), pinned=int(f[3]), ntok=int(f[4]),
+                       last=int(f[5]), chain=int(h[0]), parent=int(h[1]), tokens=toks[: int(f[4])].copy())
+
     def dump(self):
         n = self.L.ref_kv_dump(self._h, None, 0)
         buf = C.create_string_buffer(int(n) + 1)
@@ -449,3 +459,136 @@ def kvlog_thrashing(tiered: int) -> Tuple[List[int], str]:
     if st:
         raise RuntimeError("thrashing scenario failed")
     return hits.tolist(), _drain_kvlog(L)
+
+
+# ------------------------------------------------- reference engine (scripted)
+def _declare_refeng(L):
+    L.refeng_last_error.restype = C.c_char_p
+    L.refeng_create.restype = C.c_void_p
+    L.refeng_create.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
+    L.refeng_destroy.argtypes = [C.c_void_p]
+    L.refeng_now.restype = C.c_int64
+    L.refeng_now.argtypes = [C.c_void_p]
+    L.refeng_submit_call.argtypes = [C.c_void_p, U64P, C.c_int64, I64P, C.c_int64, C.c_int64, C.c_uint64, I64P]
+    L.refeng_submit_partial.argtypes = [C.c_void_p, U64P, C.c_int64, I64P, C.c_int64, C.c_uint64, I64P]
+    L.refeng_extend.argtypes = [C.c_void_p, C.c_int64, U64P, C.c_int64, I64P, C.c_int64, C.c_int64]
+    L.refeng_abandon.argtypes = [C.c_void_p, C.c_int64]
+    L.refeng_run.argtypes = [C.c_void_p, C.c_int64]
+    L.refeng_events.restype = C.c_int64
+    L.refeng_events.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+    L.refeng_overlap_scenario.restype = C.c_int64
+    L.refeng_overlap_scenario.argtypes = [C.c_int32, C.c_char_p, C.c_int64, I64P]
+    L.refeng_stream_key.restype = C.c_uint64
+    L.refeng_stream_key.argtypes = [C.c_char_p, C.c_uint64]
+
+
+def _kvlog_drain(L) -> str:
+    """Returns and clears the recording cache's op log."""
+    n = L.kvlog_take(None, 0)
+    buf = C.create_string_buffer(n + 1)
+    L.kvlog_take(buf, n + 1)
+    return buf.value.decode()
+
+
+def stream_key(request_id: str, iteration: int) -> int:
+    """Orchestrator::decode_stream_key (orchestrator.cpp:179-181)."""
+    L = ref()
+    if not hasattr(L, "_refeng"):
+        _declare_refeng(L)
+        L._refeng = True
+    return int(L.refeng_stream_key(request_id.encode(), iteration))
+
+
+class RefEngine:
+    """The UNMODIFIED reference Engine (engine.cpp) driven by a script of
+    engine-boundary actions at chosen virtual times (oracle/ref_engine.cpp).
+    ``events()`` returns every action and engine-internal KV transition
+    (pin / pin_failed / complete / finish) with the pool dump after it.
+    With ``kvlog=True`` the run goes through the recording cache and
+    ``oplog()`` returns its KvCache op log."""
+
+    def __init__(self, block_size: int, capacity: int, policy: int, sched: int = 0, cost=None, kvlog: bool = False):
+        L = kvlog_lib() if kvlog else ref()
+        if not hasattr(L, "_refeng"):
+            _declare_refeng(L)
+            L._refeng = True
+        self._L = L
+        self.kvlog = kvlog
+        if kvlog:
+            _kvlog_drain(L)
+        cst = (C.c_double * 4)(*cost) if cost is not None else None
+        self._h = L.refeng_create(block_size, capacity, policy, sched, cst)
+        if not self._h:
+            raise RuntimeError(L.refeng_last_error().decode())
+
+    def _chk(self, st):
+        if st:
+            raise RuntimeError(f"reference engine status {st}: {self._L.refeng_last_error().decode()}")
+
+    @staticmethod
+    def _tags(tags):
+        a = np.array([[int(b), int(e), int(t)] for b, e, t in tags], dtype=np.int64).reshape(-1, 3)
+        return np.ascontiguousarray(a)
+
+    def run(self, until: int = -1):
+        self._chk(self._L.refeng_run(self._h, until))
+
+    def now(self) -> int:
+        return int(self._L.refeng_now(self._h))
+
+    def submit_call(self, tokens, tags, decode_length: int, key: int) -> int:
+        t, g, out = np.ascontiguousarray(tokens, np.uint64), self._tags(tags), C.c_int64()
+        self._chk(self._L.refeng_submit_call(self._h, _u64(t), len(t), _i64(g), len(g), decode_length, key,
+                                             C.byref(out)))
+        return out.value
+
+    def submit_partial(self, tokens, tags, key: int) -> int:
+        t, g, out = np.ascontiguousarray(tokens, np.uint64), self._tags(tags), C.c_int64()
+        self._chk(self._L.refeng_submit_partial(self._h, _u64(t), len(t), _i64(g), len(g), key, C.byref(out)))
+        return out.value
+
+    def extend(self, call: int, tokens, tags, decode_length: int) -> int:
+        t, g = np.ascontiguousarray(tokens, np.uint64), self._tags(tags)
+        return self._L.refeng_extend(self._h, call, _u64(t), len(t), _i64(g), len(g), decode_length)
+
+    def abandon(self, call: int) -> int:
+        return self._L.refeng_abandon(self._h, call)
+
+    def events(self):
+        import json
+
+        n = self._L.refeng_events(self._h, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        self._L.refeng_events(self._h, buf, n + 1)
+        return [json.loads(x) for x in buf.value.decode().splitlines()]
+
+    def oplog(self) -> str:
+        return _kvlog_drain(self._L)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.refeng_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def ref_overlap_scenario(split: bool, kvlog: bool = False):
+    """scenarios.cpp:193-240 through the reference orchestrator: (timeline
+    text, FTR of R1, KvCache op log when kvlog)."""
+    L = kvlog_lib() if kvlog else ref()
+    if not hasattr(L, "_refeng"):
+        _declare_refeng(L)
+        L._refeng = True
+    if kvlog:
+        _kvlog_drain(L)
+    buf, ftr = C.create_string_buffer(1 << 20), C.c_int64()
+    n = L.refeng_overlap_scenario(1 if split else 0, buf, 1 << 20, C.byref(ftr))
+    if n < 0:
+        raise RuntimeError(L.refeng_last_error().decode())
+    log = _kvlog_drain(L) if kvlog else None
+    return buf.value.decode(), ftr.value, log

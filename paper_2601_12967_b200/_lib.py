@@ -82,10 +82,19 @@ SIGNATURES = {
     "sb_engine_cache": (VP, [VP]),
     "sb_engine_k_pool": (VP, [VP, C.c_int32]),
     "sb_engine_v_pool": (VP, [VP, C.c_int32]),
+    "sb_engine_submit_call": (C.c_int, [VP, U64P, C.c_int64, C.POINTER(TagRange), C.c_int64, C.c_int64, C.c_int64,
+                                        I32P]),
     "sb_engine_submit_partial": (C.c_int, [VP, U64P, C.c_int64, C.POINTER(TagRange), C.c_int64, C.c_int64, I32P]),
+    "sb_engine_prefill_done": (C.c_int, [VP, C.c_int32, C.c_int64, I32P]),
+    "sb_engine_extend": (C.c_int, [VP, C.c_int32, U64P, C.c_int64, C.POINTER(TagRange), C.c_int64, C.c_int64,
+                                   C.c_int64, I32P]),
     "sb_engine_abandon_partial": (C.c_int, [VP, C.c_int32]),
+    "sb_engine_finish": (C.c_int, [VP, C.c_int32, U64P, C.c_int64, C.c_int64]),
+    "sb_engine_call_info": (C.c_int, [VP, C.c_int32, I32P, I64P, I64P, I32P, I32P]),
+    "sb_engine_call_blocks": (C.c_int, [VP, C.c_int32, C.c_int32, I32P, C.c_int64, I64P]),
     "sb_engine_partial_blocks": (C.c_int, [VP, C.c_int32, I32P, C.c_int64, I64P]),
-    "sb_batch_create": (C.c_int, [VP, I32P, I64P, C.c_int32, C.POINTER(VP)]),
+    "sb_batch_create": (C.c_int, [VP, C.c_int32, U64P, I64P, C.POINTER(TagRange), I64P, I64P, U64P, C.POINTER(VP)]),
+    "sb_batch_pin_outcomes": (C.c_int, [VP, I32P]),
     "sb_batch_destroy": (None, [VP]),
     "sb_batch_stage_suffix": (C.c_int, [VP, VP, C.c_int32, VP]),
     "sb_batch_run": (C.c_int, [VP, C.c_int64, C.c_uint64, C.c_int32, VP, I32P]),

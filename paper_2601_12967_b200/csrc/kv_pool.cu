@@ -39,6 +39,7 @@
 #include "common.h"
 #include "hash.cuh"
 #include "sm100.cuh"
+#include "program.h"
 
 namespace sb {
 
@@ -56,7 +57,7 @@ constexpr int kCandSmem = 16384;  // candidate keys staged in shared memory (128
 constexpr int64_t kCoopMinCap = 16384;  // pools at least this large use the all-SM scorer
 
 enum Ctr { C_NRES = 0, C_EVICTED, C_LOOKUPS, C_HIT_TOK, C_LOOK_TOK, C_INS_BLOCKS, C_EV_BLOCKS, C_FULL, C_N };
-enum Scal { S_F = 0, S_K, S_FREE, S_NEV, S_STATUS, S_FAILPOS, S_NNEW, S_NCAND, S_ERRIDX, S_NLATE, S_N };
+enum Scal { S_F = 0, S_K, S_FREE, S_NEV, S_STATUS, S_FAILPOS, S_NNEW, S_NCAND, S_ERRIDX, S_NLATE, S_BOUND, S_N };
 // Blocks whose ref_count is -1 (reachable only through duplicate releases)
 // become eviction candidates the moment an insert hits them; at most this
 // many are tracked per insert.
@@ -939,6 +940,10 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
     const int64_t rest = P_ - f;
     Fp = min(free_cnt, rest);
     K = min(ncand, (rest > free_cnt ? rest - free_cnt : int64_t(0)) + static_cast<int64_t>(n_hc));
+  } else if (mode == 2) {  // op program: K and F bounded by k_prog_bound
+    const int64_t bnd = S.scal[S_BOUND];
+    K = min(ncand, bnd);
+    Fp = min(free_cnt, bnd);
   } else {
     K = min(ncand, needed);
   }
@@ -1375,6 +1380,10 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
     const int64_t rest = P_ - S.scal[S_F];
     Fp = min(free_cnt, rest);
     K = min(ncand, (rest > free_cnt ? rest - free_cnt : int64_t(0)) + static_cast<int64_t>(G.ctr[2]));
+  } else if (mode == 2) {  // op program: K and F bounded by k_prog_bound
+    const int64_t bnd = S.scal[S_BOUND];
+    K = min(ncand, bnd);
+    Fp = min(free_cnt, bnd);
   } else {
     K = min(ncand, needed);
   }
@@ -1897,6 +1906,16 @@ __global__ void k_priority_apply(Pool P, const int32_t* ids, int64_t n, int pinn
   }
 }
 __global__ void k_set_scal(int64_t* scal, int idx, int64_t v) { scal[idx] = v; }
+__global__ void k_release_status(Pool P, const int32_t* ids, int64_t n, const int64_t* scal, int32_t* status) {
+  if (threadIdx.x) return;
+  const int64_t e = scal[S_ERRIDX];
+  if (e >= n) {
+    *status = SB_OK;
+    return;
+  }
+  const int32_t id = ids[e];
+  *status = (id < 0 || id >= P.cap || P.ntok[id] == 0) ? SB_ERR_UNKNOWN_BLOCK : SB_ERR_ZERO_REF_RELEASE;
+}
 
 __global__ void k_evict_out(Pool P, Scratch S, int32_t* out, int64_t* n_out) {
   const int64_t K = S.scal[S_K];
@@ -1939,6 +1958,29 @@ __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
     p[i] = v;
 }
 
+#include "pool_program.cuh"
+
+// PK_INSERT descriptors of a device-described batch (sb_kv_insert_batch).
+__global__ void k_build_insert_ops(ProgOp* ops, const uint64_t* tokens, const int64_t* seq_off, const sb_tag_range* tags,
+                                   const int64_t* tag_off, const int64_t* blk_off, const uint64_t* hashes,
+                                   int32_t* out_ids, int n_seqs) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_seqs) return;
+  ProgOp o{};
+  o.kind = PK_INSERT;
+  o.n = seq_off[s + 1] - seq_off[s];
+  o.tokens = tokens + seq_off[s];
+  o.hashes = hashes + blk_off[s];
+  o.ins_tags = tags + tag_off[s];
+  o.n_ins_tags = static_cast<int32_t>(tag_off[s + 1] - tag_off[s]);
+  o.ids = out_ids + blk_off[s];
+  ops[s] = o;
+}
+__global__ void k_prog_status(const ProgRes* res, int n, int32_t* status) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n) status[s] = res[s].status;
+}
+
 // ==================================================================== host
 template <class T>
 static T* dalloc(size_t n) {
@@ -1974,6 +2016,17 @@ static void launch_probe_rows(const Pool& P, const uint64_t* tokens, const int64
   else
     k_probe_rows<4><<<grid, kProbePairs * kGroup, 0, st>>>(P, tokens, seq_off, blk_off, hashes, prehit, first_miss,
                                                             full_only_check);
+}
+
+// SB_LEGACY_INSERT=1: the per-sequence insert pipeline (probe, select, walk,
+// commit per sequence) instead of the op program — kept for A/B checks.
+static bool legacy_insert() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SB_LEGACY_INSERT");
+    v = e && atoi(e) ? 1 : 0;
+  }
+  return v == 1;
 }
 
 static int grid_for(int64_t n, int threads = 256) {
@@ -2015,7 +2068,111 @@ struct sb_kv_cache {
   int coop_grid = 0;
   size_t coop_smem = 0;
 
+  // op program (pool_program.cuh)
+  ProgOp* d_ops = nullptr;
+  int64_t ops_cap = 0;
+  ProgRes* d_res = nullptr;
+  uint64_t* d_runk = nullptr;
+  int64_t runk_cap = 0;
+  int64_t* d_pout = nullptr;
+  int64_t* h_pout = nullptr;  // pinned
+  int prog_device_attr = -1;
+
   bool use_coop() const { return P.cap >= kCoopMinCap && coop_grid > 0; }
+
+  // Ordering between the pool's own stream (per-op calls) and a caller's
+  // stream (batched calls): work on `st` starts after everything issued on
+  // the pool stream, and later pool-stream work starts after what `st` got.
+  cudaEvent_t ev_pool = nullptr, ev_user = nullptr;
+  void join_in(cudaStream_t st) {
+    if (st == stream) return;
+    if (!ev_pool) SB_CUDA(cudaEventCreateWithFlags(&ev_pool, cudaEventDisableTiming));
+    SB_CUDA(cudaEventRecord(ev_pool, stream));
+    SB_CUDA(cudaStreamWaitEvent(st, ev_pool, 0));
+  }
+  void join_out(cudaStream_t st) {
+    if (st == stream) return;
+    if (!ev_user) SB_CUDA(cudaEventCreateWithFlags(&ev_user, cudaEventDisableTiming));
+    SB_CUDA(cudaEventRecord(ev_user, st));
+    SB_CUDA(cudaStreamWaitEvent(stream, ev_user, 0));
+  }
+
+  void ensure_ops(int64_t n) {
+    if (n <= ops_cap) return;
+    cudaFree(d_ops);
+    cudaFree(d_res);
+    ops_cap = std::max<int64_t>(n, 2 * ops_cap + 8);
+    d_ops = dalloc<ProgOp>(ops_cap);
+    d_res = dalloc<ProgRes>(ops_cap);
+  }
+  void ensure_runk(int64_t n) {
+    if (n <= runk_cap) return;
+    cudaFree(d_runk);
+    runk_cap = std::max<int64_t>(n, 2 * runk_cap);
+    d_runk = dalloc<uint64_t>(runk_cap);
+  }
+
+  // Runs ops [0, n_ops) already in d_ops on stream st: per launch, the
+  // pre-state bound, one hint-aware scoring pass + select of K victims /
+  // F free ids (mode 2), then the program; repeated from the op the program
+  // stopped before (resources it could not see past) until all ops ran or
+  // an op failed.  max_pos / total_pos: block positions of the largest
+  // insert / of all inserts; pushes: worst-case candidate pushes.  Returns
+  // the number of ops applied (all of them unless one failed).
+  int64_t run_program(int64_t n_ops, int64_t max_pos, int64_t total_pos, int64_t pushes, int32_t* pin_cnt,
+                      int8_t* real_tag, int64_t now, cudaStream_t st, int64_t* evictions = nullptr) {
+    if (max_pos > kProgMaxPos)
+      throw Error(SB_ERR_UNSUPPORTED, "insert longer than " + std::to_string(kProgMaxPos) + " blocks");
+    ensure_positions(std::max<int64_t>({max_pos, 2 * total_pos + 64, 64}));
+    ensure_prehit_all(std::max<int64_t>(max_pos, 64));
+    ensure_runk(pushes + 64 * (n_ops + 1) + 4 * kRunBuf);
+    if (!d_pout) {
+      d_pout = dalloc<int64_t>(8);
+      SB_CUDA(cudaMallocHost(&h_pout, 8 * sizeof(int64_t)));
+    }
+    if (prog_device_attr != device) {
+      SB_CUDA(cudaFuncSetAttribute(k_program, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kProgSmem)));
+      prog_device_attr = device;
+    }
+    int64_t first = 0, evs = 0;
+    const unsigned gy = static_cast<unsigned>(std::max<int64_t>(1, (max_pos + 127) / 128));
+    while (first < n_ops) {
+      SB_CUDA(cudaMemsetAsync(d_pout, 0, 8 * sizeof(int64_t), st));
+      k_set_scal<<<1, 1, 0, st>>>(S.scal, S_BOUND, 64);
+      k_prog_bound<<<dim3(static_cast<unsigned>(n_ops - first), gy), 256, 0, st>>>(P, d_ops, static_cast<int>(first),
+                                                                                  static_cast<int>(n_ops), S.scal);
+      cudaStream_t saved = stream;
+      stream = st;
+      InsertArgs A{};
+      try {
+        launch_select(A, 0, 2, 0);
+      } catch (...) {
+        stream = saved;
+        throw;
+      }
+      stream = saved;
+      ProgState G{d_ops, d_res, static_cast<int32_t>(n_ops), static_cast<int32_t>(first), pin_cnt, real_tag,
+                  d_runk, runk_cap, d_pout, now};
+      k_program<<<1, kProgThreads, kProgSmem, st>>>(P, S, G);
+      SB_CHECK_LAUNCH();
+      SB_CUDA(cudaMemcpyAsync(h_pout, d_pout, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      SB_CUDA(cudaStreamSynchronize(st));
+      const int64_t next = h_pout[0];
+      evs += h_pout[2];
+      tomb_bound += h_pout[2];
+      if (next <= first) throw Error(SB_ERR_CACHE, "op program made no progress");
+      first = next;
+      if (h_pout[1] == PS_ERROR) break;  // a release error ends the batch (the reference throws)
+    }
+    if (evictions) *evictions = evs;
+    if (tomb_bound > P.cap) {
+      k_index_clear<<<grid_for(P.tcap), 256, 0, st>>>(P);
+      k_index_fill<<<grid_for(P.cap), 256, 0, st>>>(P);
+      SB_CHECK_LAUNCH();
+      tomb_bound = 0;
+    }
+    return first;
+  }
 
   void launch_select(const InsertArgs& A, int s, int mode, int64_t needed) {
     if (!use_coop()) {
@@ -2049,9 +2206,12 @@ struct sb_kv_cache {
     // S.prehit aliases d_prehit_all: freed once below
     void* ptrs[] = {P.tok, P.ntok, P.chain, P.parent, P.tag, P.ref, P.pinned, P.last, P.idx, P.slot, P.ctr,
                     S.hashes, S.chain_out, S.kind, S.freel, S.evicted, S.victims, S.taken, S.rank_of, S.keys,
-                    S.sortbuf, S.scal, S.late, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first, G.hist, G.ctr, G.keys, G.fcnt, G.ncnt, G.kmin, G.kmax};
+                    S.sortbuf, S.scal, S.late, d_ops, d_res, d_runk, d_pout, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first, G.hist, G.ctr, G.keys, G.fcnt, G.ncnt, G.kmin, G.kmax};
     for (void* p : ptrs)
       if (p) cudaFree(p);
+    if (h_pout) cudaFreeHost(h_pout);
+    if (ev_pool) cudaEventDestroy(ev_pool);
+    if (ev_user) cudaEventDestroy(ev_user);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -2164,6 +2324,56 @@ struct sb_kv_cache {
   }
 };
 
+namespace sb {
+int64_t pool_run_ops(sb_kv_cache* c, const ProgOp* h_ops, int64_t n, int32_t* d_pin_cnt, int8_t* d_real_tag,
+                     int64_t now, cudaStream_t st, ProgRes* h_res) {
+  if (n <= 0) return 0;
+  std::lock_guard<std::mutex> lk(c->mu);
+  SB_CUDA(cudaSetDevice(c->device));
+  check_now(c->P, now);
+  int64_t max_pos = 0, total = 0, pushes = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t pn = (h_ops[i].n + c->P.bs - 1) / c->P.bs;
+    max_pos = std::max(max_pos, pn);
+    total += pn;
+    pushes += pn + h_ops[i].n_chain + h_ops[i].n_pinned;
+  }
+  c->ensure_ops(n);
+  c->join_in(st);
+  SB_CUDA(cudaMemcpyAsync(c->d_ops, h_ops, sizeof(ProgOp) * n, cudaMemcpyHostToDevice, st));
+  const int64_t done = c->run_program(n, max_pos, total, pushes, d_pin_cnt, d_real_tag, now, st);
+  c->join_out(st);
+  SB_CUDA(cudaMemcpyAsync(h_res, c->d_res, sizeof(ProgRes) * n, cudaMemcpyDeviceToHost, st));
+  SB_CUDA(cudaStreamSynchronize(st));
+  return done;
+}
+
+void pool_lookup(sb_kv_cache* c, const ProgOp* h_ops, int64_t n, int64_t now, int64_t* d_hits, cudaStream_t st) {
+  if (n <= 0) return;
+  std::lock_guard<std::mutex> lk(c->mu);
+  SB_CUDA(cudaSetDevice(c->device));
+  check_now(c->P, now);
+  int64_t max_full = 0;
+  for (int64_t i = 0; i < n; ++i) max_full = std::max(max_full, h_ops[i].n / c->P.bs);
+  c->ensure_ops(n);
+  c->ensure_batch(n);
+  c->join_in(st);
+  SB_CUDA(cudaMemcpyAsync(c->d_ops, h_ops, sizeof(ProgOp) * n, cudaMemcpyHostToDevice, st));
+  k_lookup_ops_init<<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(c->P, c->d_ops, static_cast<int>(n),
+                                                                             c->d_batch_first);
+  if (max_full > 0)
+    k_lookup_ops_probe<<<dim3(static_cast<unsigned>(n), static_cast<unsigned>((max_full + 127) / 128)), 256, 0, st>>>(
+        c->P, c->d_ops, c->d_batch_first);
+  k_lookup_ops_finish<<<dim3(static_cast<unsigned>(n), static_cast<unsigned>(std::max<int64_t>(1, (max_full + 255) / 256))),
+                        256, 0, st>>>(c->P, c->d_ops, c->d_batch_first, now, d_hits);
+  SB_CHECK_LAUNCH();
+  c->join_out(st);
+}
+
+cudaStream_t pool_stream(sb_kv_cache* c) { return c->stream; }
+int pool_device(sb_kv_cache* c) { return c->device; }
+}  // namespace sb
+
 static thread_local std::string g_last_error;
 void sb::set_last_error(const std::string& m) { g_last_error = m; }
 
@@ -2209,7 +2419,9 @@ int sb_kv_gather_chain_hashes(sb_kv_cache* c, const int32_t* d_ids, const int64_
   return guard([&] {
     if (n <= 0) return int(SB_OK);
     SB_CUDA(cudaSetDevice(c->device));
-    k_gather_chain<<<grid_for(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(c->P, d_ids, d_pos, n, d_out);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    c->join_in(st);
+    k_gather_chain<<<grid_for(n), 256, 0, st>>>(c->P, d_ids, d_pos, n, d_out);
     SB_CHECK_LAUNCH();
     return int(SB_OK);
   });
@@ -2352,6 +2564,7 @@ int sb_kv_lookup_prefix_batch(sb_kv_cache* c, const uint64_t* d_tokens, const in
     if (n_seqs <= 0) return int(SB_OK);
     check_now(c->P, now);
     cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
+    c->join_in(st);
     std::vector<int64_t> off(n_seqs + 1), blk(n_seqs + 1);
     const bool pre = d_block_hashes && d_block_offsets;
     if (pre && h_block_offsets) {
@@ -2391,6 +2604,7 @@ int sb_kv_lookup_prefix_batch(sb_kv_cache* c, const uint64_t* d_tokens, const in
     k_lookup_finish<<<grid_for(std::max<int64_t>(total, n_seqs)), 256, 0, st>>>(
         c->P, d_seq_offsets, d_blk, n_seqs, total, c->d_prehit_all, c->d_batch_first, now, d_hit_tokens);
     SB_CHECK_LAUNCH();
+    c->join_out(st);
     return int(SB_OK);
   });
 }
@@ -2412,11 +2626,32 @@ int sb_kv_insert(sb_kv_cache* c, const uint64_t* tokens, int64_t n, const sb_tag
       SB_CUDA(cudaMemcpyAsync(c->d_tags, tags, sizeof(sb_tag_range) * n_tags, cudaMemcpyHostToDevice, c->stream));
     SB_CUDA(cudaMemcpyAsync(c->d_meta, meta, sizeof(meta), cudaMemcpyHostToDevice, c->stream));
     std::vector<int64_t> hb = {0, nblk};
-    c->insert_device(c->d_tok, c->d_meta, c->d_tags, c->d_meta + 2, c->d_meta + 4, nullptr, 1, now, c->d_ids,
-                     c->d_status, hb);
     int32_t st = 0;
-    SB_CUDA(cudaMemcpyAsync(&st, c->d_status, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
-    SB_CUDA(cudaStreamSynchronize(c->stream));
+    if (legacy_insert()) {
+      c->insert_device(c->d_tok, c->d_meta, c->d_tags, c->d_meta + 2, c->d_meta + 4, nullptr, 1, now, c->d_ids,
+                       c->d_status, hb);
+      SB_CUDA(cudaMemcpyAsync(&st, c->d_status, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+      SB_CUDA(cudaStreamSynchronize(c->stream));
+    } else {
+      // one PK_INSERT op through the op program
+      c->ensure_hash_all(std::max<int64_t>(nblk, 1));
+      if (nblk) launch_chain_hash(c->d_tok, c->d_meta, c->d_meta + 4, nullptr, 1, c->P.bs, 0, c->d_hash_all, c->stream);
+      ProgOp op{};
+      op.kind = PK_INSERT;
+      op.n = n;
+      op.tokens = c->d_tok;
+      op.hashes = c->d_hash_all;
+      op.ins_tags = c->d_tags;
+      op.n_ins_tags = static_cast<int32_t>(n_tags);
+      op.ids = c->d_ids;
+      c->ensure_ops(1);
+      SB_CUDA(cudaMemcpyAsync(c->d_ops, &op, sizeof(op), cudaMemcpyHostToDevice, c->stream));
+      c->run_program(1, nblk, nblk, 0, nullptr, nullptr, now, c->stream);
+      ProgRes r{};
+      SB_CUDA(cudaMemcpyAsync(&r, c->d_res, sizeof(r), cudaMemcpyDeviceToHost, c->stream));
+      SB_CUDA(cudaStreamSynchronize(c->stream));
+      st = r.status;
+    }
     if (st == 0 && nblk) {
       SB_CUDA(cudaMemcpy(out_ids, c->d_ids, sizeof(int32_t) * nblk, cudaMemcpyDeviceToHost));
       *n_out = nblk;
@@ -2442,16 +2677,40 @@ int sb_kv_insert_batch(sb_kv_cache* c, const uint64_t* d_tokens, const int64_t* 
     else
       SB_CUDA(cudaMemcpy(hb.data(), d_block_offsets, sizeof(int64_t) * (n_seqs + 1), cudaMemcpyDeviceToHost));
     // the caller's stream, taken literally (NULL = legacy default stream)
-    cudaStream_t saved = c->stream;
-    c->stream = static_cast<cudaStream_t>(stream);
-    try {
-      c->insert_device(d_tokens, d_seq_offsets, d_tags, d_tag_offsets, d_block_offsets, d_block_hashes, n_seqs, now,
-                       d_out_ids, d_status, hb);
-    } catch (...) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    c->join_in(st);
+    if (legacy_insert()) {
+      cudaStream_t saved = c->stream;
+      c->stream = st;
+      try {
+        c->insert_device(d_tokens, d_seq_offsets, d_tags, d_tag_offsets, d_block_offsets, d_block_hashes, n_seqs, now,
+                         d_out_ids, d_status, hb);
+      } catch (...) {
+        c->stream = saved;
+        throw;
+      }
       c->stream = saved;
-      throw;
+      c->join_out(st);
+      return int(SB_OK);
     }
-    c->stream = saved;
+    // the batch as PK_INSERT ops of one op program: pre-state bound, one
+    // scoring pass + select for the whole batch, one program launch
+    int64_t max_pos = 0;
+    for (int s = 0; s < n_seqs; ++s) max_pos = std::max(max_pos, hb[s + 1] - hb[s]);
+    const uint64_t* hashes = d_block_hashes;
+    if (!hashes) {
+      c->ensure_hash_all(std::max<int64_t>(hb[n_seqs], 1));
+      launch_chain_hash(d_tokens, d_seq_offsets, d_block_offsets, nullptr, n_seqs, c->P.bs, 0, c->d_hash_all, st);
+      hashes = c->d_hash_all;
+    }
+    c->ensure_ops(n_seqs);
+    k_build_insert_ops<<<(n_seqs + 127) / 128, 128, 0, st>>>(c->d_ops, d_tokens, d_seq_offsets, d_tags, d_tag_offsets,
+                                                            d_block_offsets, hashes, d_out_ids, n_seqs);
+    SB_CHECK_LAUNCH();
+    c->run_program(n_seqs, max_pos, hb[n_seqs], 0, nullptr, nullptr, now, st);
+    k_prog_status<<<(n_seqs + 127) / 128, 128, 0, st>>>(c->d_res, n_seqs, d_status);
+    SB_CHECK_LAUNCH();
+    c->join_out(st);
     return int(SB_OK);
   });
 }
@@ -2522,13 +2781,17 @@ int sb_kv_release_batch(sb_kv_cache* c, const int32_t* d_ids, int64_t n, int32_t
     std::lock_guard<std::mutex> lk(c->mu);
     SB_CUDA(cudaSetDevice(c->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
+    c->join_in(st);
     k_set_scal<<<1, 1, 0, st>>>(c->S.scal, S_ERRIDX, INT64_MAX);
     if (n > 0) {
       k_validate_ids<<<grid_for(n), 256, 0, st>>>(c->P, d_ids, n, 1, c->S.scal, 1);
       k_release_apply<<<grid_for(n), 256, 0, st>>>(c->P, d_ids, n, c->S.scal);
     }
+    // all-or-nothing outcome (kv_cache.cpp:228-236): the first failing id in
+    // order decides UnknownBlock / ZeroRefRelease
+    if (d_status) k_release_status<<<1, 32, 0, st>>>(c->P, d_ids, n, c->S.scal, d_status);
     SB_CHECK_LAUNCH();
-    (void)d_status;
+    c->join_out(st);
     return int(SB_OK);
   });
 }

@@ -2,24 +2,23 @@
 prompt splitting (paper §4.2) over the device block pool and the
 continuation-prefill attention kernel.
 
-Mirrors the reference engine's continuation API
-(/root/reference/proj/include/agentsim/engine.hpp:110-135):
+Mirrors the reference engine's call lifecycle
+(/root/reference/proj/include/agentsim/engine.hpp:104-111, src/engine.cpp):
 
-* ``submit_partial_prefill`` — insert the tool-independent prefix into the
-  block pool and pin it at the PARTIAL_PREFILL tier (Engine::pin_partial,
-  engine.cpp:250-286).  Its KV pages are produced by the (untimed) eager
-  prefill while the tool runs.
-* ``extend_prefill_batch`` — the hot path: for a batch of continuations,
-  chain-hash the full prompts, look up the cached prefix (the admission
-  lookup of engine.cpp:170), insert the prompt (hits on the pinned prefix,
-  new blocks for the tool outputs, hint-aware eviction under pool pressure:
-  Engine::complete_prefill, engine.cpp:305-322), scatter the suffix K/V into
-  the new pages and run the continuation attention layer by layer; the
-  call's block references are released at the end (engine.cpp:343-346).
-* ``abandon_partial`` — unpin (engine.cpp:234-248).
+* ``submit_call`` / ``submit_partial_prefill`` — admission lookup of the
+  prompt (engine.cpp:128-182);
+* ``prefill_done`` — Engine::complete_prefill (engine.cpp:305-322): a partial
+  not yet extended is pinned at PARTIAL_PREFILL with shared pin counts and
+  remembered real tags (pin_partial, engine.cpp:250-286), else the prompt is
+  inserted, the pins released (engine.cpp:288-303) and the old refs dropped;
+* ``extend_prefill`` (engine.cpp:184-223), ``abandon_partial``
+  (engine.cpp:234-248), ``finish_decode`` (engine.cpp:324-347).
 
-All device work is issued on one CUDA stream with no host round trip; torch
-only provides device memory.
+Every KV transition is one op of the block pool's device op program.  The
+hot path is ``ContinuationBatch``: one ``run`` is the whole lifecycle of a
+batch of agentic continuations (admission lookups, pins, extension,
+complete with hint-aware eviction, per layer KV append + tcgen05 attention,
+finish), each transition one op program over the batch.
 """
 from __future__ import annotations
 
@@ -106,17 +105,12 @@ def _p(t):
     return C.c_void_p(t.data_ptr())
 
 
-@dataclass
-class PartialHandle:
-    """ContinuationHandle (engine.hpp:72) + the pinned prefix it owns."""
-    call_id: int
-    tokens: np.ndarray
-    tags: list
-    block_ids: List[int]
-
-
 class ContinuationEngine:
     """Binding of the C++ continuation engine (csrc/engine.cu, ``sb_engine_*``)."""
+
+    # agentsim::CallState (engine.hpp:35)
+    QUEUED, PREFILLING, AWAITING_EXTENSION, DECODING, DONE, ABORTED = range(6)
+    PINNED, PIN_FAILED, COMPLETED = 1, 2, 3
 
     def __init__(self, shape: ModelShape, capacity_blocks: int, policy: int = TIERED, block_size: int = 16,
                  device: int = 0, seed: int = 0):
@@ -154,55 +148,104 @@ class ContinuationEngine:
     def v_pool(self, layer: int):
         return self._L.sb_engine_v_pool(self._h, layer)
 
-    # ---------------------------------------------------------------- API
-    def submit_partial_prefill(self, prefix_tokens: np.ndarray, tags, now: int) -> PartialHandle:
-        t = np.ascontiguousarray(prefix_tokens, dtype=np.uint64)
+    @staticmethod
+    def _tags(tags):
         arr = (_lib.TagRange * max(len(tags), 1))()
         for i, (b, e, tg) in enumerate(tags):
             arr[i].begin, arr[i].end, arr[i].tag = int(b), int(e), int(tg)
-        hid = C.c_int32(0)
-        _lib.check(self._L.sb_engine_submit_partial(self._h, t.ctypes.data_as(_lib.U64P), len(t), arr, len(tags), now,
-                                                    C.byref(hid)), "submit_partial_prefill")
-        ids = np.zeros((len(t) + 15) // 16, dtype=np.int32)
-        n = C.c_int64(0)
-        _lib.check(self._L.sb_engine_partial_blocks(self._h, hid.value, ids.ctypes.data_as(_lib.I32P), len(ids),
-                                                    C.byref(n)))
-        return PartialHandle(hid.value, t, list(tags), ids[: n.value].tolist())
+        return arr
 
-    def prefill_partials(self, handles: Sequence[PartialHandle], model: "DenseModel"):
-        """Run the model over the uncached part of each partial prefix (the
-        prefill that overlaps the tool call), writing its K/V into the pinned
-        pages (``sb_engine_prefill_partials``)."""
-        hid = np.array([h.call_id for h in handles], dtype=np.int32)
+    # ------------------------------------------------------------ lifecycle
+    def submit_call(self, tokens, tags, decode_length: int, now: int) -> int:
+        t = np.ascontiguousarray(tokens, dtype=np.uint64)
+        out = C.c_int32(0)
+        _lib.check(self._L.sb_engine_submit_call(self._h, t.ctypes.data_as(_lib.U64P), len(t), self._tags(tags),
+                                                 len(tags), decode_length, now, C.byref(out)), "submit_call")
+        return out.value
+
+    def submit_partial_prefill(self, prefix_tokens, tags, now: int) -> int:
+        t = np.ascontiguousarray(prefix_tokens, dtype=np.uint64)
+        out = C.c_int32(0)
+        _lib.check(self._L.sb_engine_submit_partial(self._h, t.ctypes.data_as(_lib.U64P), len(t), self._tags(tags),
+                                                    len(tags), now, C.byref(out)), "submit_partial_prefill")
+        return out.value
+
+    def prefill_done(self, call: int, now: int) -> int:
+        """The call's prefill finished: pin (partial) or complete.  Returns
+        PINNED / PIN_FAILED / COMPLETED."""
+        out = C.c_int32(0)
+        _lib.check(self._L.sb_engine_prefill_done(self._h, call, now, C.byref(out)), "prefill_done")
+        return out.value
+
+    def extend_prefill(self, call: int, suffix, tags, decode_length: int, now: int) -> bool:
+        t = np.ascontiguousarray(suffix, dtype=np.uint64)
+        done = C.c_int32(0)
+        _lib.check(self._L.sb_engine_extend(self._h, call, t.ctypes.data_as(_lib.U64P), len(t), self._tags(tags),
+                                            len(tags), decode_length, now, C.byref(done)), "extend_prefill")
+        return bool(done.value)
+
+    def abandon_partial(self, call: int):
+        _lib.check(self._L.sb_engine_abandon_partial(self._h, call), "abandon_partial")
+
+    def finish_decode(self, call: int, response, now: int):
+        t = np.ascontiguousarray(response, dtype=np.uint64)
+        _lib.check(self._L.sb_engine_finish(self._h, call, t.ctypes.data_as(_lib.U64P), len(t), now), "finish_decode")
+
+    def call_info(self, call: int) -> dict:
+        st, cached, prompt, nc, npn = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int32(), C.c_int32()
+        _lib.check(self._L.sb_engine_call_info(self._h, call, C.byref(st), C.byref(cached), C.byref(prompt),
+                                               C.byref(nc), C.byref(npn)), "call_info")
+        return {"state": st.value, "cached_prefix": cached.value, "prompt_tokens": prompt.value,
+                "n_chain": nc.value, "n_pinned": npn.value}
+
+    def call_blocks(self, call: int, pinned: bool = False) -> List[int]:
+        info = self.call_info(call)
+        n = info["n_pinned" if pinned else "n_chain"]
+        out = np.zeros(max(n, 1), np.int32)
+        got = C.c_int64(0)
+        _lib.check(self._L.sb_engine_call_blocks(self._h, call, int(pinned), out.ctypes.data_as(_lib.I32P), len(out),
+                                                 C.byref(got)))
+        return out[: got.value].tolist()
+
+    def cached_at_submit(self, call: int) -> int:
+        return self.call_info(call)["cached_prefix"]
+
+    def prefill_partials(self, calls: Sequence[int], model: "DenseModel"):
+        """Run the model over the uncached part of each pinned partial prefix
+        (the prefill that overlaps the tool call), writing its K/V into the
+        pinned pages (``sb_engine_prefill_partials``)."""
+        hid = np.array(list(calls), dtype=np.int32)
         _lib.check(self._L.sb_engine_prefill_partials(self._h, model._h, hid.ctypes.data_as(_lib.I32P), len(hid),
                                                       ContinuationBatch._stream()), "prefill_partials")
 
-    def cached_at_submit(self, handle: PartialHandle) -> int:
-        n = C.c_int64(0)
-        _lib.check(self._L.sb_engine_partial_cached(self._h, handle.call_id, C.byref(n)), "partial_cached")
-        return n.value
-
-    def abandon_partial(self, handle: PartialHandle):
-        _lib.check(self._L.sb_engine_abandon_partial(self._h, handle.call_id), "abandon_partial")
-
-    def make_batch(self, handles: Sequence[PartialHandle], suffix_lens: Sequence[int]) -> "ContinuationBatch":
-        return ContinuationBatch(self, list(handles), list(suffix_lens))
+    def make_batch(self, prefixes: Sequence[np.ndarray], prefix_tags: Sequence[list], suffix_lens: Sequence[int],
+                   stream_keys: Optional[Sequence[int]] = None) -> "ContinuationBatch":
+        return ContinuationBatch(self, list(prefixes), list(prefix_tags), list(suffix_lens), stream_keys)
 
 
 class ContinuationBatch:
-    """A batch of extend_prefill continuations (``sb_batch_*``)."""
+    """A batch of agentic continuations run through the engine lifecycle per
+    step (``sb_batch_*``): slot i has a fixed tool-independent prefix and a
+    fixed tool-output length; every ``run`` is n new calls."""
 
-    def __init__(self, eng: ContinuationEngine, handles: List[PartialHandle], suffix_lens: List[int]):
+    def __init__(self, eng: ContinuationEngine, prefixes, prefix_tags, suffix_lens, stream_keys=None):
         self.eng = eng
         self._L = eng._L
-        self.n = len(handles)
-        hid = np.array([h.call_id for h in handles], dtype=np.int32)
+        self.n = len(prefixes)
+        toks = np.ascontiguousarray(np.concatenate([np.asarray(p, np.uint64) for p in prefixes]), dtype=np.uint64)
+        off = np.cumsum([0] + [len(p) for p in prefixes]).astype(np.int64)
+        flat = [t for tg in prefix_tags for t in tg]
+        toff = np.cumsum([0] + [len(tg) for tg in prefix_tags]).astype(np.int64)
         sl = np.array(suffix_lens, dtype=np.int64)
+        keys = np.array(stream_keys, dtype=np.uint64) if stream_keys is not None else None
         h = C.c_void_p()
-        _lib.check(self._L.sb_batch_create(eng._h, hid.ctypes.data_as(_lib.I32P), sl.ctypes.data_as(_lib.I64P),
-                                           self.n, C.byref(h)), "batch")
+        _lib.check(self._L.sb_batch_create(eng._h, self.n, toks.ctypes.data_as(_lib.U64P), off.ctypes.data_as(_lib.I64P),
+                                           ContinuationEngine._tags(flat), toff.ctypes.data_as(_lib.I64P),
+                                           sl.ctypes.data_as(_lib.I64P),
+                                           keys.ctypes.data_as(_lib.U64P) if keys is not None else None, C.byref(h)),
+                   "batch")
         self._h = h
-        self.prefix_lens = [len(x.tokens) for x in handles]
+        self.prefix_lens = [len(p) for p in prefixes]
         self.suffix_lens = list(suffix_lens)
         self.full_lens = [p + s for p, s in zip(self.prefix_lens, self.suffix_lens)]
         self.blk_off_h = np.cumsum([0] + [(n + 15) // 16 for n in self.full_lens]).astype(np.int64)
@@ -241,7 +284,7 @@ class ContinuationBatch:
                    "stage_suffix")
         return 0
 
-    def run(self, now: int, seed: int, time_attention: bool = False) -> int:
+    def run(self, now: int, seed: int = 0, time_attention: bool = False) -> int:
         n = C.c_int32(0)
         _lib.check(self._L.sb_batch_run(self._h, now, seed, int(time_attention), self._stream(), C.byref(n)), "run")
         self.launches_per_step = n.value
@@ -253,12 +296,19 @@ class ContinuationBatch:
         return list(out)
 
     def results(self):
+        """(admission hits [n], complete statuses [n], chains the continuation
+        attended over [total_blocks] laid out by blk_off_h)."""
         hits = np.zeros(self.n, np.int64)
         st = np.zeros(self.n, np.int32)
         ids = np.zeros(self.total_blocks, np.int32)
         _lib.check(self._L.sb_batch_results(self._h, hits.ctypes.data_as(_lib.I64P), st.ctypes.data_as(_lib.I32P),
                                             ids.ctypes.data_as(_lib.I32P), self._stream()))
         return hits, st, ids
+
+    def pin_outcomes(self) -> np.ndarray:
+        out = np.zeros(self.n, np.int32)
+        _lib.check(self._L.sb_batch_pin_outcomes(self._h, out.ctypes.data_as(_lib.I32P)))
+        return out
 
     def output_sample(self, host_buf, n_rows: int = 1) -> int:
         """Async D2H of the last n_rows query rows of the last layer's attention

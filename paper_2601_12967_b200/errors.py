@@ -27,6 +27,22 @@ class ZeroRefRelease(CacheError):
     pass
 
 
+class EngineError(SimError):
+    pass
+
+
+class StaleHandle(EngineError):
+    pass
+
+
+class InvalidState(EngineError):
+    pass
+
+
+class UnknownCall(EngineError):
+    pass
+
+
 class CudaError(RuntimeError):
     pass
 
@@ -36,7 +52,7 @@ class Unsupported(ValueError):
 
 
 _BY_STATUS = {1: CacheFull, 2: UnknownBlock, 3: ZeroRefRelease, 4: CacheError, 5: ConfigError, 6: CudaError,
-              7: ValueError, 8: Unsupported}
+              7: ValueError, 8: Unsupported, 9: StaleHandle, 10: InvalidState, 11: UnknownCall}
 
 STATUS_OF = {v: k for k, v in _BY_STATUS.items()}
 

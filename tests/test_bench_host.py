@@ -31,7 +31,7 @@ def test_capacity_for_counts_shared_prefix_once():
     reqs = W.agentic_continuation_batch(4, seed=1)
     pre, suf, cap = bench.capacity_for(reqs)
     assert pre == sum(r.prefix_len // 16 for r in reqs) - 3 * (2048 // 16)
-    assert suf == sum((r.suffix_len + 15) // 16 for r in reqs)
+    assert suf == sum((r.suffix_len + 15) // 16 for r in reqs) + len(reqs)  # + one response block per call
     assert cap == pre + int(1.25 * suf) + 1
 
 

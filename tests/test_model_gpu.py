@@ -68,11 +68,8 @@ def test_dense_step_matches_torch_reference(prefix_lens, suffix_lens):
     cap = sum((p + s + 15) // 16 for p, s in zip(prefix_lens, suffix_lens)) + 4
     eng = ContinuationEngine(ModelShape(nl, hq, hkv, 128), cap, policy=1, seed=7)
     model = DenseModel(ds, seed=3)
-    handles = []
-    for i, p in enumerate(prefix_lens):
-        toks = O.materialize(0, p, 100 + i)
-        handles.append(eng.submit_partial_prefill(toks, [(0, p, 3)], now=0))
-    batch = eng.make_batch(handles, suffix_lens)
+    prefixes = [O.materialize(0, p, 100 + i) for i, p in enumerate(prefix_lens)]
+    batch = eng.make_batch(prefixes, [[(0, p, 3)] for p in prefix_lens], suffix_lens)
     batch.set_model(model)
     rng = np.random.default_rng(1)
     suffix = rng.integers(0, 2**62, sum(suffix_lens), dtype=np.int64)
@@ -183,12 +180,15 @@ def test_split_prefill_equals_monolithic_prefill():
     system = rng.integers(0, 2**62, 64, dtype=np.int64).view(np.uint64)
     pre_a = np.concatenate([system, rng.integers(0, 2**62, 96, dtype=np.int64).view(np.uint64)])
     pre_b = np.concatenate([system, rng.integers(0, 2**62, 80, dtype=np.int64).view(np.uint64)])
-    ha = eng.submit_partial_prefill(pre_a, [(0, 64, 3), (64, 160, 2)], now=0)
-    hb = eng.submit_partial_prefill(pre_b, [(0, 64, 3), (64, 144, 2)], now=1)
+    tags_a, tags_b = [(0, 64, 3), (64, 160, 2)], [(0, 64, 3), (64, 144, 2)]
+    ha = eng.submit_partial_prefill(pre_a, tags_a, now=0)
+    assert eng.prefill_done(ha, now=0) == eng.PINNED      # pages of the prefix admitted
+    hb = eng.submit_partial_prefill(pre_b, tags_b, now=1)
+    assert eng.prefill_done(hb, now=1) == eng.PINNED
     assert eng.cached_at_submit(ha) == 0 and eng.cached_at_submit(hb) == 64
     eng.prefill_partials([ha, hb], model)          # while the tools run
     sfx = [37, 50]
-    batch = eng.make_batch([ha, hb], sfx)           # the tool outputs arrive
+    batch = eng.make_batch([pre_a, pre_b], [tags_a, tags_b], sfx)  # the tool outputs arrive
     batch.set_model(model)
     suffix = rng.integers(0, 2**62, sum(sfx), dtype=np.int64)
     batch.stage_suffix_device(torch.from_numpy(suffix).cuda())
@@ -219,9 +219,7 @@ def test_split_prefill_equals_monolithic_prefill():
     # negative control: without the partial prefill the prefix pages hold the
     # engine's stand-in KV, and the same check must fail
     eng2 = ContinuationEngine(ModelShape(nl, hq, hkv, 128), 256, policy=1, seed=9)
-    h2 = [eng2.submit_partial_prefill(pre_a, [(0, 64, 3), (64, 160, 2)], now=0),
-          eng2.submit_partial_prefill(pre_b, [(0, 64, 3), (64, 144, 2)], now=1)]
-    b2 = eng2.make_batch(h2, sfx)
+    b2 = eng2.make_batch([pre_a, pre_b], [tags_a, tags_b], sfx)
     b2.set_model(model)
     b2.stage_suffix_device(torch.from_numpy(suffix).cuda())
     b2.run(now=5, seed=0)
