@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstdint>
 #include <cstring>
@@ -57,7 +58,7 @@ constexpr int kCandSmem = 16384;  // candidate keys staged in shared memory (128
 constexpr int64_t kCoopMinCap = 16384;  // pools at least this large use the all-SM scorer
 
 enum Ctr { C_NRES = 0, C_EVICTED, C_LOOKUPS, C_HIT_TOK, C_LOOK_TOK, C_INS_BLOCKS, C_EV_BLOCKS, C_FULL, C_N };
-enum Scal { S_F = 0, S_K, S_FREE, S_NEV, S_STATUS, S_FAILPOS, S_NNEW, S_NCAND, S_ERRIDX, S_NLATE, S_BOUND, S_N };
+enum Scal { S_F = 0, S_K, S_FREE, S_NEV, S_STATUS, S_FAILPOS, S_NNEW, S_NCAND, S_ERRIDX, S_NLATE, S_BOUND, S_NMISS, S_N };
 // Blocks whose ref_count is -1 (reachable only through duplicate releases)
 // become eviction candidates the moment an insert hits them; at most this
 // many are tracked per insert.
@@ -941,7 +942,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
     Fp = min(free_cnt, rest);
     K = min(ncand, (rest > free_cnt ? rest - free_cnt : int64_t(0)) + static_cast<int64_t>(n_hc));
   } else if (mode == 2) {  // op program: K and F bounded by k_prog_bound
-    const int64_t bnd = S.scal[S_BOUND];
+    const int64_t bnd = S.scal[S_NMISS] > 0 ? S.scal[S_BOUND] : 0;
     K = min(ncand, bnd);
     Fp = min(free_cnt, bnd);
   } else {
@@ -1381,7 +1382,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
     Fp = min(free_cnt, rest);
     K = min(ncand, (rest > free_cnt ? rest - free_cnt : int64_t(0)) + static_cast<int64_t>(G.ctr[2]));
   } else if (mode == 2) {  // op program: K and F bounded by k_prog_bound
-    const int64_t bnd = S.scal[S_BOUND];
+    const int64_t bnd = S.scal[S_NMISS] > 0 ? S.scal[S_BOUND] : 0;
     K = min(ncand, bnd);
     Fp = min(free_cnt, bnd);
   } else {
@@ -1974,6 +1975,7 @@ __global__ void k_build_insert_ops(ProgOp* ops, const uint64_t* tokens, const in
   o.ins_tags = tags + tag_off[s];
   o.n_ins_tags = static_cast<int32_t>(tag_off[s + 1] - tag_off[s]);
   o.ids = out_ids + blk_off[s];
+  o.pos_off = blk_off[s];
   ops[s] = o;
 }
 __global__ void k_prog_status(const ProgRes* res, int n, int32_t* status) {
@@ -2076,9 +2078,32 @@ struct sb_kv_cache {
   int64_t runk_cap = 0;
   int64_t* d_pout = nullptr;
   int64_t* h_pout = nullptr;  // pinned
+  int32_t* d_pre_all = nullptr;  // pre-program probe of every insert position
+  int64_t pre_all_cap = 0;
+  unsigned long long* d_created = nullptr;  // chain hashes created by a program
+  int64_t created_cap = 0;
   int prog_device_attr = -1;
 
   bool use_coop() const { return P.cap >= kCoopMinCap && coop_grid > 0; }
+
+  // SB_PROG_PROFILE=1: per-phase cycle counters of the op program, printed
+  // to stderr at destruction (phases: 0 setup, 1 hints, 2 re-probe, 3 flags,
+  // 4 victim window, 5 walk, 6 evictions, 7 commit, 8 late runs, 9 op
+  // dispatch, 10 op follow-ups: pins / unpins / releases)
+  unsigned long long* d_prof = nullptr;
+  unsigned long long* prof_buf() {
+    static int on = -1;
+    if (on < 0) {
+      const char* e = getenv("SB_PROG_PROFILE");
+      on = e && atoi(e) ? 1 : 0;
+    }
+    if (!on) return nullptr;
+    if (!d_prof) {
+      d_prof = dalloc<unsigned long long>(64);
+      SB_CUDA(cudaMemset(d_prof, 0, 64 * sizeof(unsigned long long)));
+    }
+    return d_prof;
+  }
 
   // Ordering between the pool's own stream (per-op calls) and a caller's
   // stream (batched calls): work on `st` starts after everything issued on
@@ -2126,6 +2151,18 @@ struct sb_kv_cache {
     ensure_positions(std::max<int64_t>({max_pos, 2 * total_pos + 64, 64}));
     ensure_prehit_all(std::max<int64_t>(max_pos, 64));
     ensure_runk(pushes + 64 * (n_ops + 1) + 4 * kRunBuf);
+    if (total_pos + 1 > pre_all_cap) {
+      cudaFree(d_pre_all);
+      pre_all_cap = std::max<int64_t>(total_pos + 1, 2 * pre_all_cap);
+      d_pre_all = dalloc<int32_t>(pre_all_cap);
+    }
+    int64_t ccap = 1024;
+    while (ccap < 2 * total_pos + 64) ccap <<= 1;
+    if (ccap > created_cap) {
+      cudaFree(d_created);
+      created_cap = ccap;
+      d_created = dalloc<unsigned long long>(created_cap);
+    }
     if (!d_pout) {
       d_pout = dalloc<int64_t>(8);
       SB_CUDA(cudaMallocHost(&h_pout, 8 * sizeof(int64_t)));
@@ -2135,12 +2172,19 @@ struct sb_kv_cache {
       prog_device_attr = device;
     }
     int64_t first = 0, evs = 0;
+    bool force = false;
     const unsigned gy = static_cast<unsigned>(std::max<int64_t>(1, (max_pos + 127) / 128));
     while (first < n_ops) {
       SB_CUDA(cudaMemsetAsync(d_pout, 0, 8 * sizeof(int64_t), st));
+      SB_CUDA(cudaMemsetAsync(d_created, 0, sizeof(unsigned long long) * ccap, st));
       k_set_scal<<<1, 1, 0, st>>>(S.scal, S_BOUND, 64);
-      k_prog_bound<<<dim3(static_cast<unsigned>(n_ops - first), gy), 256, 0, st>>>(P, d_ops, static_cast<int>(first),
-                                                                                  static_cast<int>(n_ops), S.scal);
+      k_set_scal<<<1, 1, 0, st>>>(S.scal, S_NMISS, 0);
+      k_prog_bound<<<dim3(static_cast<unsigned>(n_ops - first), gy), 256, 0, st>>>(
+          P, d_ops, static_cast<int>(first), static_cast<int>(n_ops), S.scal, d_pre_all);
+      if (force) {  // the bound left the program short once: list every candidate
+        k_set_scal<<<1, 1, 0, st>>>(S.scal, S_NMISS, 1);
+        k_set_scal<<<1, 1, 0, st>>>(S.scal, S_BOUND, 2 * total_pos + 64);
+      }
       cudaStream_t saved = stream;
       stream = st;
       InsertArgs A{};
@@ -2152,7 +2196,7 @@ struct sb_kv_cache {
       }
       stream = saved;
       ProgState G{d_ops, d_res, static_cast<int32_t>(n_ops), static_cast<int32_t>(first), pin_cnt, real_tag,
-                  d_runk, runk_cap, d_pout, now};
+                  d_runk, runk_cap, d_pout, now, d_pre_all, d_created, ccap - 1, prof_buf()};
       k_program<<<1, kProgThreads, kProgSmem, st>>>(P, S, G);
       SB_CHECK_LAUNCH();
       SB_CUDA(cudaMemcpyAsync(h_pout, d_pout, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -2160,7 +2204,12 @@ struct sb_kv_cache {
       const int64_t next = h_pout[0];
       evs += h_pout[2];
       tomb_bound += h_pout[2];
-      if (next <= first) throw Error(SB_ERR_CACHE, "op program made no progress");
+      if (next <= first) {
+        if (force) throw Error(SB_ERR_CACHE, "op program made no progress");
+        force = true;
+        continue;
+      }
+      force = false;
       first = next;
       if (h_pout[1] == PS_ERROR) break;  // a release error ends the batch (the reference throws)
     }
@@ -2206,9 +2255,19 @@ struct sb_kv_cache {
     // S.prehit aliases d_prehit_all: freed once below
     void* ptrs[] = {P.tok, P.ntok, P.chain, P.parent, P.tag, P.ref, P.pinned, P.last, P.idx, P.slot, P.ctr,
                     S.hashes, S.chain_out, S.kind, S.freel, S.evicted, S.victims, S.taken, S.rank_of, S.keys,
-                    S.sortbuf, S.scal, S.late, d_ops, d_res, d_runk, d_pout, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first, G.hist, G.ctr, G.keys, G.fcnt, G.ncnt, G.kmin, G.kmax};
+                    S.sortbuf, S.scal, S.late, d_ops, d_res, d_runk, d_pout, d_pre_all, d_created, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first, G.hist, G.ctr, G.keys, G.fcnt, G.ncnt, G.kmin, G.kmax};
     for (void* p : ptrs)
       if (p) cudaFree(p);
+    if (d_prof) {
+      unsigned long long h[64] = {};
+      cudaMemcpy(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost);
+      for (int k = 0; k < 5; ++k) {
+        fprintf(stderr, "SB_PROG_PROFILE kind %d cycles:", k);
+        for (int i = 0; i < 11; ++i) fprintf(stderr, " %d:%llu", i, h[k * 11 + i]);
+        fprintf(stderr, "\n");
+      }
+      cudaFree(d_prof);
+    }
     if (h_pout) cudaFreeHost(h_pout);
     if (ev_pool) cudaEventDestroy(ev_pool);
     if (ev_user) cudaEventDestroy(ev_user);
@@ -2332,15 +2391,17 @@ int64_t pool_run_ops(sb_kv_cache* c, const ProgOp* h_ops, int64_t n, int32_t* d_
   SB_CUDA(cudaSetDevice(c->device));
   check_now(c->P, now);
   int64_t max_pos = 0, total = 0, pushes = 0;
+  std::vector<ProgOp> ops(h_ops, h_ops + n);
   for (int64_t i = 0; i < n; ++i) {
     const int64_t pn = (h_ops[i].n + c->P.bs - 1) / c->P.bs;
+    ops[static_cast<size_t>(i)].pos_off = total;
     max_pos = std::max(max_pos, pn);
     total += pn;
     pushes += pn + h_ops[i].n_chain + h_ops[i].n_pinned;
   }
   c->ensure_ops(n);
   c->join_in(st);
-  SB_CUDA(cudaMemcpyAsync(c->d_ops, h_ops, sizeof(ProgOp) * n, cudaMemcpyHostToDevice, st));
+  SB_CUDA(cudaMemcpyAsync(c->d_ops, ops.data(), sizeof(ProgOp) * n, cudaMemcpyHostToDevice, st));
   const int64_t done = c->run_program(n, max_pos, total, pushes, d_pin_cnt, d_real_tag, now, st);
   c->join_out(st);
   SB_CUDA(cudaMemcpyAsync(h_res, c->d_res, sizeof(ProgRes) * n, cudaMemcpyDeviceToHost, st));
@@ -2644,6 +2705,7 @@ int sb_kv_insert(sb_kv_cache* c, const uint64_t* tokens, int64_t n, const sb_tag
       op.ins_tags = c->d_tags;
       op.n_ins_tags = static_cast<int32_t>(n_tags);
       op.ids = c->d_ids;
+      op.pos_off = 0;
       c->ensure_ops(1);
       SB_CUDA(cudaMemcpyAsync(c->d_ops, &op, sizeof(op), cudaMemcpyHostToDevice, c->stream));
       c->run_program(1, nblk, nblk, 0, nullptr, nullptr, now, c->stream);

@@ -52,14 +52,33 @@ struct ProgState {
   int64_t runk_cap;
   int64_t* out;           // [0] next op to run, [1] stop kind, [2] evictions, [3] inserted blocks
   int64_t now;
+  const int32_t* pre_all; // pre-program probe result of every insert position (k_prog_bound)
+  unsigned long long* created;  // chain hashes of blocks created by this program (open addressing, 0 = empty)
+  int64_t created_mask;
+  unsigned long long* prof;     // SB_PROG_PROFILE: cycles per program phase (thread 0), else null
 };
+// phase clock (thread 0, at barrier points): cycles since the previous mark
+#define PROG_T(k)                                                    \
+  do {                                                               \
+    if (G.prof && threadIdx.x == 0) {                                \
+      const unsigned long long c_ = clock64();                       \
+      G.prof[sh.pkind * 11 + (k)] += c_ - sh.tlast;                  \
+      sh.tlast = c_;                                                 \
+    }                                                                \
+  } while (0)
 
 constexpr int kProgThreads = 1024;
 constexpr int kSetSlots = 16384;   // per-insert "touched" id set (evicted or referenced), shared memory
 constexpr int kRunMax = 512;       // candidate runs
 constexpr int kRunBuf = 2048;      // keys per run (one sort in shared memory)
 constexpr int kProgMaxPos = kSetSlots / 2;  // block positions of one insert
-constexpr size_t kProgSmem = kSetSlots * sizeof(int32_t) + kRunBuf * sizeof(uint64_t);
+// dynamic shared memory: touched-id set | run sort buffer | per-position id,
+// probe list, kind
+constexpr int kWin = 2048;  // list entries pre-validated per insert (victim window)
+constexpr int kTagSmem = 256;  // insert tag ranges staged in shared memory
+constexpr size_t kProgSmem = kSetSlots * sizeof(int32_t) + kRunBuf * sizeof(uint64_t) +
+                             kWin * (sizeof(uint64_t) + sizeof(int32_t)) +
+                             kProgMaxPos * (2 * sizeof(int32_t) + sizeof(int8_t));
 
 struct ProgShared {
   uint64_t run_head[kRunMax];  // key at the head of each run (kNoKey: exhausted)
@@ -70,7 +89,15 @@ struct ProgShared {
   int64_t K, F, ncand0, free0, list_ptr, free_ptr, runk_used;
   int64_t nev, nnew, failpos;
   unsigned long long err;
-  int n_runs, n_late, status, stop, n_sort, sort_overflow;
+  int n_runs, n_late, status, stop, n_sort, sort_overflow, n_probe;
+  // victim window of the current insert: valid list entries [win_beg, win_end)
+  // compacted in list order into wkey / widx, consumed from wptr
+  int64_t win_end;
+  unsigned long long tlast;
+  int pkind;
+  int nwin, wptr, nm;
+  uint32_t warp_sums[33];
+  sb_tag_range tags_s[kTagSmem];
 };
 
 __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -97,12 +124,39 @@ __device__ __forceinline__ void set_add(int32_t* set, int32_t id) {
   }
 }
 
-// Still a candidate with exactly this key, and not touched by this insert.
-__device__ __forceinline__ bool victim_valid(const Pool& P, const int32_t* set, uint64_t k) {
+// Chain hashes of blocks this program created: a pre-program probe result
+// may be stale only for those (a miss may now hit one; a hit's id may hold a
+// re-created block), every other position's pre-program result stands.
+__device__ __forceinline__ bool created_has(const ProgState& G, uint64_t h) {
+  if (h == 0) return true;  // 0 marks an empty slot: never trust the hint
+  uint64_t s = (h ^ (h >> 31)) & static_cast<uint64_t>(G.created_mask);
+  for (;;) {
+    const unsigned long long v = G.created[s];
+    if (v == h) return true;
+    if (v == 0) return false;
+    s = (s + 1) & static_cast<uint64_t>(G.created_mask);
+  }
+}
+__device__ __forceinline__ void created_add(const ProgState& G, uint64_t h) {
+  if (h == 0) return;
+  uint64_t s = (h ^ (h >> 31)) & static_cast<uint64_t>(G.created_mask);
+  for (;;) {
+    const unsigned long long v = atomicCAS(&G.created[s], 0ull, static_cast<unsigned long long>(h));
+    if (v == 0 || v == h) return;
+    s = (s + 1) & static_cast<uint64_t>(G.created_mask);
+  }
+}
+
+// Still a candidate with exactly this key (the pool state; constant during
+// one insert's walk).
+__device__ __forceinline__ bool victim_valid_g(const Pool& P, uint64_t k) {
   const int32_t id = static_cast<int32_t>(k & P.idmask);
   if (P.ntok[id] <= 0 || P.ref[id] != 0 || P.pinned[id] != 0) return false;
-  if (victim_key(P, id) != k) return false;
-  return !set_has(set, id);
+  return victim_key(P, id) == k;
+}
+// ... and not touched by the current insert.
+__device__ __forceinline__ bool victim_valid(const Pool& P, const int32_t* set, uint64_t k) {
+  return victim_valid_g(P, k) && !set_has(set, static_cast<int32_t>(k & P.idmask));
 }
 
 // Engine::pin_partial's tag_at: first range containing pos, else USER_QUERY
@@ -148,26 +202,40 @@ __device__ void prog_flush(ProgShared& sh, uint64_t* buf, const ProgState& G) {
 // Returns a block id, or -1 (no candidate left: CacheFull), or -2 (the
 // smallest candidate cannot be decided from what the program holds: stop).
 // *late_i receives the late-list index when the victim came from there.
-__device__ int32_t prog_pop(const Pool& P, const Scratch& S, const int32_t* set, ProgShared& sh, const ProgState& G,
-                            int* late_i) {
+__device__ int32_t prog_pop(const Pool& P, const Scratch& S, const int32_t* set, const uint64_t* wkey,
+                            const int32_t* widx, ProgShared& sh, const ProgState& G, int* late_i) {
   const int lane = threadIdx.x & 31;
   *late_i = -1;
   for (;;) {
-    // list head (validated)
+    // list head: the insert's pre-validated window first, then the list
+    // beyond it validated here
     uint64_t lk = kNoKey;
+    int from_win = 0;
     if (lane == 0) {
-      int64_t p = sh.list_ptr;
-      while (p < sh.K) {
-        const uint64_t k = S.victims[p];
-        if (victim_valid(P, set, k)) {
+      while (sh.wptr < sh.nwin) {
+        const uint64_t k = wkey[sh.wptr];
+        if (!set_has(set, static_cast<int32_t>(k & P.idmask))) {
           lk = k;
+          from_win = 1;
           break;
         }
-        ++p;
+        ++sh.wptr;
       }
-      sh.list_ptr = p;
+      if (!from_win) {
+        int64_t p = max64(sh.list_ptr, sh.win_end);
+        while (p < sh.K) {
+          const uint64_t k = S.victims[p];
+          if (victim_valid(P, set, k)) {
+            lk = k;
+            break;
+          }
+          ++p;
+        }
+        sh.list_ptr = p;
+      }
     }
     lk = __shfl_sync(0xffffffffu, lk, 0);
+    from_win = __shfl_sync(0xffffffffu, from_win, 0);
     // run heads (keys cached in shared memory, validated when chosen)
     uint64_t rk = kNoKey;
     int rr = -1;
@@ -197,12 +265,19 @@ __device__ int32_t prog_pop(const Pool& P, const Scratch& S, const int32_t* set,
     tk = __shfl_sync(0xffffffffu, tk, 0);
     ti = __shfl_sync(0xffffffffu, ti, 0);
     const uint64_t best = min(lk, min(rk, tk));
-    const bool list_short = sh.list_ptr >= sh.K && sh.K < sh.ncand0;  // unselected candidates exist
+    const bool list_short = lk == kNoKey && sh.K < sh.ncand0;  // list used up, unselected candidates exist
     if (best == kNoKey) return list_short ? -2 : -1;
     // every unselected candidate's key is above the last selected one
     if (list_short && (sh.K == 0 || best > S.victims[sh.K - 1])) return -2;
     if (best == lk) {
-      if (lane == 0) sh.list_ptr += 1;
+      if (lane == 0) {
+        if (from_win) {
+          sh.list_ptr = widx[sh.wptr] + 1;
+          sh.wptr += 1;
+        } else {
+          sh.list_ptr += 1;
+        }
+      }
       __syncwarp();
       return static_cast<int32_t>(lk & P.idmask);
     }
@@ -231,11 +306,18 @@ __device__ int32_t prog_pop(const Pool& P, const Scratch& S, const int32_t* set,
 // Returns the status; sh.stop = PS_BEFORE when the op must be left for the
 // next program (no global state was modified).
 __device__ int prog_insert(const Pool& P, const Scratch& S, const ProgState& G, ProgShared& sh, int32_t* set,
-                           uint64_t* buf, const ProgOp& op, const sb_tag_range* tags, int64_t ntags) {
+                           uint64_t* buf, uint64_t* wkey, int32_t* widx, int32_t* pb, int8_t* pk, int32_t* pprobe,
+                           const ProgOp& op, const sb_tag_range* tags, int64_t ntags) {
   const int t = threadIdx.x, lane = t & 31;
   const int64_t n = op.n;
   const int64_t Pn = (n + P.bs - 1) / P.bs;
   const int64_t now = G.now;
+  // the insert's tag ranges, staged in shared memory when they fit
+  if (ntags <= kTagSmem) {
+    for (int64_t i = t; i < ntags; i += blockDim.x) sh.tags_s[i] = tags[i];
+    __syncthreads();
+    tags = sh.tags_s;
+  }
   // tag coverage (kv_cache.cpp:105-115): a CacheError with no effect
   if (!tags_cover(tags, ntags, n)) return SB_ERR_CACHE;
   if (Pn == 0) return SB_OK;
@@ -247,33 +329,109 @@ __device__ int prog_insert(const Pool& P, const Scratch& S, const ProgState& G, 
     sh.failpos = -1;
     sh.status = SB_OK;
   }
-  // live probe of every position against the current index (positions of
-  // one insert never match blocks created by the same insert)
+  // block of every position: the pre-program probe result (k_prog_bound),
+  // re-probed against the live index only where this program may have
+  // changed the answer (positions of one insert never match blocks created
+  // by the same insert)
+  if (t == 0) sh.n_probe = 0;
+  __syncthreads();
+  PROG_T(0);
+  for (int64_t p = t; p < Pn; p += blockDim.x) {
+    const int64_t off = p * P.bs;
+    const int len = static_cast<int>(min(P.bs, n - off));
+    const uint64_t h = op.hashes[p];
+    const uint64_t par = p ? op.hashes[p - 1] : kRootHash;
+    int32_t b = G.pre_all[op.pos_off + p];
+    bool probe = created_has(G, h);
+    if (b >= 0 && !(P.ntok[b] == len && P.chain[b] == h && P.parent[b] == par)) probe = true;  // evicted / reused
+    if (probe) {
+      pprobe[atomicAdd(&sh.n_probe, 1)] = static_cast<int32_t>(p);
+      b = -1;
+    }
+    pb[p] = b;
+  }
+  __syncthreads();
+  PROG_T(1);
   {
     const int pair = t >> 1, part = t & 1;
     const int pairs = blockDim.x >> 1;
-    for (int64_t base = 0; base < Pn; base += pairs) {
-      const int64_t p = base + pair;
-      const bool active = p < Pn;
-      const int64_t pc = active ? p : Pn - 1;
+    const int np = sh.n_probe;
+    for (int base = 0; base < np; base += pairs) {
+      const int i = base + pair;
+      const bool active = i < np;
+      const int64_t pc = active ? pprobe[i] : pprobe[np - 1];
       const int64_t off = pc * P.bs;
       const int len = static_cast<int>(min(P.bs, n - off));
       const uint64_t h = op.hashes[pc];
       const uint64_t parent = pc ? op.hashes[pc - 1] : kRootHash;
       const int32_t b = P.bs == 16 ? probe_find_g<true>(P, active, h, parent, op.tokens + off, len, part)
                                    : probe_find_g<false>(P, active, h, parent, op.tokens + off, len, part);
-      if (active && part == 0) {
-        int8_t fl = 0;  // 1: candidate, 2: late (ref -1, reachable through duplicate releases)
-        if (b >= 0 && P.pinned[b] == 0) {
-          const int32_t rf = P.ref[b];
-          fl = rf == 0 ? 1 : (rf == -1 ? 2 : 0);
-        }
-        S.prehit[p] = b;
-        S.kind[p] = fl;
-      }
+      if (active && part == 0) pb[pc] = b;
     }
   }
   __syncthreads();
+  PROG_T(2);
+  if (t == 0) sh.nm = 0;
+  __syncthreads();
+  for (int64_t p0 = 0; p0 < Pn; p0 += blockDim.x) {  // warp-uniform trip count
+    const int64_t p = p0 + t;
+    int8_t fl = 0;  // 1: candidate, 2: late (ref -1, reachable through duplicate releases)
+    int w = 0;      // victims this position may consume
+    if (p < Pn) {
+      const int32_t b = pb[p];
+      if (b >= 0 && P.pinned[b] == 0) {
+        const int32_t rf = P.ref[b];
+        fl = rf == 0 ? 1 : (rf == -1 ? 2 : 0);
+      }
+      pk[p] = fl;
+      w = b < 0 ? 1 : (fl == 1 ? 2 : 0);
+    }
+    w = __reduce_add_sync(0xffffffffu, w);
+    if ((t & 31) == 0 && w) atomicAdd(&sh.nm, w);
+  }
+  __syncthreads();
+  PROG_T(3);
+  // victim window: the list entries this insert's walk may take, validated
+  // against the pool state (which the walk does not change) by every thread
+  // and compacted in list order
+  {
+    const int64_t ptr0 = sh.list_ptr;
+    const int W = static_cast<int>(min64(min64(sh.K - ptr0, kWin), sh.nm > 0 ? sh.nm + 32 : 0));
+    uint32_t* flag = reinterpret_cast<uint32_t*>(buf);  // run buffer unused until the commit
+    uint64_t k0 = kNoKey, k1 = kNoKey;
+    uint32_t f0 = 0, f1 = 0;
+    if (W > 0) {
+      if (2 * t < W) {
+        k0 = S.victims[ptr0 + 2 * t];
+        f0 = victim_valid_g(P, k0);
+      }
+      if (2 * t + 1 < W) {
+        k1 = S.victims[ptr0 + 2 * t + 1];
+        f1 = victim_valid_g(P, k1);
+      }
+      flag[2 * t] = f0;
+      flag[2 * t + 1] = f1;
+      __syncthreads();
+      const uint32_t total = block_scan_2048(flag, sh.warp_sums);
+      if (f0) {
+        wkey[flag[2 * t]] = k0;
+        widx[flag[2 * t]] = static_cast<int32_t>(ptr0 + 2 * t);
+      }
+      if (f1) {
+        wkey[flag[2 * t + 1]] = k1;
+        widx[flag[2 * t + 1]] = static_cast<int32_t>(ptr0 + 2 * t + 1);
+      }
+      if (t == 0) sh.nwin = static_cast<int>(total);
+    } else if (t == 0) {
+      sh.nwin = 0;
+    }
+    if (t == 0) {
+      sh.wptr = 0;
+      sh.win_end = ptr0 + max(W, 0);
+    }
+  }
+  __syncthreads();
+  PROG_T(4);
   // ---- the walk: warp 0 replays the sequential decisions
   if (t < 32) {
     const uint64_t now_bits = static_cast<uint64_t>(now + P.lbias) << P.idb;
@@ -286,53 +444,76 @@ __device__ int prog_insert(const Pool& P, const Scratch& S, const ProgState& G, 
       int32_t b = -1;
       int8_t fl = 0;
       if (p < Pn) {
-        b = S.prehit[p];
-        fl = S.kind[p];
+        b = pb[p];
+        fl = pk[p];
       }
       // a candidate hit may have been evicted earlier in this insert
       const bool touched = b >= 0 && fl == 1 && set_has(set, b);
-      const bool plain = lane >= cnt || (b >= 0 && fl == 0);
-      const bool miss = lane >= cnt || b < 0;
-      if (__all_sync(0xffffffffu, plain)) {  // hits on non-candidates: nothing to decide
-        if (lane < cnt) {
-          S.kind[p] = 0;
-          S.chain_out[p] = b;
-        }
-        continue;
+      // leading positions that need no decision: hits on non-candidates and
+      // hits on candidates not evicted earlier in this insert (no eviction
+      // happens among them, so their order does not matter; referenced
+      // candidates are marked so no later miss of this insert evicts them)
+      const bool easy_hit = lane < cnt && b >= 0 && (fl == 0 || (fl == 1 && !touched));
+      const unsigned hard = __ballot_sync(0xffffffffu, lane < cnt && !easy_hit);
+      const int m = hard ? __ffs(hard) - 1 : cnt;
+      if (lane < m) {
+        pk[p] = 0;
+        pb[p] = b;
+        if (fl == 1) set_add(set, b);
       }
+      __syncwarp();
+      if (m == cnt) continue;
       const bool runs_live = __shfl_sync(0xffffffffu, sh.n_runs, 0) > 0;
+      const bool miss = lane < m || lane >= cnt || b < 0;
       if (__all_sync(0xffffffffu, miss) && sh.n_late == 0 && !runs_live) {
-        // every position misses: the i-th takes the next free id, else the
+        // positions m.. all miss: the i-th takes the next free id, else the
         // next valid list victim — all lanes at once
-        const int64_t a = min64(cnt, max64(0, sh.F - fi));
+        const int nm = cnt - m, mi = lane - m;  // misses, this lane's miss index
+        const int64_t a = min64(nm, max64(0, sh.F - fi));
         int32_t id = -1;
-        if (lane < a) id = S.freel[fi + lane];
-        int64_t need = cnt - a, got = 0;
+        if (mi >= 0 && mi < a) id = S.freel[fi + mi];
+        int64_t need = nm - a, got = 0;
         const bool free_short = need > 0 && sh.F < sh.free0;  // unlisted free ids: cannot decide
         if (free_short) {
           stop = PS_BEFORE;
           break;
         }
-        int64_t ptr = sh.list_ptr;
-        while (got < need && ptr < sh.K) {
-          // lanes validate the next 32 list entries; the r-th valid one goes
-          // to the (a + got + r)-th miss of the chunk
-          const int64_t e = ptr + lane;
-          const uint64_t k = e < sh.K ? S.victims[e] : kNoKey;
-          const bool v = e < sh.K && victim_valid(P, set, k);
+        while (got < need) {
+          // the next 32 candidates in list order: window entries (validated
+          // before the walk; only this insert's touched set is checked), then
+          // list entries beyond the window, validated here
+          const bool win = sh.wptr < sh.nwin;
+          const int64_t base = win ? sh.wptr : max64(sh.list_ptr, sh.win_end);
+          const int64_t lim = win ? sh.nwin : sh.K;
+          if (base >= lim) break;
+          const int64_t e = base + lane;
+          uint64_t k = kNoKey;
+          bool v = false;
+          if (e < lim) {
+            k = win ? wkey[e] : S.victims[e];
+            v = win ? !set_has(set, static_cast<int32_t>(k & P.idmask)) : victim_valid(P, set, k);
+          }
           const unsigned bal = __ballot_sync(0xffffffffu, v);
           const int rk = __popc(bal & ((1u << lane) - 1));
           const int take = static_cast<int>(min64(__popc(bal), need - got));
           if (v && rk < take) sh.wtmp[rk] = k;
           __syncwarp();
-          const int r = lane - static_cast<int>(a + got);
-          if (r >= 0 && r < take) id = static_cast<int32_t>(sh.wtmp[r] & P.idmask);
+          const int r = mi - static_cast<int>(a + got);
+          if (mi >= 0 && r >= 0 && r < take) id = static_cast<int32_t>(sh.wtmp[r] & P.idmask);
           const unsigned last = __ballot_sync(0xffffffffu, v && rk == take - 1);
-          ptr = (take > 0 && take < __popc(bal)) ? ptr + (__ffs(last) - 1) + 1 : min64(ptr + 32, sh.K);
+          const int64_t next = (take > 0 && take < __popc(bal)) ? base + (__ffs(last) - 1) + 1 : min64(base + 32, lim);
+          if (lane == 0) {
+            if (win) {
+              if (take > 0) sh.list_ptr = widx[base + (__ffs(last) - 1)] + 1;
+              sh.wptr = static_cast<int>(next);
+            } else {
+              sh.list_ptr = next;
+            }
+          }
           got += take;
           __syncwarp();
         }
-        int64_t nok = cnt;
+        int64_t nok = nm;
         if (got < need) {
           if (sh.K < sh.ncand0) {  // unselected candidates: cannot decide
             stop = PS_BEFORE;
@@ -340,17 +521,16 @@ __device__ int prog_insert(const Pool& P, const Scratch& S, const ProgState& G, 
           }
           nok = a + got;  // CacheFull at the first unassigned miss
           status = SB_ERR_CACHE_FULL;
-          failpos = p0 + nok;
+          failpos = p0 + m + nok;
         }
-        if (lane < nok) {
-          S.kind[p] = 1;
-          S.chain_out[p] = id;
-          if (lane >= a) {
+        if (mi >= 0 && mi < nok) {
+          pk[p] = 1;
+          pb[p] = id;
+          if (mi >= a) {
             set_add(set, id);
-            S.evicted[nev + (lane - a)] = id;
+            S.evicted[nev + (mi - a)] = id;
           }
         }
-        if (lane == 0) sh.list_ptr = ptr;
         nev += max64(0, nok - a);
         nnew += nok;
         fi += min64(nok, a);
@@ -358,7 +538,7 @@ __device__ int prog_insert(const Pool& P, const Scratch& S, const ProgState& G, 
         continue;
       }
       // general path: position by position (warp-uniform loop)
-      for (int i = 0; i < cnt; ++i) {
+      for (int i = m; i < cnt; ++i) {
         const int32_t bb = __shfl_sync(0xffffffffu, b, i);
         const int8_t ff = static_cast<int8_t>(__shfl_sync(0xffffffffu, static_cast<int>(fl), i));
         const bool tt = __shfl_sync(0xffffffffu, touched, i);
@@ -375,8 +555,8 @@ __device__ int prog_insert(const Pool& P, const Scratch& S, const ProgState& G, 
               sh.lpos[sh.n_late] = static_cast<int32_t>(q);
               sh.n_late += 1;
             }
-            S.kind[q] = 0;
-            S.chain_out[q] = bb;
+            pk[q] = 0;
+            pb[q] = bb;
           }
           __syncwarp();
           continue;
@@ -392,7 +572,7 @@ __device__ int prog_insert(const Pool& P, const Scratch& S, const ProgState& G, 
             break;
           }
           int li = -1;
-          id = prog_pop(P, S, set, sh, G, &li);
+          id = prog_pop(P, S, set, wkey, widx, sh, G, &li);
           if (id == -2) {
             stop = PS_BEFORE;
             break;
@@ -403,15 +583,15 @@ __device__ int prog_insert(const Pool& P, const Scratch& S, const ProgState& G, 
             break;
           }
           if (lane == 0) {
-            if (li >= 0) S.kind[sh.lpos[li]] = 2;  // hit, then evicted later in this insert
+            if (li >= 0) pk[sh.lpos[li]] = 2;  // hit, then evicted later in this insert
             set_add(set, id);
             S.evicted[nev] = id;
           }
           ++nev;
         }
         if (lane == 0) {
-          S.kind[q] = 1;
-          S.chain_out[q] = id;
+          pk[q] = 1;
+          pb[q] = id;
         }
         ++nnew;
         __syncwarp();
@@ -427,6 +607,7 @@ __device__ int prog_insert(const Pool& P, const Scratch& S, const ProgState& G, 
     }
   }
   __syncthreads();
+  PROG_T(5);
   if (sh.stop != PS_NONE) return SB_OK;
   const int status = sh.status;
   const int64_t nev = sh.nev;
@@ -437,11 +618,12 @@ __device__ int prog_insert(const Pool& P, const Scratch& S, const ProgState& G, 
     P.ntok[v] = 0;
   }
   __syncthreads();
+  PROG_T(6);
   const int64_t limit = status == SB_OK ? Pn : sh.failpos;
   for (int64_t p = t; p < Pn; p += blockDim.x) {
     if (p < limit) {
-      const int kd = S.kind[p];
-      const int32_t id = S.chain_out[p];
+      const int kd = pk[p];
+      const int32_t id = pb[p];
       if (kd == 0) {
         if (status == SB_OK) P.ref[id] += 1;  // distinct blocks per position
         P.last[id] = now;
@@ -449,7 +631,15 @@ __device__ int prog_insert(const Pool& P, const Scratch& S, const ProgState& G, 
         const int64_t off = p * P.bs;
         const int len = static_cast<int>(min(P.bs, n - off));
         uint64_t* dst = P.tok + static_cast<int64_t>(id) * P.bs;
-        for (int i = 0; i < len; ++i) dst[i] = op.tokens[off + i];
+        if (len == 16) {  // all loads in flight before the stores
+          uint64_t v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = op.tokens[off + i];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) dst[i] = v[i];
+        } else {
+          for (int i = 0; i < len; ++i) dst[i] = op.tokens[off + i];
+        }
         const uint64_t h = op.hashes[p];
         const uint64_t par = p ? op.hashes[p - 1] : kRootHash;
         P.ntok[id] = len;
@@ -460,9 +650,10 @@ __device__ int prog_insert(const Pool& P, const Scratch& S, const ProgState& G, 
         P.last[id] = now;
         P.pinned[id] = 0;
         index_insert(P, h, id, par, len);
+        created_add(G, h);
       }
     }
-    op.ids[p] = status == SB_OK ? S.chain_out[p] : -1;
+    op.ids[p] = status == SB_OK ? pb[p] : -1;
   }
   if (t == 0) {
     if (nev > 0) {
@@ -480,6 +671,7 @@ __device__ int prog_insert(const Pool& P, const Scratch& S, const ProgState& G, 
     G.out[3] += status == SB_OK ? sh.nnew : 0;
   }
   __syncthreads();
+  PROG_T(7);
   // late candidates raised to ref 0 and not evicted are candidates from now on
   if (status == SB_OK) {
     if (t < sh.n_late && sh.lkey[t] != kNoKey) {
@@ -489,6 +681,7 @@ __device__ int prog_insert(const Pool& P, const Scratch& S, const ProgState& G, 
     __syncthreads();
     prog_flush(sh, buf, G);
   }
+  PROG_T(8);
   (void)lane;
   return status;
 }
@@ -551,6 +744,11 @@ __global__ void __launch_bounds__(kProgThreads, 1) k_program(Pool P, Scratch S, 
   extern __shared__ __align__(16) uint8_t prog_dyn[];
   int32_t* set = reinterpret_cast<int32_t*>(prog_dyn);
   uint64_t* buf = reinterpret_cast<uint64_t*>(prog_dyn + kSetSlots * sizeof(int32_t));
+  uint64_t* wkey = buf + kRunBuf;                            // victim window keys
+  int32_t* widx = reinterpret_cast<int32_t*>(wkey + kWin);   // ... and their list positions
+  int32_t* pb = widx + kWin;                                 // per position: block (after the walk: the chain id)
+  int32_t* pprobe = pb + kProgMaxPos;                       // positions to re-probe
+  int8_t* pk = reinterpret_cast<int8_t*>(pprobe + kProgMaxPos);  // per position: candidacy, then kind
   __shared__ ProgShared sh;
   __shared__ sb_tag_range pin_range;
   const int t = threadIdx.x;
@@ -567,12 +765,14 @@ __global__ void __launch_bounds__(kProgThreads, 1) k_program(Pool P, Scratch S, 
     sh.sort_overflow = 0;
     sh.stop = PS_NONE;
     sh.n_late = 0;
+    sh.tlast = clock64();
   }
   __syncthreads();
   int c = G.first;
   for (; c < G.n_ops; ++c) {
     const ProgOp op = G.ops[c];
     const int64_t Pn = (op.n + P.bs - 1) / P.bs;
+    if (t == 0) sh.pkind = op.kind;
     // resources this op may need: runs and run storage (worst case)
     const int64_t pushes = (op.kind == PK_INSERT ? 0 : op.n_chain + op.n_pinned + Pn) + kLateMax;
     const int64_t runs_needed = 3 + (pushes + kRunBuf - 1) / kRunBuf * 2;
@@ -592,6 +792,7 @@ __global__ void __launch_bounds__(kProgThreads, 1) k_program(Pool P, Scratch S, 
         Pn > S.pmax) {
       break;  // left for the next program
     }
+    PROG_T(9);
     ProgRes r{SB_OK, PO_NONE, op.n_chain, op.n_pinned};
     int stop_after = 0;
     const bool inserts = op.kind != PK_ABANDON;
@@ -605,7 +806,7 @@ __global__ void __launch_bounds__(kProgThreads, 1) k_program(Pool P, Scratch S, 
         tg = &pin_range;
         ntg = 1;
       }
-      ist = prog_insert(P, S, G, sh, set, buf, op, tg, ntg);
+      ist = prog_insert(P, S, G, sh, set, buf, wkey, widx, pb, pk, pprobe, op, tg, ntg);
       if (sh.stop == PS_BEFORE) break;
       if (ist == SB_ERR_CACHE_FULL) stop_after = 1;
     }
@@ -700,6 +901,7 @@ __global__ void __launch_bounds__(kProgThreads, 1) k_program(Pool P, Scratch S, 
         stop_after = 2;
     }
     __syncthreads();
+    PROG_T(10);
     if (t == 0) G.res[c] = r;
     if (stop_after) {
       if (t == 0) sh.stop = stop_after == 2 ? PS_ERROR : PS_AFTER;
@@ -716,12 +918,15 @@ __global__ void __launch_bounds__(kProgThreads, 1) k_program(Pool P, Scratch S, 
   }
 }
 
-// Upper bound of the victims / free ids a program can consume: every insert
-// position that misses in the pre-program state, plus twice every position
-// that hits a current candidate (it may be evicted first, and its list
-// entry is then skipped), plus slack.  One lane pair per position.
+// Pre-program probe of every insert position (kept for the program as a
+// hint) and the bound of the victims / free ids the program can consume:
+// every position that misses in the pre-program state, plus twice every
+// position that hits a current candidate (it may be evicted first, and its
+// list entry is then skipped), plus slack — and none at all when no position
+// misses (a hit can only turn into a miss after an eviction, which needs a
+// miss first).  One lane pair per position.
 __global__ void __launch_bounds__(256) k_prog_bound(Pool P, const ProgOp* __restrict__ ops, int first, int n_ops,
-                                                    int64_t* scal) {
+                                                    int64_t* scal, int32_t* pre_all) {
   const int o = first + blockIdx.x;
   const ProgOp op = ops[o];
   if (op.kind == PK_ABANDON) return;
@@ -738,10 +943,13 @@ __global__ void __launch_bounds__(256) k_prog_bound(Pool P, const ProgOp* __rest
   const int32_t b = P.bs == 16 ? probe_find_g<true>(P, active, h, parent, op.tokens + off, len, part)
                                : probe_find_g<false>(P, active, h, parent, op.tokens + off, len, part);
   if (!active || part) return;
-  int64_t add = 0;
-  if (b < 0) add = 1;
-  else if (P.pinned[b] == 0 && P.ref[b] <= 0) add = 2;
-  if (add) atomicAdd(reinterpret_cast<unsigned long long*>(&scal[S_BOUND]), static_cast<unsigned long long>(add));
+  pre_all[op.pos_off + p] = b;
+  if (b < 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&scal[S_NMISS]), 1ull);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&scal[S_BOUND]), 1ull);
+  } else if (P.pinned[b] == 0 && P.ref[b] <= 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&scal[S_BOUND]), 2ull);
+  }
 }
 
 // ---- descriptor lookups: KvCache::lookup_prefix (kv_cache.cpp:85-101) of

@@ -24,6 +24,7 @@ struct ProgOp {
   int32_t n_pinned;      // the call's partial-prefill pins (engine.hpp:154)
   int32_t _pad;
   int64_t n;             // insert tokens
+  int64_t pos_off;       // first slot of this op's block positions in the pre-program probe array (host-filled)
   const uint64_t* tokens;
   const uint64_t* hashes;  // chain hash of every insert block
   const sb_tag_range* ins_tags;
