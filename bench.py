@@ -1,21 +1,31 @@
 """Benchmark of the engine-side hot path of Sutradhara on B200.
 
-Workload = BASELINE.json configs[1]: 64 concurrent agentic requests (4-8 tool
-iterations each) sharing a 2K-token system prefix, each caught at the moment
-its tool outputs arrive.  One step = one batched continuation prefill over
-the Llama-3-8B-shaped paged KV pool (32 layers, 32 q / 8 kv heads, d=128):
+Headline (BASELINE.json configs[1]): 64 concurrent agentic requests (4-8 tool
+iterations each) sharing a 2K-token system prefix, each at the moment its
+tool outputs arrive.  One step = the engine-side lifecycle of those 64 calls
+over the Llama-3-8B-shaped paged KV pool (32 layers, 32 q / 8 kv heads):
 
-  chain-hash the prompts (prefix hashes gathered from the pinned pool blocks,
-  suffix folded) -> prefix lookup -> insert (hint-aware eviction under pool
-  pressure) -> block tables -> per layer {KV append, continuation attention}
-  -> release
+  submit_partial_prefill (prefix chain hashes + admission lookups) ->
+  pin_partial -> extend_prefill (tool outputs, suffix-only hashing) ->
+  complete_prefill (insert with hint-aware eviction, release pins / partial
+  refs) -> per layer {KV append, continuation attention} -> finish_decode
 
-``value`` is suffix (tool-output) tokens per second with inputs resident in
-HBM; ``e2e`` is the same through the public engine API with the step's
-suffix tokens copied host->device and an output sample copied back, inside
-the timed region.  The per-layer q / k / v of this step are seeded stand-ins
-generated once per batch: the dense layers around the attention are measured
-separately as ``full_model`` (configs[2], the whole Llama-3-8B-shaped model).
+each KV transition one op program over the batch (reference semantics).
+``value`` is tool-output tokens per second with inputs resident in HBM;
+``e2e`` is the same through the public engine API with the step's suffix
+tokens copied host->device and an output row copied back, inside the timed
+region.  The per-layer q / k / v are seeded stand-ins generated once per
+batch; the full dense model is ``full_model`` (configs[2]).
+
+Also in the line: ``roofline`` (the attention, tensor-bound), ``pool``
+(the engine-side KV work of the step, timed live), ``roofline_pool`` (the
+pool kernels at the largest single-GPU configs, HBM-bound), ``trace``
+(configs[3]: one 512-request synthetic agent trace sharded over the ranks,
+replayed by the UNMODIFIED reference engine/orchestrator on the B200 pool),
+``pressure`` (configs[4]: pool at 25-100 % of the working set, hint-aware vs
+LRU), ``thrashing`` (configs[0]: the paper's scenario, LRU vs hint), and
+``cpu_baseline`` (the reference's own KvCache + engine lifecycle code for the
+same step, measured in full on the host).
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
@@ -48,7 +58,9 @@ def parse():
     ap.add_argument("--requests", type=int, default=N_REQ)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true", help="skip the configs[2] full-model measurement")
-    ap.add_argument("--no-trace", action="store_true", help="skip the trace replay (p50 FTR / hit rate)")
+    ap.add_argument("--no-trace", action="store_true", help="skip configs[3] / [4] / [0] (drop-in trace metrics)")
+    ap.add_argument("--no-pool-roofline", action="store_true", help="skip the pool-kernel rooflines")
+    ap.add_argument("--trace-requests", type=int, default=512)
     return ap.parse_args()
 
 
@@ -202,14 +214,14 @@ def run_ours(args, rank, world, local_rank):
 
     sample_buf = torch.empty(LLAMA3_8B.n_q_heads * LLAMA3_8B.head_dim, dtype=torch.int16).pin_memory()
 
-    def step(s, e2e=False, time_attention=False):
+    def step(s, e2e=False, timed=False):
         nonlocal now
         now += 1
         if e2e:
             batch.stage_suffix_host(suffix_host[s])
         else:
             batch.stage_suffix_device(suffix_dev[s])
-        n = batch.run(now, seed=s, time_attention=time_attention)
+        n = batch.run(now, seed=s, time_attention=timed)
         if e2e:
             return n, batch.output_sample(sample_buf)  # last token's output row, last layer (D2H)
         return n, 0
@@ -230,11 +242,12 @@ def run_ours(args, rank, world, local_rank):
     t0.record()
     launches = 0
     for s in range(args.warmup, args.warmup + args.steps):
-        launches += step(s, time_attention=(s == args.warmup + args.steps - 1))[0]
+        launches += step(s, timed=(s == args.warmup + args.steps - 1))[0]
     t1.record()
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
     attn_ms = batch.attention_ms()  # per-layer launches of the last timed step (CUDA events, same stream)
+    pool_ms = batch.pool_ms()       # its engine-side KV phases
     # ---- timed: end to end through the public API (H2D suffix, D2H sample)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -251,27 +264,30 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop()
 
     attn_avg_ms = float(np.mean(attn_ms))
-    # hit rate of the admission lookups (prefix hit tokens / prompt tokens)
+    # hint-aware KV hit rate of the admission lookups (cached prefix tokens / prompt tokens)
     hits, status, _ = batch.results()
     hit_rate = float(hits.sum()) / float(sum(batch.full_lens))
     stats = eng.cache.stats()
-    assert (status == 0).all()
+    assert (status == 0).all() and (batch.pin_outcomes() == 1).all()
 
     # max over ranks; NCCL only for the cross-GPU statistics reduction
     mx, sm = reduce_over_ranks([ms, ms_e2e, float(hits.sum()), float(sum(batch.full_lens)),
-                                float(stats["evicted_blocks"]), attn_avg_ms], dev)
-    ms, ms_e2e, attn_avg_ms = mx[0], mx[1], mx[5]
+                                float(stats["evicted_blocks"]), attn_avg_ms, sum(pool_ms)], dev)
+    ms, ms_e2e, attn_avg_ms, pool_total = mx[0], mx[1], mx[5], mx[6]
     hit_rate = sm[2] / sm[3]
     prefix_tokens = int(sum(batch.prefix_lens))
     del batch, eng
     torch.cuda.empty_cache()
     # configs[2] on every rank (weak scaling; its timing is max-reduced over ranks)
     full_model = None if args.no_dense else run_dense(args, rank, world, local_rank)
-    trace = None
-    if not args.no_trace:  # sharded over the ranks, gathered on rank 0
-        per_gpu = tokens_per_step / (ms / args.steps) * 1e3
-        per_gpu_full = full_model["tokens_per_s"] / world if full_model else None
-        trace = trace_replay_metrics(per_gpu, local_rank, per_gpu_full, rank, world, dev)
+    extra = {}
+    if not args.no_trace:  # configs[3] sharded over the ranks, [4] points spread over the ranks, [0]
+        extra = dropin_metrics(args, rank, world, local_rank, dev)
+    roof_pool = None
+    if not args.no_pool_roofline and rank == 0:
+        roof_pool = pool_rooflines()
+    if world > 1:
+        dist.barrier()
     if rank != 0:
         return None
 
@@ -294,7 +310,8 @@ def run_ours(args, rank, world, local_rank):
         "data": "synthetic (deterministic agentic trace; random-init Llama-3-8B-shaped KV/activations)",
         "config": {
             "workload": "configs[1]: 64 concurrent agentic requests, 4-8 tool iterations, shared 2K-token system "
-                        "prefix; continuation prefill of each request's tool outputs over its cached prefix",
+                        "prefix; per step the engine-side lifecycle of 64 continuations (admission lookup, pin, "
+                        "extend with fresh tool outputs, complete with hint-aware eviction, attention, finish)",
             "model_shape": "Llama-3-8B attention: 32 layers x 32 q / 8 kv heads x 128, 16-token KV pages",
             "requests_per_gpu": args.requests,
             "suffix_tokens_per_step_per_gpu": tokens_per_step,
@@ -302,10 +319,12 @@ def run_ours(args, rank, world, local_rank):
             "kv_pool_blocks_per_gpu": cap,
             "kv_pool_gib_per_gpu": round(cap * LLAMA3_8B.kv_bytes_per_token * 16 / 2**30, 1),
             "eviction_policy": "tiered (hint-aware)",
-            "parallelism": f"requests sharded, {world} independent pools; NCCL all-reduce of cache stats only",
+            "parallelism": f"requests sharded, {world} independent pools; NCCL only for the statistics reduction "
+                           "and the gather of per-request trace metrics",
             "l2": "inputs larger than L2 (KV pool >> 126 MB)",
-            "scope": "hash + lookup + insert/evict + KV append + attention (q/k/v stand-ins generated once per "
-                     "batch); the full dense model is the separate full_model measurement",
+            "scope": "prefix hashing + admission lookup + pin + suffix hashing + complete (insert/evict) + KV "
+                     "append + attention + finish (q/k/v stand-ins generated once per batch); the full dense "
+                     "model is the separate full_model measurement",
         },
         "hit_rate": hit_rate,
         "evicted_blocks_per_step": stats["evicted_blocks"] / max(1, (args.warmup + 2 * args.steps)),
@@ -318,6 +337,13 @@ def run_ours(args, rank, world, local_rank):
                      "peak_source": f"{peak_kind} bf16_tflops_sustained (kernel timed inside a long step)",
                      "flops_per_launch": flops_attn, "avg_launch_ms": attn_avg_ms,
                      "launches_timed": len(attn_ms)},
+        "pool": {"ms_per_step": pool_total, "share_of_step": pool_total / (ms / args.steps),
+                 "phases_ms": {"submit_and_pin": pool_ms[0], "extend_and_complete": pool_ms[1],
+                               "finish": pool_ms[2]},
+                 "tokens_per_s_pool_only": tokens_per_step * world / (pool_total * 1e-3),
+                 "note": "CUDA events around the engine-side KV phases of the last timed step (hashing, lookups, "
+                         "op programs incl. their scoring/select and host syncs); the rest of the step is KV "
+                         "append + attention"},
         "clocks": clk,
     }
     pw, lim = clk.get("power_w"), clk.get("power_limit_w")
@@ -338,10 +364,11 @@ def run_ours(args, rank, world, local_rank):
                     "3 alternating rounds of 6 launches each (median)"}
     except Exception as e:  # library absent or incompatible: no reference point
         line["roofline"]["library_reference"] = {"unavailable": str(e)[:200]}
-    if trace is not None:
-        line.update(trace)
+    if roof_pool is not None:
+        line["roofline_pool"] = roof_pool
+    line.update(extra)
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(reqs, budget_s=20.0)
+        line["cpu_baseline"] = cpu_baseline(reqs)
     return line
 
 
@@ -447,138 +474,191 @@ def run_dense(args, rank, world, local_rank):
     return out
 
 
-TRACE = dict(n_requests=60, seed=1, capacity_blocks=8192, workload="default")
+# configs[3]: ONE synthetic agent trace of the reference generator, request
+# i -> rank i mod N, each rank's shard on its own pool of TRACE_POOL blocks
+TRACE_SEED, TRACE_POOL = 1, 8192
+# configs[4]: a lighter workload (smaller prompts/outputs) so the pool can be
+# swept across its working set; points spread over the ranks
+PRESSURE_GEN = [320.0, 48.0, 24.0, 48.0, 0.5, 0.3, 0.45, 0.0]
+PRESSURE_REQUESTS = 128
 
 
-def trace_replay_metrics(tokens_per_s: float, device: int, full_model_tokens_per_s=None, rank: int = 0,
-                         world: int = 1, dev=None):
-    """p50 FTR and hint-aware hit rate on the reference's synthetic agent
-    trace (trace_gen default workload, 60 requests per GPU, 8192-block pool per
-    GPU), replayed with every KV decision on the B200 pool (csrc/replay.cu):
-    - reference cost model: identical to the reference simulator's numbers
-      (tests/test_replay_gpu.py), for the Sutradhara and Baseline presets;
-    - B200-calibrated: prefill charged at the measured per-GPU full-model
-      continuation-prefill rate (configs[2], all dense layers + attention) when
-      available, else at the attention-path rate, instead of the reference's
-      0.05 ms/token (decode model unchanged).
-    With N GPUs the trace is sharded: rank r replays its own 60 requests (seed
-    1 + r) on its own pool, and the per-request FTRs and the hit / prompt /
-    eviction counters are gathered over NCCL for the job-wide p50 and hit rate
-    (the only cross-GPU traffic)."""
+def _p50(v):
+    v = np.sort(np.asarray(v))
+    return float(v[max(1, int(np.ceil(0.5 * len(v)))) - 1]) if len(v) else None
+
+
+def gather_rows(rows: np.ndarray, world: int, dev=None) -> np.ndarray:
+    """All-gather of per-rank 2-D float64 tables (rows padded to the largest
+    shard) — the only collective of the trace metrics."""
     import torch
-    from paper_2601_12967_b200.replay import replay
+    import torch.distributed as dist
 
-    cfg = dict(TRACE)
-    cfg["seed"] = TRACE["seed"] + rank
-    t0 = time.perf_counter()
-    runs = {"sutradhara": replay(preset="sutradhara", device=device, **cfg)}
-    wall = time.perf_counter() - t0
-    runs["baseline"] = replay(preset="baseline", device=device, **cfg)
-    rate = full_model_tokens_per_s or tokens_per_s
-    cal_cost = [1000.0 / rate, 20.0, 2.0, 256]
-    runs["sutradhara_cal"] = replay(preset="sutradhara", device=device, cost=cal_cost, **cfg)
-    runs["baseline_cal"] = replay(preset="baseline", device=device, cost=cal_cost, **cfg)
-
-    def gathered(r):
-        """(all ranks' FTRs, e2e times, hit tokens, prompt tokens, evictions)"""
-        row = np.concatenate([r.ftr_ms, r.e2e_ms, [r.hit_tokens.sum(), r.prompt_tokens.sum(), r.evictions]])
-        t = torch.tensor(row, dtype=torch.float64, device=dev)
-        import torch.distributed as dist
-
-        if world > 1 and dist.is_initialized():
-            if dist.get_backend() == "gloo":
-                t = t.cpu()
-            parts = [torch.empty_like(t) for _ in range(world)]
-            dist.all_gather(parts, t)
-            t = torch.stack(parts)
-        else:
-            t = t[None]
-        a = t.cpu().numpy()
-        n = len(r.ftr_ms)
-        return a[:, :n].ravel(), a[:, n:2 * n].ravel(), a[:, 2 * n].sum(), a[:, 2 * n + 1].sum(), a[:, 2 * n + 2].sum()
-
-    def p50(v):
-        v = np.sort(v)
-        return float(v[max(1, int(np.ceil(0.5 * len(v)))) - 1])
-
-    g = {k: gathered(r) for k, r in runs.items()}
-    if rank != 0:
-        return None
-    summ = {k: {"p50_ftr_ms": p50(v[0]), "p50_e2e_ms": p50(v[1]), "hit_rate": float(v[2] / max(1.0, v[3])),
-                "evictions": int(v[4])} for k, v in g.items()}
-    out = {"p50_ftr_ms": summ["sutradhara"]["p50_ftr_ms"]}
-    out["trace"] = {
-        "workload": f"reference trace_gen default workload, 60 requests per GPU (seeds 1..{world}), "
-                    f"pool 8192 x 16-token blocks per GPU, {world} GPU(s)",
-        "sutradhara": summ["sutradhara"],
-        "baseline": summ["baseline"],
-        "b200_calibrated": {"prefill_ms_per_token": cal_cost[0],
-                            "prefill_rate_source": "full_model (configs[2]), per GPU" if full_model_tokens_per_s
-                            else "attention path (configs[1]), per GPU",
-                            "sutradhara_p50_ftr_ms": summ["sutradhara_cal"]["p50_ftr_ms"],
-                            "baseline_p50_ftr_ms": summ["baseline_cal"]["p50_ftr_ms"],
-                            "sutradhara_hit_rate": summ["sutradhara_cal"]["hit_rate"]},
-        "replay_wall_s": wall,
-    }
-    out["hint_aware_hit_rate"] = summ["sutradhara"]["hit_rate"]
+    if world <= 1 or not (dist.is_available() and dist.is_initialized()):
+        return rows
+    gloo = dist.get_backend() == "gloo"
+    n = torch.tensor([rows.shape[0]], dtype=torch.int64, device=None if gloo else dev)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(ns, n)
+    m = int(max(int(x.item()) for x in ns))
+    pad = np.full((m, rows.shape[1]), np.nan)
+    pad[: rows.shape[0]] = rows
+    t = torch.from_numpy(pad).to(None if gloo else dev)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    out = np.concatenate([p.cpu().numpy()[: int(k.item())] for p, k in zip(parts, ns)])
     return out
 
 
-# ----------------------------------------------------------- CPU reference
-def cpu_baseline(reqs, budget_s: float = 20.0, threads: int = 0):
-    """The reference's own CPU path on a bounded sample of one step:
-    KvCache lookup + insert + release of the reference (oracle/_ref, built from
-    /root/reference) for as many requests as fit the budget, plus an fp32
-    attention port for one request x one layer; both extrapolated to the full
-    step by new-block count and FLOPs.  The reference computes no attention
-    itself (its engine charges a cost model, engine.cpp:35-39)."""
-    import torch
-    from oracle import oracle as O
-    from paper_2601_12967_b200 import workload as W
-    from paper_2601_12967_b200.attention import attention_flops
-    from paper_2601_12967_b200.engine import LLAMA3_8B
+def trace_summary(tab: np.ndarray, evictions: float, wall: float) -> dict:
+    """tab columns: ftr, e2e, hit, prompt, tool, wait, prefill, decode."""
+    ftr, e2e, hit, prm, tool = tab[:, 0], tab[:, 1], tab[:, 2], tab[:, 3], tab[:, 4]
+    share = tool / np.maximum(ftr, 1.0)
+    return {"requests": int(len(ftr)), "p50_ftr_ms": _p50(ftr), "p90_ftr_ms": float(np.percentile(ftr, 90)),
+            "p50_e2e_ms": _p50(e2e), "hit_rate": float(hit.sum() / max(1.0, prm.sum())), "evictions": int(evictions),
+            "tool_share_of_ftr": {"p10": float(np.percentile(share, 10)), "p50": float(np.percentile(share, 50)),
+                                  "p90": float(np.percentile(share, 90)),
+                                  "frac_in_30_80pct": float(((share >= 0.3) & (share <= 0.8)).mean()),
+                                  "definition": "critical (non-overlapped) tool time / FTR, the FTR breakdown of "
+                                                "metrics.cpp:104-129"},
+            "replay_wall_s": wall}
 
-    if threads:
-        torch.set_num_threads(threads)
-    cores = torch.get_num_threads()
-    pre_b, suf_b, cap = capacity_for(reqs)
+
+def dropin_metrics(args, rank, world, local_rank, dev, lib_path=None):
+    """configs[3] / [4] / [0] through the drop-in: the UNMODIFIED reference
+    engine and orchestrator with every KV decision on this rank's B200 pool
+    (paper_2601_12967_b200/dropin.py).  lib_path = the pure reference library
+    for the reference arm."""
+    from paper_2601_12967_b200 import dropin as D
+
+    os.environ["SB_DEVICE"] = str(local_rank)  # the binding's pool device
+    kw = {} if lib_path is None else {"lib_path": lib_path}
+    out = {}
+    # ---- configs[3]: one trace, sharded
+    res = {}
+    for preset in ("sutradhara", "baseline"):
+        r = D.run_shard(args.trace_requests, TRACE_SEED, preset, TRACE_POOL, shard=rank, n_shards=world, **kw)
+        tab = np.stack([r.ftr_ms, r.e2e_ms, r.hit_tokens, r.prompt_tokens, r.tool_ms, r.wait_ms, r.prefill_ms,
+                        r.decode_ms], 1).astype(np.float64)
+        tab = gather_rows(tab, world, dev)
+        ev = gather_rows(np.array([[r.evictions, r.wall_s]], np.float64), world, dev)
+        res[preset] = trace_summary(tab, ev[:, 0].sum(), float(ev[:, 1].max()))
+    out["p50_ftr_ms"] = res["sutradhara"]["p50_ftr_ms"]
+    out["hint_aware_hit_rate"] = res["sutradhara"]["hit_rate"]
+    out["trace"] = {
+        "workload": f"configs[3]: reference trace_gen default workload, {args.trace_requests} requests (seed "
+                    f"{TRACE_SEED}), request i on rank i mod {world}, {TRACE_POOL}-block pool per rank; replayed by "
+                    "the unmodified reference engine/orchestrator with its KvCache on the B200 pool "
+                    "(integration/agentsim_kvcache_b200.cpp), reference cost model",
+        "sutradhara": res["sutradhara"], "baseline": res["baseline"],
+        "ftr_p50_improvement": 1.0 - res["sutradhara"]["p50_ftr_ms"] / res["baseline"]["p50_ftr_ms"]}
+    # ---- configs[4]: pool pressure sweep, hint-aware vs LRU (points spread over the ranks)
+    big = D.run_shard(PRESSURE_REQUESTS, TRACE_SEED, "sutradhara", 1 << 22, gen=PRESSURE_GEN, **kw)
+    working = int(np.ceil(float(big.prompt_tokens.sum() - big.hit_tokens.sum()) / 16))
+    points = [(f, pol) for f in (0.25, 0.5, 0.75, 1.0) for pol in (1, 0)]
+    rows = []
+    for i, (f, pol) in enumerate(points):
+        if i % world != rank:
+            continue
+        r = D.run_shard(PRESSURE_REQUESTS, TRACE_SEED, "sutradhara", max(16, int(f * working)), gen=PRESSURE_GEN,
+                        kv_tiering=pol, **kw)
+        rows.append([i, f, pol, _p50(r.ftr_ms), float(r.hit_tokens.sum() / max(1, r.prompt_tokens.sum())),
+                     r.evictions])
+    rows = gather_rows(np.array(rows, np.float64).reshape(-1, 6), world, dev)
+    sweep = []
+    for f in (0.25, 0.5, 0.75, 1.0):
+        pt = {"pool_fraction_of_working_set": f, "pool_blocks": max(16, int(f * working))}
+        for r in rows:
+            if r[1] == f:
+                k = "hint_aware" if r[2] == 1 else "lru"
+                pt[k] = {"p50_ftr_ms": r[3], "hit_rate": r[4], "evictions": int(r[5])}
+        sweep.append(pt)
+    out["pressure"] = {"workload": f"configs[4]: {PRESSURE_REQUESTS}-request trace (trace_gen default, prompt/tool "
+                                  f"sizes {PRESSURE_GEN[:4]}), Sutradhara preset, kv_tiering on (hint-aware) vs off "
+                                  f"(LRU); working set = blocks the trace inserts with an unbounded pool",
+                       "working_set_blocks": working, "points": sweep}
+    # ---- configs[0]: the paper's KV-thrashing scenario, LRU vs hint
+    if rank == 0:
+        lru, hint = D.thrashing(False, **kw), D.thrashing(True, **kw)
+        out["thrashing"] = {"workload": "configs[0]-scale: scenarios.cpp:45-85, three 2-iteration requests whose "
+                                        "first-iteration chains exactly fill a 120-block pool (16-token blocks)",
+                            "lru": {"it2_hit_tokens": lru[0], "hit_rate": lru[1], "evictions": lru[2]},
+                            "hint_aware": {"it2_hit_tokens": hint[0], "hit_rate": hint[1], "evictions": hint[2]}}
+    return out
+
+
+def pool_rooflines():
+    """The pool kernels at the largest single-GPU configs (bench_kv.py),
+    algorithmic bytes / device time vs the measured HBM bandwidth."""
+    import bench_kv
+
+    bench_kv.QUIET = True
+    bench_kv.ROWS.clear()
+    bench_kv.main("hash,probe_big,evict_small,evict,append")
+    keep = []
+    for r in bench_kv.ROWS:
+        keep.append({k: r[k] for k in ("kernel", "config", "achieved_gbs", "peak_gbs", "frac", "seconds",
+                                        "algorithmic_bytes", "timing") if k in r} | (
+            {"parts_us": r["parts_us"]} if "parts_us" in r else {}))
+    return {"bound": "hbm", "unit": "GB/s", "rows": keep,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
+            "bytes": "algorithmic bytes per launch (bench_kv.py docstring / DESIGN.md), CUPTI device time, L2 "
+                     "flushed between launches"}
+
+
+# ----------------------------------------------------------- CPU reference
+def reference_step(reqs, steps: int, warmup: int):
+    """The reference's own code for the engine-side KV work of the configs[1]
+    step: its KvCache (kv_cache.cpp, compiled in oracle/_ref) driven by the
+    engine lifecycle of engine.cpp:128-347 (oracle/engine_oracle.py) — the
+    same per-step calls as our batch (64 lookups, pins, extensions,
+    completions, finishes at one virtual time), measured in full.  Returns
+    (seconds per timed step, kind)."""
+    from oracle import oracle as O
+    from oracle.engine_oracle import EngineOracle
+    from paper_2601_12967_b200 import workload as W
+
+    _, _, cap = capacity_for(reqs)
     kind = "reference"
     try:
         c = O.RefCache(16, cap, 1)
     except Exception:
         c = O.OracleCache(16, cap, 1)
         kind = "port"
-    for r in reqs:
-        st, ids = c.insert(r.prefix_tokens, r.prefix_tags, 0)
-        c.set_reuse_priority(ids, 1, 4)
-    # one warm step so the pool is at steady-state pressure, then the timed sample
-    t_cache, new_blocks_done, done = 0.0, 0, 0
-    total_new = sum((r.suffix_len + 15) // 16 for r in reqs)
-    for phase in (0, 1):
+    eo = EngineOracle(c, 16)
+    keys = [hash((1, i)) & 0xFFFFFFFFFFFF for i in range(len(reqs))]
+    times = []
+    for s in range(warmup + steps):
+        now = 10 + s
+        sfx = [W.fresh_suffix_tokens(r, s) for r in reqs]
         t0 = time.perf_counter()
-        for i, r in enumerate(reqs):
-            toks = np.concatenate([r.prefix_tokens, W.fresh_suffix_tokens(r, 100 + phase)])
-            tags = list(r.prefix_tags) + [(r.prefix_len, len(toks), 1)]
-            c.lookup_prefix(toks, 10 + phase)
-            st, ids = c.insert(toks, tags, 10 + phase)
-            if st == 0:
-                c.release(ids)
-            if phase == 1:
-                done += 1
-                new_blocks_done += (r.suffix_len + 15) // 16
-                if time.perf_counter() - t0 > budget_s / 2:
-                    break
-            elif time.perf_counter() - t0 > budget_s:
-                break
-        if phase == 1:
-            t_cache = time.perf_counter() - t0
-    t_cache_full = t_cache * total_new / max(1, new_blocks_done)
-    # attention port: fp32 on the host cores, one layer of as many requests as
-    # fit an ~8 s budget (cycling through the batch), extrapolated by FLOPs
+        calls = [eo.submit(r.prefix_tokens, r.prefix_tags, now, partial=True) for r in reqs]
+        for cid in calls:
+            eo.prefill_done(cid, now)
+        for cid, x in zip(calls, sfx):
+            eo.extend(cid, x, [(0, len(x), 1)], now)
+        for cid in calls:
+            eo.prefill_done(cid, now)
+        for i, cid in enumerate(calls):
+            eo.finish(cid, np.array([O.decode_token(keys[i], 0)], np.uint64), now)
+        dt = time.perf_counter() - t0
+        if s >= warmup:
+            times.append(dt)
+        eo.calls.clear()
+    return float(np.mean(times)), kind
+
+
+def attention_port(reqs, budget_s: float = 8.0):
+    """fp32 attention of the step on the host cores (torch), request-layers
+    timed until the budget: the compute the reference only charges."""
+    import torch
+    from paper_2601_12967_b200.attention import attention_flops
+    from paper_2601_12967_b200.engine import LLAMA3_8B
+
     sh = LLAMA3_8B
     g = torch.Generator().manual_seed(0)
     t_attn, f_sample, n_done = 0.0, 0.0, 0
-    while t_attn < 8.0 and n_done < 4 * len(reqs):
+    while t_attn < budget_s and n_done < 4 * len(reqs):
         r = reqs[n_done % len(reqs)]
         P, S = r.prefix_len, r.suffix_len
         q = torch.randn(sh.n_q_heads, S, sh.head_dim, generator=g)
@@ -593,52 +673,68 @@ def cpu_baseline(reqs, budget_s: float = 20.0, threads: int = 0):
         t_attn += time.perf_counter() - t0
         f_sample += attention_flops([S], [P + S], sh.n_q_heads)
         n_done += 1
-    f_total = attention_flops([x.suffix_len for x in reqs], [x.prefix_len + x.suffix_len for x in reqs],
-                              sh.n_q_heads) * sh.n_layers
-    t_attn_full = t_attn * f_total / f_sample
-    tokens = sum(x.suffix_len for x in reqs)
-    step_s = t_cache_full + t_attn_full
-    return {"value": tokens / step_s, "unit": "tokens/s", "cores": cores, "kind": kind,
-            "sample": f"reference KvCache lookup+insert+release for {done}/{len(reqs)} requests "
-                      f"({t_cache:.2f}s, extrapolated by new blocks) + fp32 attention port for {n_done} request-layers "
-                      f"({t_attn:.2f}s, extrapolated by FLOPs x {f_total / f_sample:.0f})",
-            "step_s_extrapolated": step_s, "cache_s": t_cache_full, "attention_s": t_attn_full}
+    return {"tflops": f_sample / t_attn / 1e12, "request_layers_timed": n_done, "seconds": t_attn,
+            "cores": torch.get_num_threads()}
+
+
+def cpu_baseline(reqs):
+    """The reference's own CPU code for this step's engine-side KV work,
+    measured in full (no extrapolation), plus the fp32 attention port."""
+    import torch
+
+    step_s, kind = reference_step(reqs, steps=1, warmup=1)
+    tokens = sum(r.suffix_len for r in reqs)
+    att = attention_port(reqs)
+    return {"value": tokens / step_s, "unit": "tokens/s", "cores": 1, "kind": kind,
+            "sample": f"one full configs[1] step ({len(reqs)} calls: admission lookup, pin, extend, complete, "
+                      f"finish) of the reference KvCache + engine lifecycle, after one warm-up step: "
+                      f"{step_s:.3f} s; the reference computes no attention (it charges a cost model)",
+            "reference_cache_ops": {"s_per_step": step_s, "tokens_per_s": tokens / step_s, "threads": 1},
+            "attention_port": att | {"note": "fp32 torch attention of this step's requests on the host cores "
+                                             f"({torch.get_num_threads()} threads), sampled request-layers; "
+                                             "not part of value"}}
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU implementation of the path on the
+    host — its KvCache + engine lifecycle for the configs[1] step (value,
+    measured in full per step) and its own simulator replaying the same
+    configs[3] trace shard as one rank of ours at N=8 (trace)."""
     if rank != 0:
         return None
     reqs = setup_workload(0, args.requests)
-    vals = []
-    for _ in range(args.warmup + args.steps):
-        vals.append(cpu_baseline(reqs, budget_s=15.0))
-    timed = vals[args.warmup:]
-    v = float(np.mean([x["value"] for x in timed]))
-    cb = dict(timed[-1])
-    cb["value"] = v
-    trace = None
-    try:  # the reference's own replay of the same synthetic agent trace (its CPU simulator)
-        from oracle import oracle as O
-
-        res = {}
-        for name, preset in (("sutradhara", 2), ("baseline", 0)):
-            ftr, e2e, hit, prm, ev, wall = O.ref_run_trace(TRACE["n_requests"], TRACE["seed"], preset,
-                                                           TRACE["capacity_blocks"], 16)
-            f = np.sort(ftr)
-            res[name] = {"p50_ftr_ms": float(f[max(1, int(np.ceil(0.5 * len(f)))) - 1]),
-                         "hit_rate": float(hit.sum()) / float(prm.sum()), "evictions": ev, "replay_wall_s": wall}
-        trace = res
-    except Exception as e:  # pragma: no cover
-        trace = {"unavailable": str(e)}
-    return {
+    step_s, kind = reference_step(reqs, steps=args.steps, warmup=args.warmup)
+    tokens = sum(r.suffix_len for r in reqs)
+    v = tokens / step_s
+    line = {
         "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean([x["step_s_extrapolated"] for x in timed])),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "configs[1] (same requests/tokens as our arm)", "host_threads": cb["cores"]},
-        "impl": "reference", "cpu_baseline": cb, "trace": trace,
-        "p50_ftr_ms": trace.get("sutradhara", {}).get("p50_ftr_ms") if isinstance(trace, dict) else None,
+        "warmup": args.warmup, "ms_per_step": 1e3 * step_s, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64 (block pool) / no attention", "data": "synthetic",
+        "config": {"workload": "configs[1] (same 64 calls and pool as our arm): the reference KvCache "
+                               "(kv_cache.cpp) + engine lifecycle (engine.cpp:128-347) per step; the reference "
+                               "computes no attention", "host_threads": 1},
+        "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": 1, "kind": kind,
+                         "sample": f"{args.steps} full steps after {args.warmup} warm-up steps"},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:  # the same trace shard through the pure reference simulator (one rank's share at N=8)
+        from oracle.oracle import REF_DIR
+        from paper_2601_12967_b200 import dropin as D
+
+        lib = os.path.join(REF_DIR, "libagentsim_ref.so")
+        res = {}
+        for preset in ("sutradhara", "baseline"):
+            r = D.run_shard(args.trace_requests, TRACE_SEED, preset, TRACE_POOL, shard=0, n_shards=8, lib_path=lib)
+            tab = np.stack([r.ftr_ms, r.e2e_ms, r.hit_tokens, r.prompt_tokens, r.tool_ms, r.wait_ms, r.prefill_ms,
+                            r.decode_ms], 1).astype(np.float64)
+            res[preset] = trace_summary(tab, r.evictions, r.wall_s)
+        line["trace"] = {"workload": f"shard 0 of 8 of the {args.trace_requests}-request configs[3] trace on one "
+                                     f"{TRACE_POOL}-block pool (the reference simulator, single thread)", **res}
+        line["p50_ftr_ms"] = res["sutradhara"]["p50_ftr_ms"]
+    except Exception as e:  # pragma: no cover
+        line["trace"] = {"unavailable": str(e)[:200]}
+    return line
 
 
 def main():

@@ -81,6 +81,10 @@ def timed(fn, reps=10, warm=3, kernels=(), flush=False):
     return api, dev
 
 
+ROWS = []  # every emitted row (bench.py collects them as roofline_pool)
+QUIET = False
+
+
 def emit(kernel, config, bytes_, api_s, dev_s, hbm, launches=1, parts=None):
     """frac uses the kernel's own device time when the profiler saw it."""
     sec = dev_s * launches if dev_s else api_s
@@ -90,7 +94,9 @@ def emit(kernel, config, bytes_, api_s, dev_s, hbm, launches=1, parts=None):
            "achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm}
     if parts:
         row["parts_us"] = {k: round(v * 1e6, 2) for k, v in parts.items() if v}
-    print(json.dumps(row), flush=True)
+    ROWS.append(row)
+    if not QUIET:
+        print(json.dumps(row), flush=True)
 
 
 def fill_pool(L, cache, dev, n_seqs, toks, st):
@@ -136,16 +142,18 @@ def evict_bench(L, cache, cap, hbm):
              parts={k: kt.get(k) for k in ("k_plan", "k_score", "k_select_coop")})
 
 
-def main():
+def main(only=None):
     import argparse
 
     import torch
     from paper_2601_12967_b200 import _lib
     from paper_2601_12967_b200.kv_cache import CacheConfig, KvCache
 
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="hash,probe,probe_big,evict_small,evict,evict_big,append")
-    only = set(ap.parse_args().only.split(","))
+    if only is None:
+        ap = argparse.ArgumentParser()
+        ap.add_argument("--only", default="hash,probe,probe_big,evict_small,evict,evict_big,append")
+        only = ap.parse_args().only
+    only = set(only.split(","))
     L = _lib.lib()
     hbm = float(peaks()["hbm_gbs"])
     dev = torch.device("cuda")

@@ -150,6 +150,12 @@ uint64_t sb_kv_total_evicted(const sb_kv_cache* cache);  /* kv_cache.hpp:104 */
 int32_t sb_kv_policy(const sb_kv_cache* cache);
 /* KvCache::contains(id) — 1 resident, 0 not      kv_cache.hpp:106 */
 int sb_kv_contains(const sb_kv_cache* cache, int32_t id);
+/* Ids evicted by the most recent sb_kv_insert / sb_kv_evict on this pool
+ * (kv_cache.cpp:147-149, 177-197), in eviction order: with the ids an insert
+ * returns, the residency change of one call — what a binding mirroring
+ * KvCache::blocks_ needs, in O(change) instead of O(capacity).  *n_out gets
+ * the full count; at most cap ids are copied. */
+int sb_kv_last_evicted(const sb_kv_cache* cache, int32_t* out, int64_t cap, int64_t* n_out);
 /* Resident block ids in ascending order (the key set of KvCache::blocks_,
  * kv_cache.hpp:124); out holds capacity entries. */
 int sb_kv_resident_ids(const sb_kv_cache* cache, int32_t* out, int64_t* n_out);
@@ -195,7 +201,9 @@ int sb_kv_insert_batch(sb_kv_cache* cache, const uint64_t* d_tokens,
                        int32_t n_seqs, int64_t now, int32_t* d_out_ids, int32_t* d_status,
                        void* stream);
 /* Batched release of d_ids[0..n) (all-or-nothing like release(); negative
- * ids — the outputs of failed inserts — are skipped). */
+ * ids — the outputs of failed inserts — are skipped).  d_status (optional,
+ * device int32) receives SB_OK or, when nothing was released, the status of
+ * the first failing id in order (UnknownBlock / ZeroRefRelease). */
 int sb_kv_release_batch(sb_kv_cache* cache, const int32_t* d_ids, int64_t n, int32_t* d_status,
                         void* stream);
 /* Counters for the cross-GPU statistics reduction: [lookups, hit_tokens,
@@ -355,6 +363,9 @@ int sb_batch_run(sb_batch* batch, int64_t now, uint64_t seed, int32_t time_atten
                  void* stream, int32_t* launches);
 /* Per-layer attention times of the last timed run (ms, n_layers floats). */
 int sb_batch_attention_ms(sb_batch* batch, float* out);
+/* Pool-side phases of the last timed run (ms, 3 floats): submit + pin_partial,
+ * extend + complete_prefill, finish_decode. */
+int sb_batch_pool_ms(sb_batch* batch, float* out);
 /* Last step: admission-lookup hits (tokens per call), complete_prefill
  * statuses, and the chains the continuation attended over (ceil(full/16)
  * ids per call, packed). */
@@ -408,23 +419,6 @@ int sb_engine_partial_cached(sb_engine* engine, int32_t handle, int64_t* cached_
 int sb_batch_model_result(sb_batch* batch, int32_t* next_tokens, float* logits, void* stream);
 /* Dense-layer FLOPs of one run (2 * tokens * weights of all layers). */
 int sb_batch_dense_flops(const sb_batch* batch, double* flops);
-
-/* ---- agentic trace replay on the B200 pool (FTR / hit rate) ---------- */
-/* Generates the reference's synthetic agent trace (trace_gen.cpp:96-193;
- * workload "default" | "tool_heavy" | "iteration_heavy", gen[8] overrides as
- * [prompt_median, tool_out_median, decode_inter_median, decode_final_median,
- * qps, depth_p, fanout_p, ratio_scale], <= 0 keeps the default) and replays it
- * with the reference's engine/orchestrator timing rules (engine.cpp,
- * orchestrator.cpp) while every KV decision runs on a fresh B200 pool.
- * preset: 0 baseline, 1 baseline_sched, 2 sutradhara (runner.cpp:120-153).
- * cost (NULL = reference defaults): [prefill_ms_per_token,
- * decode_ms_per_token, batch_decode_overhead_ms, chunk_size].  Outputs per
- * request: FTR, e2e (virtual ms), prefix-hit and prompt tokens. */
-int sb_replay_generated(const char* workload, const double* gen, int32_t n_requests,
-                        uint64_t seed, int32_t preset, int64_t capacity_blocks,
-                        int64_t block_size, const double* cost, int32_t device, int64_t* ftr,
-                        int64_t* e2e, int64_t* hit_tokens, int64_t* prompt_tokens,
-                        uint64_t* evictions);
 
 #ifdef __cplusplus
 }

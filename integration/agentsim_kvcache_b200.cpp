@@ -8,11 +8,14 @@
 //
 // The header's inline accessors (resident_blocks, contains, free_blocks,
 // total_evicted) read the private members `blocks_` and `total_evicted_`, so
-// the binding keeps them mirrored after every mutating call (the key set of
-// blocks_ == resident ids on the device).
+// the binding keeps them mirrored after every call that changes residency
+// (insert / evict), from the change itself: the ids the call evicted
+// (sb_kv_last_evicted) and the chain it returned — O(change), no O(capacity)
+// read-back.  The pool's device comes from SB_DEVICE / LOCAL_RANK.
 //
 // Build (see oracle/Makefile target `b200`): compile with the reference's
 // include/ on the include path and link against libsutradhara_b200.so.
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -62,22 +65,30 @@ std::uint64_t kv_chain_hash(std::uint64_t parent, std::span<const TokenId> t) {
   return sb_kv_chain_hash_host(parent, t.data(), static_cast<int64_t>(t.size()));
 }
 
-// Mirrors residency and the eviction counter into the header-visible members.
-static void sync_mirror(sb_kv_cache* p, std::unordered_map<std::int32_t, KvBlock>& blocks,
-                        std::set<std::int32_t>& free_ids, std::uint64_t& total_evicted, int64_t cap) {
-  std::vector<int32_t> ids(static_cast<size_t>(cap));
+// Mirrors the residency change of one insert / evict into the
+// header-visible members, in O(change): the ids the device evicted
+// (sb_kv_last_evicted) leave blocks_, the chain an insert returned is
+// resident (new blocks, including evicted-and-reused ids, get fresh records).
+static void apply_delta(sb_kv_cache* p, std::unordered_map<std::int32_t, KvBlock>& blocks,
+                        const std::vector<std::int32_t>& chain, std::uint64_t& total_evicted) {
   int64_t n = 0;
-  check(sb_kv_resident_ids(p, ids.data(), &n));
-  std::unordered_map<std::int32_t, KvBlock> next;
-  next.reserve(static_cast<size_t>(n));
-  for (int64_t i = 0; i < n; ++i) {
-    auto it = blocks.find(ids[i]);
-    if (it != blocks.end()) next.emplace(ids[i], std::move(it->second));
-    else next[ids[i]].block_id = ids[i];
+  check(sb_kv_last_evicted(p, nullptr, 0, &n));
+  std::vector<int32_t> ev(static_cast<size_t>(n));
+  if (n) check(sb_kv_last_evicted(p, ev.data(), n, &n));
+  for (int32_t id : ev) blocks.erase(id);
+  for (int32_t id : chain) {
+    auto it = blocks.find(id);
+    if (it == blocks.end()) blocks[id].block_id = id;
   }
-  blocks.swap(next);
-  free_ids.clear();
-  total_evicted = sb_kv_total_evicted(p);
+  total_evicted += static_cast<std::uint64_t>(n);
+}
+
+// The device this pool lives on: SB_DEVICE, else the torchrun LOCAL_RANK,
+// else 0 — one pool per GPU when each rank runs its own engine.
+static int pool_device() {
+  for (const char* v : {"SB_DEVICE", "LOCAL_RANK"})
+    if (const char* e = std::getenv(v)) return std::atoi(e);
+  return 0;
 }
 
 KvCache::KvCache(const CacheConfig& config) : config_(config) {
@@ -85,7 +96,8 @@ KvCache::KvCache(const CacheConfig& config) : config_(config) {
   if (config_.capacity_blocks < 1) throw ConfigError("cache capacity_blocks must be >= 1");
   sb_kv_cache* p = nullptr;
   check(sb_kv_create(config.block_size, config.capacity_blocks,
-                     config.policy == EvictionPolicy::kTiered ? SB_POLICY_TIERED : SB_POLICY_LRU, 0, &p));
+                     config.policy == EvictionPolicy::kTiered ? SB_POLICY_TIERED : SB_POLICY_LRU, pool_device(),
+                     &p));
   auto old = g_pools.find(this);
   if (old != g_pools.end()) sb_kv_destroy(old->second);
   g_pools[this] = p;
@@ -107,9 +119,9 @@ std::vector<std::int32_t> KvCache::insert(std::span<const TokenId> tokens, std::
   int64_t n = 0;
   int st = sb_kv_insert(pool(this), tokens.data(), static_cast<int64_t>(tokens.size()), tr.data(),
                         static_cast<int64_t>(tr.size()), now, out.data(), &n);
-  sync_mirror(pool(this), blocks_, free_ids_, total_evicted_, config_.capacity_blocks);
+  out.resize(st == SB_OK ? static_cast<size_t>(n) : 0);
+  apply_delta(pool(this), blocks_, out, total_evicted_);
   if (st != SB_OK) raise(st);
-  out.resize(static_cast<size_t>(n));
   return out;
 }
 
@@ -117,7 +129,7 @@ std::vector<std::int32_t> KvCache::evict(std::size_t needed) {
   std::vector<std::int32_t> out(needed + 1);
   int64_t n = 0;
   check(sb_kv_evict(pool(this), static_cast<int64_t>(needed), out.data(), &n));
-  sync_mirror(pool(this), blocks_, free_ids_, total_evicted_, config_.capacity_blocks);
+  apply_delta(pool(this), blocks_, {}, total_evicted_);
   out.resize(static_cast<size_t>(n));
   return out;
 }

@@ -58,6 +58,7 @@ SIGNATURES = {
     "sb_kv_total_evicted": (C.c_uint64, [VP]),
     "sb_kv_policy": (C.c_int32, [VP]),
     "sb_kv_contains": (C.c_int, [VP, C.c_int32]),
+    "sb_kv_last_evicted": (C.c_int, [VP, I32P, C.c_int64, I64P]),
     "sb_kv_resident_ids": (C.c_int, [VP, I32P, I64P]),
     "sb_kv_block": (C.c_int, [VP, C.c_int32, C.POINTER(BlockInfo), U64P]),
     "sb_kv_blocks": (C.c_int, [VP, I32P, C.c_int64, C.POINTER(BlockInfo)]),
@@ -99,11 +100,10 @@ SIGNATURES = {
     "sb_batch_stage_suffix": (C.c_int, [VP, VP, C.c_int32, VP]),
     "sb_batch_run": (C.c_int, [VP, C.c_int64, C.c_uint64, C.c_int32, VP, I32P]),
     "sb_batch_attention_ms": (C.c_int, [VP, C.POINTER(C.c_float)]),
+    "sb_batch_pool_ms": (C.c_int, [VP, C.POINTER(C.c_float)]),
     "sb_batch_results": (C.c_int, [VP, I64P, I32P, I32P, VP]),
     "sb_batch_copy_output": (C.c_int, [VP, C.c_int64, C.c_int64, VP, VP]),
     "sb_batch_info": (C.c_int, [VP, I64P, I64P, I64P, C.POINTER(C.c_double), C.POINTER(VP)]),
-    "sb_replay_generated": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), C.c_int32, C.c_uint64, C.c_int32, C.c_int64,
-                                      C.c_int64, C.POINTER(C.c_double), C.c_int32, I64P, I64P, I64P, I64P, U64P]),
     "sb_kv_append": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, VP]),
     "sb_model_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_float,
                                   C.c_uint64, C.c_int32, C.POINTER(VP)]),

@@ -64,7 +64,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=8) as ex:
         objs = list(ex.map(compile_one, _sources()))
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-ccbin", "/usr/bin/g++", "-cudart", "static", *objs, "-lcublas", "-o", tmp]
+    cmd = [NVCC, *ARCH, "-shared", "-ccbin", "/usr/bin/g++", "-cudart", "static", *objs, "-lcublas",
+           "-Xlinker", "-soname=libsutradhara_b200.so", "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

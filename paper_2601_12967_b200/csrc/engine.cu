@@ -570,10 +570,13 @@ struct sb_batch {
   std::vector<int32_t> pin_outcome, complete_status;
   __nv_bfloat16 *q = nullptr, *k_new = nullptr, *v_new = nullptr, *out = nullptr;
   std::vector<cudaEvent_t> ev0, ev1;
+  cudaEvent_t evp[6] = {};  // pool phases of a timed run: [0,1) submit+pin, [2,3) extend+complete, [4,5) finish
   double attn_flops = 0;
   sb_model* model = nullptr;
   ModelWorkspace* mw = nullptr;
   ~sb_batch() {
+    for (auto e : evp)
+      if (e) cudaEventDestroy(e);
     cudaSetDevice(eng->device);
     model_workspace_destroy(mw);
     void* ptrs[] = {tokens, hashes, suffix, keys, ids, chain, pinned, tags, suffix_off, slot_off, resp_pos, chain_off, hits,
@@ -751,6 +754,7 @@ int sb_batch_create(sb_engine* e, int32_t n, const uint64_t* prefix_tokens, cons
         SB_CUDA(cudaEventCreate(&b->ev0[l]));
         SB_CUDA(cudaEventCreate(&b->ev1[l]));
       }
+      for (auto& ev : b->evp) SB_CUDA(cudaEventCreate(&ev));
     } catch (...) {
       delete b;
       throw;
@@ -787,6 +791,7 @@ int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention
     auto chk = [](int s) {
       if (s) throw Error(s, sb_last_error());
     };
+    if (time_attention) SB_CUDA(cudaEventRecord(b->evp[0], st));
     // 1. submit_partial_prefill x n: prefix chain hashes + admission lookups (engine.cpp:170)
     chk(sb_chain_hash_segments(b->tokens, b->seg_pre, b->blk_pre, nullptr, n, 16, b->hashes, st));
     pool_lookup(e->cache, b->lookup_ops.data(), n, now, b->hits, st);
@@ -795,6 +800,7 @@ int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention
     for (auto& o : b->pin_ops) o.n_chain = o.n_pinned = 0;
     pool_run_ops(e->cache, b->pin_ops.data(), n, e->d_pin_cnt, e->d_real_tag, now, st, b->res.data());
     n_launch += 4;
+    if (time_attention) SB_CUDA(cudaEventRecord(b->evp[1], st));
     b->pin_outcome.assign(static_cast<size_t>(n), 0);
     for (int i = 0; i < n; ++i) {
       b->pin_outcome[i] = b->res[i].outcome;
@@ -803,12 +809,14 @@ int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention
     }
     // 3. extend_prefill x n (suffix tokens staged by sb_batch_stage_suffix):
     //    incremental hashing of the suffix from the prefix's last full block
+    if (time_attention) SB_CUDA(cudaEventRecord(b->evp[2], st));
     k_seg_parents<<<(n + 127) / 128, 128, 0, st>>>(b->hashes, b->chain_off, b->blk_sfx, n, b->par_sfx);
     chk(sb_chain_hash_segments(b->tokens, b->seg_sfx, b->blk_sfx, b->par_sfx, n, 16, b->hashes, st));
     n_launch += 2;
     // 4. complete_prefill x n (program)
     pool_run_ops(e->cache, b->complete_ops.data(), n, e->d_pin_cnt, e->d_real_tag, now, st, b->res.data());
     n_launch += 4;
+    if (time_attention) SB_CUDA(cudaEventRecord(b->evp[3], st));
     b->complete_status.assign(static_cast<size_t>(n), 0);
     for (int i = 0; i < n; ++i) {
       b->complete_status[i] = b->res[i].status;
@@ -854,13 +862,27 @@ int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention
       }
     }
     // 6. finish_decode x n with the first response token (program)
+    if (time_attention) SB_CUDA(cudaEventRecord(b->evp[4], st));
     k_response_tokens<<<(n + 127) / 128, 128, 0, st>>>(model_tok, b->keys, b->resp_pos, n, b->tokens);
     k_seg_parents<<<(n + 127) / 128, 128, 0, st>>>(b->hashes, b->chain_off, b->blk_resp, n, b->par_resp);
     chk(sb_chain_hash_segments(b->tokens, b->seg_resp, b->blk_resp, b->par_resp, n, 16, b->hashes, st));
     n_launch += 3;
     pool_run_ops(e->cache, b->finish_ops.data(), n, e->d_pin_cnt, e->d_real_tag, now, st, b->res.data());
+    if (time_attention) SB_CUDA(cudaEventRecord(b->evp[5], st));
     n_launch += 4;
     if (launches) *launches = n_launch;
+    return int(SB_OK);
+  });
+}
+
+// Pool-side phases of the last timed run (ms): submit + pin_partial,
+// extend + complete_prefill, finish_decode (each including its host sync).
+int sb_batch_pool_ms(sb_batch* b, float* out) {
+  return guard([&] {
+    for (int k = 0; k < 3; ++k) {
+      SB_CUDA(cudaEventSynchronize(b->evp[2 * k + 1]));
+      SB_CUDA(cudaEventElapsedTime(&out[k], b->evp[2 * k], b->evp[2 * k + 1]));
+    }
     return int(SB_OK);
   });
 }

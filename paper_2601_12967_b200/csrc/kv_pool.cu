@@ -2083,6 +2083,7 @@ struct sb_kv_cache {
   unsigned long long* d_created = nullptr;  // chain hashes created by a program
   int64_t created_cap = 0;
   int prog_device_attr = -1;
+  std::vector<int32_t> last_evicted;  // ids evicted by the last per-op insert / evict (sb_kv_last_evicted)
 
   bool use_coop() const { return P.cap >= kCoopMinCap && coop_grid > 0; }
 
@@ -2708,9 +2709,14 @@ int sb_kv_insert(sb_kv_cache* c, const uint64_t* tokens, int64_t n, const sb_tag
       op.pos_off = 0;
       c->ensure_ops(1);
       SB_CUDA(cudaMemcpyAsync(c->d_ops, &op, sizeof(op), cudaMemcpyHostToDevice, c->stream));
-      c->run_program(1, nblk, nblk, 0, nullptr, nullptr, now, c->stream);
+      int64_t evs = 0;
+      c->run_program(1, nblk, nblk, 0, nullptr, nullptr, now, c->stream, &evs);
       ProgRes r{};
       SB_CUDA(cudaMemcpyAsync(&r, c->d_res, sizeof(r), cudaMemcpyDeviceToHost, c->stream));
+      c->last_evicted.resize(static_cast<size_t>(evs));
+      if (evs)
+        SB_CUDA(cudaMemcpyAsync(c->last_evicted.data(), c->S.evicted, sizeof(int32_t) * evs, cudaMemcpyDeviceToHost,
+                                c->stream));
       SB_CUDA(cudaStreamSynchronize(c->stream));
       st = r.status;
     }
@@ -2795,6 +2801,7 @@ int sb_kv_evict(sb_kv_cache* c, int64_t needed, int32_t* out_ids, int64_t* n_out
     SB_CUDA(cudaStreamSynchronize(c->stream));
     if (k) SB_CUDA(cudaMemcpy(out_ids, c->d_ids, sizeof(int32_t) * k, cudaMemcpyDeviceToHost));
     *n_out = k;
+    c->last_evicted.assign(out_ids, out_ids + k);
     c->maybe_rebuild_index(k);
     return int(SB_OK);
   });
@@ -2891,6 +2898,13 @@ int64_t sb_kv_resident_blocks(const sb_kv_cache* c) { return static_cast<int64_t
 int64_t sb_kv_free_blocks(const sb_kv_cache* c) { return c->P.cap - sb_kv_resident_blocks(c); }
 uint64_t sb_kv_total_evicted(const sb_kv_cache* c) { return c->read_ctr(C_EVICTED); }
 int32_t sb_kv_policy(const sb_kv_cache* c) { return c->P.policy; }
+
+int sb_kv_last_evicted(const sb_kv_cache* c, int32_t* out, int64_t cap, int64_t* n_out) {
+  *n_out = static_cast<int64_t>(c->last_evicted.size());
+  const int64_t m = std::min<int64_t>(cap, *n_out);
+  if (out && m > 0) std::memcpy(out, c->last_evicted.data(), sizeof(int32_t) * m);
+  return SB_OK;
+}
 
 int sb_kv_contains(const sb_kv_cache* c, int32_t id) {
   if (id < 0 || id >= c->P.cap) return 0;

@@ -295,6 +295,13 @@ class ContinuationBatch:
         _lib.check(self._L.sb_batch_attention_ms(self._h, out))
         return list(out)
 
+    def pool_ms(self) -> List[float]:
+        """Pool-side phases of the last timed run: [submit + pin, extend +
+        complete, finish] in ms (CUDA events on the batch's stream)."""
+        out = (C.c_float * 3)()
+        _lib.check(self._L.sb_batch_pool_ms(self._h, out))
+        return list(out)
+
     def results(self):
         """(admission hits [n], complete statuses [n], chains the continuation
         attended over [total_blocks] laid out by blk_off_h)."""

@@ -53,15 +53,15 @@ def _free_port():
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    # the gather pattern of bench.trace_replay_metrics: fixed-size rows per rank
-    row = torch.tensor([10.0 * rank + i for i in range(5)], dtype=torch.float64)
-    parts = [torch.empty_like(row) for _ in range(world)]
-    dist.all_gather(parts, row)
-    q.put((rank, torch.stack(parts).numpy().tolist()))
+    # bench.gather_rows: ragged per-rank tables (one trace shard per rank)
+    rows = np.array([[10.0 * rank + i, float(i)] for i in range(3 + rank)])
+    out = bench.gather_rows(rows, world)
+    q.put((rank, out.tolist()))
     dist.destroy_process_group()
 
 
 def test_trace_stats_gather_world2():
+    """The configs[3] gather: rank r's shard rows, in rank order, ragged."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -72,7 +72,15 @@ def test_trace_stats_gather_world2():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert res[0][1] == res[1][1] == [[0.0, 1.0, 2.0, 3.0, 4.0], [10.0, 11.0, 12.0, 13.0, 14.0]]
+    exp = [[0.0, 0.0], [1.0, 1.0], [2.0, 2.0], [10.0, 0.0], [11.0, 1.0], [12.0, 2.0], [13.0, 3.0]]
+    assert res[0][1] == res[1][1] == exp
+
+
+def test_trace_summary_tool_share():
+    tab = np.array([[100, 200, 16, 64, 50, 10, 30, 10], [200, 300, 0, 64, 20, 100, 60, 20]], np.float64)
+    s = bench.trace_summary(tab, 7, 1.5)
+    assert s["p50_ftr_ms"] == 100 and s["hit_rate"] == 16 / 128 and s["evictions"] == 7
+    assert s["tool_share_of_ftr"]["frac_in_30_80pct"] == 0.5
 
 
 def test_clock_sampler_parses_power_and_reasons():
