@@ -17,12 +17,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 
-def measure(n_requests: int = 64, launches: int = 6, flashinfer: bool = False) -> dict:
-    """Our kernel (and optionally flashinfer's trtllm-gen kernel) on the same
-    synthetic paged KV / queries of the configs[1] step."""
+def setup(n_requests: int = 64, flashinfer: bool = False):
+    """The configs[1] step's attention problem on synthetic paged KV:
+    (q, k_pool, v_pool, q_off, kv_lens, table, work, out, run_ours, run_fi)
+    with run_fi = flashinfer's trtllm-gen paged context kernel on the same
+    tensors (None when flashinfer is absent or not requested)."""
     import torch
     from paper_2601_12967_b200 import workload as W
-    from paper_2601_12967_b200.attention import attention_flops, attention_work_list, continuation_attention
+    from paper_2601_12967_b200.attention import attention_work_list, continuation_attention
 
     reqs = W.agentic_continuation_batch(n_requests, seed=1)
     hq, hkv = 32, 8
@@ -43,25 +45,46 @@ def measure(n_requests: int = 64, launches: int = 6, flashinfer: bool = False) -
     q_off = torch.tensor(np.cumsum([0] + q_lens), dtype=torch.int32, device="cuda")
     kvl = torch.tensor(kv_lens, dtype=torch.int32, device="cuda")
     work = torch.from_numpy(attention_work_list(q_lens, kv_lens, hq, hkv)).cuda()
-    flops = attention_flops(q_lens, kv_lens, hq)
     out = torch.empty_like(q)
 
     def run_ours():
         continuation_attention(q, kp, vp, q_off, kvl, table, max(q_lens), out=out, work=work)
+        return out
 
     run_fi = None
     if flashinfer:
-        import flashinfer.prefill as FP
+        try:
+            import flashinfer.prefill as FP
 
-        ws = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
-        seq_lens = torch.tensor(kv_lens, dtype=torch.int32, device="cuda")
-        cum_kv = torch.tensor(np.cumsum([0] + kv_lens), dtype=torch.int32, device="cuda")
-        fo = torch.empty_like(q)
+            ws = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
+            seq_lens = torch.tensor(kv_lens, dtype=torch.int32, device="cuda")
+            cum_kv = torch.tensor(np.cumsum([0] + kv_lens), dtype=torch.int32, device="cuda")
+            fo = torch.empty_like(q)
 
-        def run_fi():
-            return FP.trtllm_batch_context_with_kv_cache(q, (kp, vp), ws, table, seq_lens, max(q_lens), max(kv_lens),
-                                                         1.0 / np.sqrt(128), 1.0, len(reqs), q_off, cum_kv, out=fo,
-                                                         kv_layout="HND", causal=True)
+            def run_fi():
+                FP.trtllm_batch_context_with_kv_cache(q, (kp, vp), ws, table, seq_lens, max(q_lens), max(kv_lens),
+                                                      1.0 / np.sqrt(128), 1.0, len(reqs), q_off, cum_kv, out=fo,
+                                                      kv_layout="HND", causal=True)
+                return fo
+        except Exception:
+            run_fi = None
+    return q, kp, vp, q_off, kvl, table, work, out, run_ours, run_fi
+
+
+def measure(n_requests: int = 64, launches: int = 6, flashinfer: bool = False) -> dict:
+    """Our kernel (and optionally flashinfer's trtllm-gen kernel) on the same
+    synthetic paged KV / queries of the configs[1] step."""
+    import torch
+    from paper_2601_12967_b200 import workload as W
+    from paper_2601_12967_b200.attention import attention_flops
+
+    reqs = W.agentic_continuation_batch(n_requests, seed=1)
+    q_lens = [r.suffix_len for r in reqs]
+    kv_lens = [r.prefix_len + r.suffix_len for r in reqs]
+    flops = attention_flops(q_lens, kv_lens, 32)
+    q, kp, vp, q_off, kvl, table, work, out, run_ours, run_fi = setup(n_requests, flashinfer)
+    if flashinfer and run_fi is None:
+        raise RuntimeError("flashinfer trtllm-gen kernel unavailable")
 
     def timed(fn, n):
         ts = []
@@ -90,7 +113,7 @@ def measure(n_requests: int = 64, launches: int = 6, flashinfer: bool = False) -
         fms = float(np.median(fts))
         fi = {"kernel": "flashinfer trtllm_batch_context_with_kv_cache (trtllm-gen cubin)", "ms": fms,
               "tflops": flops / fms / 1e9,
-              "max_abs_diff_vs_ours": float((fo.float() - out.float()).abs().max()),
+              "max_abs_diff_vs_ours": float((run_fi().float() - run_ours().float()).abs().max()),
               "max_abs_out": float(out.float().abs().max())}
     res = {"kernel": "k_continuation_attention", "ms": ms, "tflops": flops / ms / 1e9, "flops": flops,
            "checksum": float(out.float().abs().mean()), "flashinfer": fi}

@@ -94,7 +94,8 @@ def test_continuation_attention_matches_fp32(case, use_work_list):
     ref = ref_attention(q, kp, vp, qo.cpu(), kl.cpu(), tb, scale)
     err = (out.float() - ref).abs().max().item()
     assert torch.isfinite(out.float()).all()
-    assert err <= REL_TOL_BF16 * ref.abs().max().item() + 1e-3, err
+    rel = err / ref.abs().max().item()
+    assert rel <= REL_TOL_BF16, rel
 
 
 @pytest.mark.gpu
@@ -122,7 +123,7 @@ def test_kv_append_then_attend():
             assert torch.equal(vp[page, :, pos % 16], v_new[tok])
     out = continuation_attention(q, kp, vp, qo, kl, tb, max(q_lens))
     ref = ref_attention(q, kp, vp, qo.cpu(), kl.cpu(), tb, 1 / math.sqrt(128))
-    assert (out.float() - ref).abs().max().item() <= REL_TOL_BF16 * ref.abs().max().item() + 1e-3
+    assert (out.float() - ref).abs().max().item() <= REL_TOL_BF16 * ref.abs().max().item()
 
 
 @pytest.mark.gpu
@@ -147,7 +148,48 @@ def test_running_max_keeps_growing():
     ref = ref_attention(q, kp, vp, qo.cpu(), kl.cpu(), tb, 1 / math.sqrt(128))
     assert torch.isfinite(out.float()).all()
     err = (out.float() - ref).abs().max().item()
-    assert err <= REL_TOL_BF16 * ref.abs().max().item() + 1e-3, err
+    assert err <= REL_TOL_BF16 * ref.abs().max().item(), err
+
+
+@pytest.mark.gpu
+def test_attention_at_the_bench_shape():
+    """The configs[1] step's attention problem itself (64 requests, 98,896
+    suffix queries over 441,888 cached prefix keys, 32 q / 8 kv heads, pages
+    spread over the pool): sampled sequences x every head x first / middle /
+    last query rows vs the fp32 reference, max-norm relative <= 1e-2; and,
+    when flashinfer's trtllm-gen paged kernel loads, the whole output against
+    it within the same bound."""
+    import torch
+    import bench_attn
+
+    q, kp, vp, q_off, kvl, table, work, out, run_ours, run_fi = bench_attn.setup(64, flashinfer=True)
+    run_ours()
+    torch.cuda.synchronize()
+    n = len(kvl)
+    qo = q_off.cpu().tolist()
+    worst = 0.0
+    for s in range(0, n, 7):
+        a, b = qo[s], qo[s + 1]
+        rows = sorted({a, a + 1, (a + b) // 2, b - 2, b - 1})
+        kl = int(kvl[s])
+        pages = table[s, : (kl + 15) // 16].long()
+        k = kp[pages].float().permute(1, 0, 2, 3).reshape(8, -1, 128)[:, :kl].repeat_interleave(4, 0)
+        v = vp[pages].float().permute(1, 0, 2, 3).reshape(8, -1, 128)[:, :kl].repeat_interleave(4, 0)
+        for r in rows:
+            qs = q[r].float()[:, None, :]                              # [32, 1, 128]
+            pos = kl - (b - a) + (r - a)
+            sc = (qs @ k[:, : pos + 1].transpose(1, 2)) / math.sqrt(128)
+            ref = (torch.softmax(sc, -1) @ v[:, : pos + 1])[:, 0]     # [32, 128]
+            rel = ((out[r].float() - ref).abs().max() / ref.abs().max()).item()
+            worst = max(worst, rel)
+    print(f"bench-shape attention: worst sampled max-norm relative error {worst:.2e}")
+    assert worst <= REL_TOL_BF16, worst
+    if run_fi is not None:
+        fo = run_fi()
+        torch.cuda.synchronize()
+        rel = ((fo.float() - out.float()).abs().max() / out.float().abs().max()).item()
+        print(f"vs trtllm-gen: max-norm relative difference {rel:.2e}")
+        assert rel <= REL_TOL_BF16, rel
 
 
 REL_TOL_F32 = 1e-5

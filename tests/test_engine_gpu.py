@@ -77,3 +77,19 @@ def test_engine_steps_match_oracle(n_req, slack, policy):
     cap = pre + int(slack * suf) + 1
     eng = ContinuationEngine(ModelShape(n_layers=2, n_q_heads=8, n_kv_heads=2, head_dim=128), cap, policy=policy)
     run_and_check(eng, reqs, cap, policy, steps=4, sys_len=256)
+
+
+@pytest.mark.gpu
+def test_engine_steps_match_reference_at_bench_shape():
+    """The configs[1] bench step itself: bench.py's 64 requests, its
+    capacity_for() pool (27K blocks, ~5.5K evictions per step), 3 steps,
+    checked against the reference's own KvCache (oracle/_ref) under the
+    engine lifecycle after every step."""
+    import bench
+    from paper_2601_12967_b200.engine import ContinuationEngine, ModelShape
+
+    reqs = bench.setup_workload(0, 64)
+    _, _, cap = bench.capacity_for(reqs)
+    eng = ContinuationEngine(ModelShape(n_layers=1, n_q_heads=8, n_kv_heads=2, head_dim=128), cap, policy=1)
+    run_and_check(eng, reqs, cap, 1, steps=3, sys_len=2048)
+    assert eng.cache.total_evicted() > 5000

@@ -56,18 +56,17 @@ def _rms(x, w, eps=1e-5):
     return x * (x.pow(2).mean(-1, keepdim=True) + eps).rsqrt() * w
 
 
-@pytest.mark.gpu
-@pytest.mark.parametrize("prefix_lens,suffix_lens", [([48, 96, 16], [37, 70, 1]), ([256], [130])])
-def test_dense_step_matches_torch_reference(prefix_lens, suffix_lens):
+def _dense_check(ds, prefix_lens, suffix_lens, model_seed=3, eng_seed=7):
+    """Run one continuation step of the dense model through the engine and
+    compare last-token logits with the torch fp32 restatement."""
     import torch
     import torch.nn.functional as F
-    from paper_2601_12967_b200.engine import ContinuationEngine, DenseModel, DenseShape, ModelShape
+    from paper_2601_12967_b200.engine import ContinuationEngine, DenseModel, ModelShape
 
-    hq, hkv, d, dff, vocab, nl = 4, 2, 512, 1024, 1000, 2
-    ds = DenseShape(n_layers=nl, d_model=d, n_q_heads=hq, n_kv_heads=hkv, d_ff=dff, vocab=vocab, rope_theta=10000.0)
-    cap = sum((p + s + 15) // 16 for p, s in zip(prefix_lens, suffix_lens)) + 4
-    eng = ContinuationEngine(ModelShape(nl, hq, hkv, 128), cap, policy=1, seed=7)
-    model = DenseModel(ds, seed=3)
+    hq, hkv, d, dff, vocab, nl = ds.n_q_heads, ds.n_kv_heads, ds.d_model, ds.d_ff, ds.vocab, ds.n_layers
+    cap = sum((p + s + 15) // 16 for p, s in zip(prefix_lens, suffix_lens)) + 4 + len(prefix_lens)
+    eng = ContinuationEngine(ModelShape(nl, hq, hkv, 128), cap, policy=1, seed=eng_seed)
+    model = DenseModel(ds, seed=model_seed)
     prefixes = [O.materialize(0, p, 100 + i) for i, p in enumerate(prefix_lens)]
     batch = eng.make_batch(prefixes, [[(0, p, 3)] for p in prefix_lens], suffix_lens)
     batch.set_model(model)
@@ -89,8 +88,6 @@ def test_dense_step_matches_torch_reference(prefix_lens, suffix_lens):
     emb = _dev_tensor(*model.weight(-1, 0), (vocab, d))
     lm = _dev_tensor(*model.weight(-1, 1), (vocab, d))
     fnorm = _dev_tensor(*model.weight(-1, 2), (d,))
-    pools = [(_dev_tensor(eng.k_pool(l), cap * hkv * 16 * 128, (cap, hkv, 16, 128)),
-              _dev_tensor(eng.v_pool(l), cap * hkv * 16 * 128, (cap, hkv, 16, 128))) for l in range(nl)]
     blk = np.cumsum([0] + [(p + s + 15) // 16 for p, s in zip(prefix_lens, suffix_lens)])
     ref_logits = []
     off = 0
@@ -101,19 +98,22 @@ def test_dense_step_matches_torch_reference(prefix_lens, suffix_lens):
         pos = torch.arange(p, p + s, device="cuda")
         pages = torch.from_numpy(ids[blk[si]:blk[si] + p // 16]).long().cuda()
         for l in range(nl):
+            kp = _dev_tensor(eng.k_pool(l), cap * hkv * 16 * 128, (cap, hkv, 16, 128))
+            vp = _dev_tensor(eng.v_pool(l), cap * hkv * 16 * 128, (cap, hkv, 16, 128))
             xn = _bf(_rms(x, W[l, 4]))
             qkv = _bf(xn @ W[l, 0].t()).reshape(s, hq + 2 * hkv, 128)
             q = _bf(_rope(qkv[:, :hq], pos, ds.rope_theta))
             k = _bf(_rope(qkv[:, hq:hq + hkv], pos, ds.rope_theta))
             v = qkv[:, hq + hkv:]
-            kp, vp = pools[l]
             kpre = kp[pages].permute(1, 0, 2, 3).reshape(hkv, -1, 128)  # [hkv, p, 128]
             vpre = vp[pages].permute(1, 0, 2, 3).reshape(hkv, -1, 128)
+            del kp, vp
             K = torch.cat([kpre, k.permute(1, 0, 2)], 1).repeat_interleave(hq // hkv, 0)
             V = torch.cat([vpre, v.permute(1, 0, 2)], 1).repeat_interleave(hq // hkv, 0)
             sc = q.permute(1, 0, 2) @ K.transpose(1, 2) / math.sqrt(128)
             mask = torch.arange(p + s, device="cuda")[None, :] > (p + torch.arange(s, device="cuda"))[:, None]
             a = _bf((torch.softmax(sc.masked_fill(mask, float("-inf")), -1) @ V).permute(1, 0, 2).reshape(s, d))
+            del K, V, sc
             x = _bf(x + a @ W[l, 1].t())
             xn = _bf(_rms(x, W[l, 5]))
             gu = _bf(xn @ W[l, 2].t())
@@ -125,13 +125,35 @@ def test_dense_step_matches_torch_reference(prefix_lens, suffix_lens):
     got = torch.from_numpy(logits)
     tol = 2e-2 * ref.abs().max().item()
     err = (got - ref).abs().max().item()
-    print(f"dense step: max |logit err| {err:.3e} vs tol {tol:.3e} (max |logit| {ref.abs().max().item():.3f})")
+    print(f"dense step {ds}: max |logit err| {err:.3e} vs tol {tol:.3e} (max |logit| {ref.abs().max().item():.3f})")
     assert ref.abs().max().item() > 0
     assert err <= tol, (err, tol)
     top2 = ref.topk(2, -1).values
     for i in range(len(prefix_lens)):
         if (top2[i, 0] - top2[i, 1]).item() > 2 * tol:
             assert nxt[i] == int(ref[i].argmax()), i
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prefix_lens,suffix_lens", [([48, 96, 16], [37, 70, 1]), ([256], [130])])
+def test_dense_step_matches_torch_reference(prefix_lens, suffix_lens):
+    from paper_2601_12967_b200.engine import DenseShape
+
+    ds = DenseShape(n_layers=2, d_model=512, n_q_heads=4, n_kv_heads=2, d_ff=1024, vocab=1000, rope_theta=10000.0)
+    _dense_check(ds, prefix_lens, suffix_lens)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_layers,prefix_lens,suffix_lens", [(2, [8192], [256]), (1, [32768, 8192], [160, 96])])
+def test_dense_step_at_llama3_8b_shape(n_layers, prefix_lens, suffix_lens):
+    """configs[2]'s model shape: d_model 4096, 32 q / 8 kv heads, d_ff 14336,
+    vocab 128256, RoPE theta 5e5, 8K and 32K cached prefixes."""
+    from paper_2601_12967_b200.engine import LLAMA3_8B_DENSE, DenseShape
+
+    ds = DenseShape(n_layers=n_layers, d_model=LLAMA3_8B_DENSE.d_model, n_q_heads=LLAMA3_8B_DENSE.n_q_heads,
+                    n_kv_heads=LLAMA3_8B_DENSE.n_kv_heads, d_ff=LLAMA3_8B_DENSE.d_ff, vocab=LLAMA3_8B_DENSE.vocab,
+                    rope_theta=LLAMA3_8B_DENSE.rope_theta)
+    _dense_check(ds, prefix_lens, suffix_lens)
 
 
 def _torch_forward_logits(tok_ids, W, emb, lm, fnorm, nl, hq, hkv, d, dff, theta):
