@@ -25,6 +25,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include <cmath>
 #include <algorithm>
 #include <cstdint>
@@ -551,11 +553,15 @@ extern "C" int sb_continuation_attention(const void* q, const void* k_pool, cons
     prm.scale_log2 = softmax_scale * 1.4426950408889634f;
     prm.work = d_work;
     auto kern = attn::k_continuation_attention;
-    static bool attr_set = false;
-    if (!attr_set) {
-      SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmemBytes));
-      attr_set = true;
-    }
+    // the attribute is per device context: set once per device, thread-safe
+    static std::once_flag attr_once[64];
+    int dev = 0;
+    SB_CUDA(cudaGetDevice(&dev));
+    cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once[dev & 63], [&] {
+      attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmemBytes);
+    });
+    SB_CUDA(attr_err);
     const int64_t grid = d_work ? static_cast<int64_t>(n_work) : static_cast<int64_t>(n_seqs) * n_kv_heads * prm.pairs_per_seq;
     if (grid <= 0) return int(SB_OK);
     kern<<<static_cast<unsigned>(grid), attn::kThreads, attn::kSmemBytes, static_cast<cudaStream_t>(stream)>>>(

@@ -58,7 +58,7 @@ constexpr int kCandSmem = 16384;  // candidate keys staged in shared memory (128
 constexpr int64_t kCoopMinCap = 16384;  // pools at least this large use the all-SM scorer
 
 enum Ctr { C_NRES = 0, C_EVICTED, C_LOOKUPS, C_HIT_TOK, C_LOOK_TOK, C_INS_BLOCKS, C_EV_BLOCKS, C_FULL, C_N };
-enum Scal { S_F = 0, S_K, S_FREE, S_NEV, S_STATUS, S_FAILPOS, S_NNEW, S_NCAND, S_ERRIDX, S_NLATE, S_BOUND, S_NMISS, S_N };
+enum Scal { S_F = 0, S_K, S_FREE, S_NEV, S_STATUS, S_FAILPOS, S_NNEW, S_NCAND, S_ERRIDX, S_NLATE, S_BOUND, S_NMISS, S_NLATEHIT, S_N };
 // Blocks whose ref_count is -1 (reachable only through duplicate releases)
 // become eviction candidates the moment an insert hits them; at most this
 // many are tracked per insert.
@@ -2145,8 +2145,11 @@ struct sb_kv_cache {
   // an op failed.  max_pos / total_pos: block positions of the largest
   // insert / of all inserts; pushes: worst-case candidate pushes.  Returns
   // the number of ops applied (all of them unless one failed).
+  int32_t* d_first_op = nullptr;  // miss-free pin batches: first op pinning each block (INT_MAX = none)
+
   int64_t run_program(int64_t n_ops, int64_t max_pos, int64_t total_pos, int64_t pushes, int32_t* pin_cnt,
-                      int8_t* real_tag, int64_t now, cudaStream_t st, int64_t* evictions = nullptr) {
+                      int8_t* real_tag, int64_t now, cudaStream_t st, int64_t* evictions = nullptr,
+                      bool all_pin = false) {
     if (max_pos > kProgMaxPos)
       throw Error(SB_ERR_UNSUPPORTED, "insert longer than " + std::to_string(kProgMaxPos) + " blocks");
     ensure_positions(std::max<int64_t>({max_pos, 2 * total_pos + 64, 64}));
@@ -2180,11 +2183,30 @@ struct sb_kv_cache {
       SB_CUDA(cudaMemsetAsync(d_created, 0, sizeof(unsigned long long) * ccap, st));
       k_set_scal<<<1, 1, 0, st>>>(S.scal, S_BOUND, 64);
       k_set_scal<<<1, 1, 0, st>>>(S.scal, S_NMISS, 0);
+      k_set_scal<<<1, 1, 0, st>>>(S.scal, S_NLATEHIT, 0);
       k_prog_bound<<<dim3(static_cast<unsigned>(n_ops - first), gy), 256, 0, st>>>(
           P, d_ops, static_cast<int>(first), static_cast<int>(n_ops), S.scal, d_pre_all);
       if (force) {  // the bound left the program short once: list every candidate
         k_set_scal<<<1, 1, 0, st>>>(S.scal, S_NMISS, 1);
         k_set_scal<<<1, 1, 0, st>>>(S.scal, S_BOUND, 2 * total_pos + 64);
+      }
+      if (all_pin && first == 0 && !force) {
+        // pin batch with no miss and no ref -1 hit: the ops commute (k_pin_nomiss_*)
+        SB_CUDA(cudaMemcpyAsync(h_pout + 4, S.scal + S_NMISS, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        SB_CUDA(cudaStreamSynchronize(st));
+        if (h_pout[4] == 0 && h_pout[5] == 0) {
+          if (!d_first_op) {
+            d_first_op = dalloc<int32_t>(P.cap);
+            SB_CUDA(cudaMemsetAsync(d_first_op, 0x7f, sizeof(int32_t) * P.cap, st));
+          }
+          const dim3 g(static_cast<unsigned>(n_ops), static_cast<unsigned>(std::min<int64_t>(gy * 128 / 256 + 1, 64)));
+          k_pin_nomiss_a<<<g, 256, 0, st>>>(P, d_ops, 0, d_pre_all, d_first_op, now);
+          k_pin_nomiss_b<<<g, 256, 0, st>>>(P, d_ops, 0, pin_cnt, d_first_op, real_tag);
+          k_pin_nomiss_c<<<g, 256, 0, st>>>(P, d_ops, 0, pin_cnt, d_first_op, d_res);
+          SB_CHECK_LAUNCH();
+          if (evictions) *evictions = 0;
+          return n_ops;
+        }
       }
       cudaStream_t saved = stream;
       stream = st;
@@ -2256,7 +2278,7 @@ struct sb_kv_cache {
     // S.prehit aliases d_prehit_all: freed once below
     void* ptrs[] = {P.tok, P.ntok, P.chain, P.parent, P.tag, P.ref, P.pinned, P.last, P.idx, P.slot, P.ctr,
                     S.hashes, S.chain_out, S.kind, S.freel, S.evicted, S.victims, S.taken, S.rank_of, S.keys,
-                    S.sortbuf, S.scal, S.late, d_ops, d_res, d_runk, d_pout, d_pre_all, d_created, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first, G.hist, G.ctr, G.keys, G.fcnt, G.ncnt, G.kmin, G.kmax};
+                    S.sortbuf, S.scal, S.late, d_ops, d_res, d_runk, d_pout, d_pre_all, d_created, d_first_op, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first, G.hist, G.ctr, G.keys, G.fcnt, G.ncnt, G.kmin, G.kmax};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (d_prof) {
@@ -2403,7 +2425,9 @@ int64_t pool_run_ops(sb_kv_cache* c, const ProgOp* h_ops, int64_t n, int32_t* d_
   c->ensure_ops(n);
   c->join_in(st);
   SB_CUDA(cudaMemcpyAsync(c->d_ops, ops.data(), sizeof(ProgOp) * n, cudaMemcpyHostToDevice, st));
-  const int64_t done = c->run_program(n, max_pos, total, pushes, d_pin_cnt, d_real_tag, now, st);
+  bool all_pin = d_pin_cnt != nullptr;
+  for (int64_t i = 0; i < n; ++i) all_pin = all_pin && h_ops[i].kind == PK_PIN;
+  const int64_t done = c->run_program(n, max_pos, total, pushes, d_pin_cnt, d_real_tag, now, st, nullptr, all_pin);
   c->join_out(st);
   SB_CUDA(cudaMemcpyAsync(h_res, c->d_res, sizeof(ProgRes) * n, cudaMemcpyDeviceToHost, st));
   SB_CUDA(cudaStreamSynchronize(st));

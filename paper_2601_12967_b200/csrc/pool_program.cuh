@@ -949,6 +949,7 @@ __global__ void __launch_bounds__(256) k_prog_bound(Pool P, const ProgOp* __rest
     atomicAdd(reinterpret_cast<unsigned long long*>(&scal[S_BOUND]), 1ull);
   } else if (P.pinned[b] == 0 && P.ref[b] <= 0) {
     atomicAdd(reinterpret_cast<unsigned long long*>(&scal[S_BOUND]), 2ull);
+    if (P.ref[b] < 0) atomicAdd(reinterpret_cast<unsigned long long*>(&scal[S_NLATEHIT]), 1ull);
   }
 }
 
@@ -992,4 +993,65 @@ __global__ void __launch_bounds__(256) k_lookup_ops_finish(Pool P, const ProgOp*
   for (int64_t p = static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x; p < f;
        p += static_cast<int64_t>(gridDim.y) * blockDim.x)
     P.last[op.ids[p]] = now;
+}
+
+// ---- miss-free pin batches: pin_partial x n in parallel --------------------
+// When no insert position of a program of PK_PIN ops misses in the
+// pre-program state (k_prog_bound: S_NMISS == 0) and none hits a ref -1
+// block, no insert can evict anything (a hit turns into a miss only after an
+// eviction, which needs a miss first), so every op's effects commute: each
+// position references its pre-probe block (ref + 1, last_used = now), every
+// block gets pinned at PARTIAL_PREFILL with its pin count raised once per op,
+// and a block's real tag is recorded by the FIRST op (in op order) that pins
+// it from count 0 (engine.cpp:273-279) — found with an atomicMin over op
+// indices.  Three grid-wide passes instead of a sequential program.
+__global__ void __launch_bounds__(256) k_pin_nomiss_a(Pool P, const ProgOp* __restrict__ ops, int first,
+                                                      const int32_t* __restrict__ pre_all, int32_t* first_op,
+                                                      int64_t now) {
+  const int o = first + blockIdx.x;
+  const ProgOp op = ops[o];
+  const int64_t Pn = (op.n + P.bs - 1) / P.bs;
+  for (int64_t p = static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x; p < Pn;
+       p += static_cast<int64_t>(gridDim.y) * blockDim.x) {
+    const int32_t b = pre_all[op.pos_off + p];
+    atomicAdd(&P.ref[b], 1);
+    P.last[b] = now;
+    op.ids[p] = b;
+    atomicMin(&first_op[b], o);
+  }
+}
+__global__ void __launch_bounds__(256) k_pin_nomiss_b(Pool P, const ProgOp* __restrict__ ops, int first,
+                                                      const int32_t* __restrict__ pin_cnt, const int32_t* first_op,
+                                                      int8_t* real_tag) {
+  const int o = first + blockIdx.x;
+  const ProgOp op = ops[o];
+  const int64_t Pn = (op.n + P.bs - 1) / P.bs;
+  for (int64_t p = static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x; p < Pn;
+       p += static_cast<int64_t>(gridDim.y) * blockDim.x) {
+    const int32_t b = op.ids[p];
+    if (first_op[b] == o && pin_cnt[b] == 0) {
+      const int cur = P.tag[b];
+      real_tag[b] = static_cast<int8_t>(cur != SB_TAG_PARTIAL_PREFILL ? cur
+                                                                      : engine_tag_at(op.real_tags, op.n_real_tags,
+                                                                                      p * P.bs));
+    }
+  }
+}
+__global__ void __launch_bounds__(256) k_pin_nomiss_c(Pool P, const ProgOp* __restrict__ ops, int first,
+                                                      int32_t* pin_cnt, int32_t* first_op, ProgRes* res) {
+  const int o = first + blockIdx.x;
+  const ProgOp op = ops[o];
+  const int64_t Pn = (op.n + P.bs - 1) / P.bs;
+  for (int64_t p = static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x; p < Pn;
+       p += static_cast<int64_t>(gridDim.y) * blockDim.x) {
+    const int32_t b = op.ids[p];
+    atomicAdd(&pin_cnt[b], 1);
+    P.pinned[b] = 1;
+    P.tag[b] = SB_TAG_PARTIAL_PREFILL;
+    op.chain[p] = b;
+    op.pinned[p] = b;
+    first_op[b] = 0x7fffffff;
+  }
+  if (blockIdx.y == 0 && threadIdx.x == 0)
+    res[o] = ProgRes{SB_OK, PO_PINNED, static_cast<int32_t>(Pn), static_cast<int32_t>(Pn)};
 }
