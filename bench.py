@@ -268,6 +268,7 @@ def run_ours(args, rank, world, local_rank):
     hits, status, _ = batch.results()
     hit_rate = float(hits.sum()) / float(sum(batch.full_lens))
     stats = eng.cache.stats()
+    prog_stats = eng.cache.program_stats()
     assert (status == 0).all() and (batch.pin_outcomes() == 1).all()
 
     # max over ranks; NCCL only for the cross-GPU statistics reduction
@@ -341,6 +342,8 @@ def run_ours(args, rank, world, local_rank):
                  "phases_ms": {"submit_and_pin": pool_ms[0], "extend_and_complete": pool_ms[1],
                                "finish": pool_ms[2]},
                  "tokens_per_s_pool_only": tokens_per_step * world / (pool_total * 1e-3),
+                 "op_programs": prog_stats | {"note": "engine op programs run / applied by the parallel path "
+                                                      "(pool_batch.cuh) instead of the one-CTA sequential program"},
                  "note": "CUDA events around the engine-side KV phases of the last timed step (hashing, lookups, "
                          "op programs incl. their scoring/select and host syncs); the rest of the step is KV "
                          "append + attention"},

@@ -34,14 +34,23 @@ def peaks():
 _FLUSH = None
 
 
+_CLEAN = None
+
+
 def flush_l2():
-    """Overwrite a buffer twice the size of L2 so the next launch reads HBM."""
+    """Overwrite a buffer twice the size of L2 so the next launch reads HBM,
+    then read a second buffer of the same size so the lines L2 holds are
+    clean: the write-back of the flush's dirty lines is not charged to the
+    kernel that follows (SB_FLUSH=write keeps the write-only flush)."""
     import torch
 
-    global _FLUSH
+    global _FLUSH, _CLEAN
     if _FLUSH is None:
         _FLUSH = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
+        _CLEAN = torch.ones(64 << 20, dtype=torch.int32, device="cuda")
     _FLUSH.fill_(1)
+    if os.environ.get("SB_FLUSH", "writeread") != "write":
+        _CLEAN.max()
 
 
 def timed(fn, reps=10, warm=3, kernels=(), flush=False):

@@ -209,6 +209,9 @@ int sb_kv_release_batch(sb_kv_cache* cache, const int32_t* d_ids, int64_t n, int
 /* Counters for the cross-GPU statistics reduction: [lookups, hit_tokens,
  * looked_up_tokens, inserted_blocks, evicted_blocks, cache_full_events]. */
 int sb_kv_stats(const sb_kv_cache* cache, uint64_t out[6]);
+/* Diagnostics of the batched op programs (no reference counterpart):
+ * [programs run, programs applied by the parallel path]. */
+int sb_kv_program_stats(const sb_kv_cache* cache, uint64_t out[2]);
 
 /* ---- continuation-prefill attention over the paged pool --------------- */
 /* Replaces the prefill cost model of the reference engine

@@ -68,6 +68,7 @@ SIGNATURES = {
     "sb_kv_insert_batch": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int64, VP, VP, VP]),
     "sb_kv_release_batch": (C.c_int, [VP, VP, C.c_int64, VP, VP]),
     "sb_kv_stats": (C.c_int, [VP, U64P]),
+    "sb_kv_program_stats": (C.c_int, [VP, U64P]),
     "sb_continuation_attention": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                             C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_float, VP,
                                             C.c_int32, VP]),

@@ -1960,6 +1960,7 @@ __global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
 }
 
 #include "pool_program.cuh"
+#include "pool_batch.cuh"
 
 // PK_INSERT descriptors of a device-described batch (sb_kv_insert_batch).
 __global__ void k_build_insert_ops(ProgOp* ops, const uint64_t* tokens, const int64_t* seq_off, const sb_tag_range* tags,
@@ -2083,6 +2084,10 @@ struct sb_kv_cache {
   unsigned long long* d_created = nullptr;  // chain hashes created by a program
   int64_t created_cap = 0;
   int prog_device_attr = -1;
+  // parallel op-program path (pool_batch.cuh)
+  FastBuf FB{};
+  int64_t fb_ops_cap = 0, fb_pos_cap = 0, fb_ev_cap = 0, fb_dup_cap = 0;
+  unsigned long long fast_runs = 0, fast_taken = 0;
   std::vector<int32_t> last_evicted;  // ids evicted by the last per-op insert / evict (sb_kv_last_evicted)
 
   bool use_coop() const { return P.cap >= kCoopMinCap && coop_grid > 0; }
@@ -2146,6 +2151,101 @@ struct sb_kv_cache {
   // insert / of all inserts; pushes: worst-case candidate pushes.  Returns
   // the number of ops applied (all of them unless one failed).
   int32_t* d_first_op = nullptr;  // miss-free pin batches: first op pinning each block (INT_MAX = none)
+
+  static bool fast_enabled() {
+    static int on = -1;
+    if (on < 0) {
+      const char* e = getenv("SB_PROG_FAST");
+      on = e && e[0] == '0' ? 0 : 1;
+    }
+    return on == 1;
+  }
+  // scratch of the parallel path; per-block arrays start neutral and are
+  // restored by k_fast_reset after every use
+  void ensure_fast(int64_t n_ops, int64_t total_pos, int64_t events) {
+    if (!FB.hit_op) {
+      FB.hit_op = dalloc<int32_t>(P.cap);
+      FB.hit_max = dalloc<int32_t>(P.cap);
+      FB.dref = dalloc<int32_t>(P.cap);
+      FB.ev_max = dalloc<int32_t>(P.cap);
+      FB.nrel = dalloc<int32_t>(P.cap);
+      FB.nunp = dalloc<int32_t>(P.cap);
+      FB.flags = dalloc<int32_t>(P.cap);
+      FB.ctl = dalloc<int64_t>(FC_N);
+      k_fill_i32<<<grid_for(P.cap), 256>>>(FB.hit_op, P.cap, kNoOp);
+      k_fill_i32<<<grid_for(P.cap), 256>>>(FB.hit_max, P.cap, -1);
+      k_fill_i32<<<grid_for(P.cap), 256>>>(FB.ev_max, P.cap, -1);
+      SB_CUDA(cudaMemset(FB.dref, 0, sizeof(int32_t) * P.cap));
+      SB_CUDA(cudaMemset(FB.nrel, 0, sizeof(int32_t) * P.cap));
+      SB_CUDA(cudaMemset(FB.nunp, 0, sizeof(int32_t) * P.cap));
+      SB_CUDA(cudaMemset(FB.flags, 0, sizeof(int32_t) * P.cap));
+      SB_CUDA(cudaDeviceSynchronize());
+    }
+    if (n_ops + 1 > fb_ops_cap) {
+      cudaFree(FB.miss_cnt);
+      cudaFree(FB.miss_base);
+      fb_ops_cap = std::max<int64_t>(n_ops + 1, 2 * fb_ops_cap);
+      FB.miss_cnt = dalloc<int32_t>(fb_ops_cap);
+      FB.miss_base = dalloc<int32_t>(fb_ops_cap);
+    }
+    if (total_pos + 1 > fb_pos_cap) {
+      cudaFree(FB.mrank);
+      cudaFree(FB.mpos);
+      cudaFree(FB.miss_id);
+      cudaFree(FB.mflag);
+      fb_pos_cap = std::max<int64_t>(total_pos + 1, 2 * fb_pos_cap);
+      FB.mrank = dalloc<int32_t>(fb_pos_cap);
+      FB.mpos = dalloc<int32_t>(fb_pos_cap);
+      FB.miss_id = dalloc<int32_t>(fb_pos_cap);
+      FB.mflag = dalloc<uint8_t>(fb_pos_cap);
+    }
+    if (events + 1 > fb_ev_cap) {
+      cudaFree(FB.pend_raw_key);
+      cudaFree(FB.pend_raw_op);
+      cudaFree(FB.pend_key);
+      cudaFree(FB.pend_who);
+      fb_ev_cap = std::max<int64_t>(events + 1, 2 * fb_ev_cap);
+      FB.pend_raw_key = dalloc<uint64_t>(fb_ev_cap);
+      FB.pend_raw_op = dalloc<int32_t>(fb_ev_cap);
+      FB.pend_key = dalloc<uint64_t>(fb_ev_cap);
+      FB.pend_who = dalloc<int32_t>(fb_ev_cap);
+    }
+    int64_t dc = 1024;
+    while (dc < 2 * total_pos + 64) dc <<= 1;
+    if (dc > fb_dup_cap) {
+      cudaFree(FB.dup);
+      fb_dup_cap = dc;
+      FB.dup = dalloc<unsigned long long>(fb_dup_cap);
+    }
+    FB.dup_mask = dc - 1;
+  }
+  // the parallel path for ops [0, n_ops); stream-ordered, decides on the device
+  void launch_fast(int64_t n_ops, int64_t max_pos, int64_t total_pos, int64_t pushes, int32_t* pin_cnt,
+                   int8_t* real_tag, int64_t now, cudaStream_t st) {
+    ensure_fast(n_ops, total_pos, std::max(pushes, total_pos) + total_pos + 64);
+    SB_CUDA(cudaMemsetAsync(FB.ctl, 0, sizeof(int64_t) * FC_N, st));
+    SB_CUDA(cudaMemsetAsync(FB.dup, 0, sizeof(unsigned long long) * (FB.dup_mask + 1), st));
+    const unsigned no = static_cast<unsigned>(n_ops);
+    const dim3 g2(no, static_cast<unsigned>(std::min<int64_t>(64, std::max<int64_t>(1, (max_pos + 255) / 256))));
+    k_fast_events<<<no, kFastThreads, 0, st>>>(P, d_ops, d_pre_all, pin_cnt, FB);
+    k_fast_blocks<<<no, 256, 0, st>>>(P, d_ops, d_pre_all, pin_cnt, real_tag, now, FB);
+    k_fast_plan<<<1, kFastThreads, 0, st>>>(P, S, d_ops, static_cast<int>(n_ops), now, FB);
+    k_fast_touch<<<g2, 256, 0, st>>>(P, d_ops, d_pre_all, pin_cnt, real_tag, now, FB);
+    k_fast_evict<<<grid_for(std::max<int64_t>(total_pos, 1)), 256, 0, st>>>(P, FB);
+    k_fast_create<<<g2, 256, 0, st>>>(P, d_ops, d_pre_all, now, FB);
+    if (pin_cnt) {
+      if (!d_first_op) {
+        d_first_op = dalloc<int32_t>(P.cap);
+        k_fill_i32<<<grid_for(P.cap), 256, 0, st>>>(d_first_op, P.cap, kNoOp);
+      }
+      k_fast_pin_a<<<g2, 256, 0, st>>>(P, d_ops, d_first_op, FB);
+      k_fast_pin_b<<<g2, 256, 0, st>>>(P, d_ops, pin_cnt, d_first_op, real_tag, FB);
+      k_fast_pin_c<<<g2, 256, 0, st>>>(P, d_ops, pin_cnt, d_first_op, FB);
+    }
+    k_fast_reset<<<g2, 256, 0, st>>>(P, d_ops, d_pre_all, FB);
+    k_fast_finish<<<no, 256, 0, st>>>(P, S, d_ops, d_res, static_cast<int>(n_ops), d_pout, FB);
+    SB_CHECK_LAUNCH();
+  }
 
   int64_t run_program(int64_t n_ops, int64_t max_pos, int64_t total_pos, int64_t pushes, int32_t* pin_cnt,
                       int8_t* real_tag, int64_t now, cudaStream_t st, int64_t* evictions = nullptr,
@@ -2218,12 +2318,20 @@ struct sb_kv_cache {
         throw;
       }
       stream = saved;
+      const bool fast = first == 0 && !force && fast_enabled();
+      if (fast) launch_fast(n_ops, max_pos, total_pos, pushes, pin_cnt, real_tag, now, st);
       ProgState G{d_ops, d_res, static_cast<int32_t>(n_ops), static_cast<int32_t>(first), pin_cnt, real_tag,
-                  d_runk, runk_cap, d_pout, now, d_pre_all, d_created, ccap - 1, prof_buf()};
+                  d_runk, runk_cap, d_pout, now, d_pre_all, d_created, ccap - 1, prof_buf(),
+                  fast ? FB.ctl + FC_DONE : nullptr};
       k_program<<<1, kProgThreads, kProgSmem, st>>>(P, S, G);
       SB_CHECK_LAUNCH();
       SB_CUDA(cudaMemcpyAsync(h_pout, d_pout, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      if (fast) SB_CUDA(cudaMemcpyAsync(h_pout + 6, FB.ctl + FC_DONE, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
       SB_CUDA(cudaStreamSynchronize(st));
+      if (fast) {
+        ++fast_runs;
+        fast_taken += h_pout[6] ? 1 : 0;
+      }
       const int64_t next = h_pout[0];
       evs += h_pout[2];
       tomb_bound += h_pout[2];
@@ -2281,6 +2389,12 @@ struct sb_kv_cache {
                     S.sortbuf, S.scal, S.late, d_ops, d_res, d_runk, d_pout, d_pre_all, d_created, d_first_op, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first, G.hist, G.ctr, G.keys, G.fcnt, G.ncnt, G.kmin, G.kmax};
     for (void* p : ptrs)
       if (p) cudaFree(p);
+    void* fptrs[] = {FB.hit_op, FB.hit_max, FB.dref, FB.ev_max, FB.nrel, FB.nunp, FB.flags, FB.miss_cnt, FB.miss_base,
+                     FB.mrank, FB.mpos, FB.miss_id, FB.mflag, FB.pend_raw_key, FB.pend_raw_op, FB.pend_key,
+                     FB.pend_who, FB.dup, FB.ctl};
+    for (void* p : fptrs)
+      if (p) cudaFree(p);
+    if (d_prof) fprintf(stderr, "SB_PROG_PROFILE parallel path: %llu of %llu programs\n", fast_taken, fast_runs);
     if (d_prof) {
       unsigned long long h[64] = {};
       cudaMemcpy(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost);
@@ -3070,6 +3184,14 @@ int sb_kv_dump(const sb_kv_cache* c, char* buf, int64_t cap, int64_t* len) {
       std::memcpy(buf, out.data(), m);
       buf[m] = 0;
     }
+    return int(SB_OK);
+  });
+}
+
+int sb_kv_program_stats(const sb_kv_cache* c, uint64_t out[2]) {
+  return guard([&] {
+    out[0] = c->fast_runs;
+    out[1] = c->fast_taken;
     return int(SB_OK);
   });
 }

@@ -56,6 +56,7 @@ struct ProgState {
   unsigned long long* created;  // chain hashes of blocks created by this program (open addressing, 0 = empty)
   int64_t created_mask;
   unsigned long long* prof;     // SB_PROG_PROFILE: cycles per program phase (thread 0), else null
+  const int64_t* skip;          // non-null and set: the parallel path (pool_batch.cuh) applied the program
 };
 // phase clock (thread 0, at barrier points): cycles since the previous mark
 #define PROG_T(k)                                                    \
@@ -752,6 +753,7 @@ __global__ void __launch_bounds__(kProgThreads, 1) k_program(Pool P, Scratch S, 
   __shared__ ProgShared sh;
   __shared__ sb_tag_range pin_range;
   const int t = threadIdx.x;
+  if (G.skip && *G.skip) return;
   if (t == 0) {
     sh.K = S.scal[S_K];
     sh.F = S.scal[S_FREE];

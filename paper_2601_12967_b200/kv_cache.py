@@ -183,3 +183,9 @@ class KvCache:
         _lib.check(self._L.sb_kv_stats(self._h, out), "stats")
         keys = ["lookups", "hit_tokens", "looked_up_tokens", "inserted_blocks", "evicted_blocks", "cache_full"]
         return dict(zip(keys, [int(x) for x in out]))
+
+    def program_stats(self) -> dict:
+        """Op programs run on this pool and how many the parallel path applied."""
+        out = (C.c_uint64 * 2)()
+        _lib.check(self._L.sb_kv_program_stats(self._h, out), "program_stats")
+        return {"programs": int(out[0]), "parallel": int(out[1])}

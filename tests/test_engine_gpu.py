@@ -93,3 +93,5 @@ def test_engine_steps_match_reference_at_bench_shape():
     eng = ContinuationEngine(ModelShape(n_layers=1, n_q_heads=8, n_kv_heads=2, head_dim=128), cap, policy=1)
     run_and_check(eng, reqs, cap, 1, steps=3, sys_len=2048)
     assert eng.cache.total_evicted() > 5000
+    st = eng.cache.program_stats()  # the batched programs ran on the parallel path (pool_batch.cuh)
+    assert st["parallel"] >= 2 * 3, st
