@@ -571,12 +571,25 @@ struct sb_batch {
   __nv_bfloat16 *q = nullptr, *k_new = nullptr, *v_new = nullptr, *out = nullptr;
   std::vector<cudaEvent_t> ev0, ev1;
   cudaEvent_t evp[6] = {};  // pool phases of a timed run: [0,1) submit+pin, [2,3) extend+complete, [4,5) finish
+  // Prefix hashing of the NEXT step's calls runs on a side stream while this
+  // step's attention runs (the tool-independent prefix is known before the
+  // tool returns, paper section 4.2): two hash buffers, the next step's
+  // prefix blocks hashed into the one this step does not use.
+  uint64_t* hbuf[2] = {nullptr, nullptr};
+  int hsel = 0;
+  bool hready[2] = {false, false};
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_side_in = nullptr, ev_side_out[2] = {nullptr, nullptr};
   double attn_flops = 0;
   sb_model* model = nullptr;
   ModelWorkspace* mw = nullptr;
   ~sb_batch() {
     for (auto e : evp)
       if (e) cudaEventDestroy(e);
+    for (auto e : {ev_side_in, ev_side_out[0], ev_side_out[1]})
+      if (e) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
+    if (hbuf[1]) cudaFree(hbuf[1]);
     cudaSetDevice(eng->device);
     model_workspace_destroy(mw);
     void* ptrs[] = {tokens, hashes, suffix, keys, ids, chain, pinned, tags, suffix_off, slot_off, resp_pos, chain_off, hits,
@@ -666,6 +679,11 @@ int sb_batch_create(sb_engine* e, int32_t n, const uint64_t* prefix_tokens, cons
       b->tokens = upload(toks);
       b->tags = upload(tags);
       b->hashes = dmalloc<uint64_t>(b->total_blk_cap);
+      b->hbuf[0] = b->hashes;
+      b->hbuf[1] = dmalloc<uint64_t>(b->total_blk_cap);
+      SB_CUDA(cudaStreamCreateWithFlags(&b->side, cudaStreamNonBlocking));
+      SB_CUDA(cudaEventCreateWithFlags(&b->ev_side_in, cudaEventDisableTiming));
+      for (auto& ev : b->ev_side_out) SB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
       b->ids = dmalloc<int32_t>(b->total_blk_cap);
       b->chain = dmalloc<int32_t>(b->total_blk_cap);
       b->pinned = dmalloc<int32_t>(b->total_blk_cap);
@@ -792,8 +810,19 @@ int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention
       if (s) throw Error(s, sb_last_error());
     };
     if (time_attention) SB_CUDA(cudaEventRecord(b->evp[0], st));
-    // 1. submit_partial_prefill x n: prefix chain hashes + admission lookups (engine.cpp:170)
-    chk(sb_chain_hash_segments(b->tokens, b->seg_pre, b->blk_pre, nullptr, n, 16, b->hashes, st));
+    // this step's hash buffer (the ops read their chain hashes from it)
+    b->hashes = b->hbuf[b->hsel];
+    for (auto* v : {&b->lookup_ops, &b->pin_ops, &b->complete_ops, &b->finish_ops})
+      for (int i = 0; i < n; ++i) (*v)[i].hashes = b->hashes + b->blk_off_h[static_cast<size_t>(i)];
+    // 1. submit_partial_prefill x n: prefix chain hashes (hashed ahead on the
+    // side stream during the previous step when possible) + admission lookups (engine.cpp:170)
+    if (b->hready[b->hsel]) {
+      SB_CUDA(cudaStreamWaitEvent(st, b->ev_side_out[b->hsel], 0));
+      b->hready[b->hsel] = false;
+    } else {
+      chk(sb_chain_hash_segments(b->tokens, b->seg_pre, b->blk_pre, nullptr, n, 16, b->hashes, st));
+    }
+    SB_CUDA(cudaEventRecord(b->ev_side_in, st));  // the other buffer's last readers (previous step) are done
     pool_lookup(e->cache, b->lookup_ops.data(), n, now, b->hits, st);
     n_launch += 4;
     // 2. the prefix prefill completes: pin_partial x n (program)
@@ -861,6 +890,15 @@ int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention
         n_launch += 2;
       }
     }
+    // the next step's prefix hashes, overlapping this step's attention
+    {
+      const int nx = b->hsel ^ 1;
+      SB_CUDA(cudaStreamWaitEvent(b->side, b->ev_side_in, 0));
+      chk(sb_chain_hash_segments(b->tokens, b->seg_pre, b->blk_pre, nullptr, n, 16, b->hbuf[nx], b->side));
+      SB_CUDA(cudaEventRecord(b->ev_side_out[nx], b->side));
+      b->hready[nx] = true;
+      n_launch += 1;
+    }
     // 6. finish_decode x n with the first response token (program)
     if (time_attention) SB_CUDA(cudaEventRecord(b->evp[4], st));
     k_response_tokens<<<(n + 127) / 128, 128, 0, st>>>(model_tok, b->keys, b->resp_pos, n, b->tokens);
@@ -870,6 +908,7 @@ int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention
     pool_run_ops(e->cache, b->finish_ops.data(), n, e->d_pin_cnt, e->d_real_tag, now, st, b->res.data());
     if (time_attention) SB_CUDA(cudaEventRecord(b->evp[5], st));
     n_launch += 4;
+    b->hsel ^= 1;
     if (launches) *launches = n_launch;
     return int(SB_OK);
   });

@@ -2229,7 +2229,7 @@ struct sb_kv_cache {
     const dim3 g2(no, static_cast<unsigned>(std::min<int64_t>(64, std::max<int64_t>(1, (max_pos + 255) / 256))));
     k_fast_events<<<no, kFastThreads, 0, st>>>(P, d_ops, d_pre_all, pin_cnt, FB);
     k_fast_blocks<<<no, 256, 0, st>>>(P, d_ops, d_pre_all, pin_cnt, real_tag, now, FB);
-    k_fast_plan<<<1, kFastThreads, 0, st>>>(P, S, d_ops, static_cast<int>(n_ops), now, FB);
+    k_fast_plan<<<1, kFastThreads, kPlanSmem, st>>>(P, S, d_ops, static_cast<int>(n_ops), now, FB, prof_buf());
     k_fast_touch<<<g2, 256, 0, st>>>(P, d_ops, d_pre_all, pin_cnt, real_tag, now, FB);
     k_fast_evict<<<grid_for(std::max<int64_t>(total_pos, 1)), 256, 0, st>>>(P, FB);
     k_fast_create<<<g2, 256, 0, st>>>(P, d_ops, d_pre_all, now, FB);
@@ -2273,6 +2273,7 @@ struct sb_kv_cache {
     }
     if (prog_device_attr != device) {
       SB_CUDA(cudaFuncSetAttribute(k_program, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kProgSmem)));
+      SB_CUDA(cudaFuncSetAttribute(k_fast_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPlanSmem)));
       prog_device_attr = device;
     }
     int64_t first = 0, evs = 0;
@@ -2394,7 +2395,12 @@ struct sb_kv_cache {
                      FB.pend_who, FB.dup, FB.ctl};
     for (void* p : fptrs)
       if (p) cudaFree(p);
-    if (d_prof) fprintf(stderr, "SB_PROG_PROFILE parallel path: %llu of %llu programs\n", fast_taken, fast_runs);
+    if (d_prof) {
+      unsigned long long hp[64] = {};
+      cudaMemcpy(hp, d_prof, sizeof(hp), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "SB_PROG_PROFILE parallel path: %llu of %llu programs; k_fast_plan walks %llu: prelude %llu walk %llu cycles\n",
+              fast_taken, fast_runs, hp[62], hp[60], hp[61]);
+    }
     if (d_prof) {
       unsigned long long h[64] = {};
       cudaMemcpy(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost);

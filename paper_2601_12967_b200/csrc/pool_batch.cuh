@@ -51,6 +51,10 @@ enum MissFlag { MF_EXISTING = 1, MF_SUPERSEDED = 2 };
 constexpr int kFastThreads = 1024;
 constexpr int kFastMaxOps = 1024;  // ops of a program whose new candidates are tracked per op (kFastPlan smem)
 constexpr int32_t kNoOp = 0x7fffffff;
+constexpr int kPlanWin = 4096;     // victim-list entries k_fast_plan stages in shared memory
+constexpr int kPlanNew = 4096;     // new blocks of FINISH ops tracked as candidates (shared memory)
+constexpr size_t kPlanSmem = (2 * kFastMaxOps + kPlanWin + kPlanNew) * sizeof(uint64_t) +
+                             (7 * kFastMaxOps + 2 + kPlanWin + 2 * kPlanNew) * sizeof(int32_t);
 
 struct FastBuf {
   // per pool block (cap), neutral values restored by k_fast_reset
@@ -250,12 +254,10 @@ __global__ void __launch_bounds__(256) k_fast_blocks(Pool P, const ProgOp* __res
 
 // ---- 3. one CTA: rank the misses, decide every miss's id in the reference's order
 __global__ void __launch_bounds__(kFastThreads) k_fast_plan(Pool P, Scratch S, const ProgOp* __restrict__ ops,
-                                                            int n_ops, int64_t now, FastBuf F) {
+                                                            int n_ops, int64_t now, FastBuf F,
+                                                            unsigned long long* prof) {
+  const unsigned long long c0 = clock64();
   __shared__ uint32_t warp_sums[33];
-  __shared__ int32_t seg_base[kFastMaxOps + 1];  // pending segment of op o: [seg_base[o], seg_base[o + 1])
-  __shared__ int32_t seg_fill[kFastMaxOps];
-  __shared__ uint64_t seg_min[kFastMaxOps];
-  __shared__ int32_t seg_arg[kFastMaxOps];
   __shared__ int any_finish_miss, fail_sh;
   const int t = threadIdx.x, lane = t & 31;
   if (F.ctl[FC_FAIL]) return;
@@ -335,41 +337,108 @@ __global__ void __launch_bounds__(kFastThreads) k_fast_plan(Pool P, Scratch S, c
     return;
   }
   if (n_ops > kFastMaxOps) return fast_fail(F);
-  // ---- pending segments: existing new candidates by op z, then room for the
-  // FINISH ops' own new blocks (each becomes a candidate after its release)
-  for (int o = t; o < n_ops; o += blockDim.x) seg_fill[o] = 0;
-  __syncthreads();
-  for (int64_t i = t; i < npend; i += blockDim.x) atomicAdd(&seg_fill[F.pend_raw_op[i]], 1);
-  __syncthreads();
-  if (t == 0) {
-    int acc = 0;
-    for (int o = 0; o < n_ops; ++o) {
-      seg_base[o] = acc;
-      acc += seg_fill[o] + (ops[o].kind == PK_FINISH ? F.miss_cnt[o] : 0);
-      seg_fill[o] = 0;
-    }
-    seg_base[n_ops] = acc;
+  // ---- new candidates by the op z from which they are candidates:
+  //   E part: pool blocks reaching ref 0 & unpinned at their last event
+  //           (k_fast_blocks), segment [segE[z], segE[z + 1]) of F.pend_key;
+  //   N part: FINISH's own new blocks (candidates once it releases its
+  //           insert's refs), [noff[z], noff[z + 1]) of nkey in shared memory.
+  extern __shared__ __align__(16) uint8_t plan_dyn[];
+  uint64_t* minE = reinterpret_cast<uint64_t*>(plan_dyn);
+  uint64_t* minN = minE + kFastMaxOps;
+  uint64_t* lkey = minN + kFastMaxOps;    // list window: keys
+  uint64_t* nkey = lkey + kPlanWin;       // N entries: key (id or-ed in when assigned)
+  int32_t* segE = reinterpret_cast<int32_t*>(nkey + kPlanNew);
+  int32_t* noff = segE + kFastMaxOps + 1;
+  int32_t* fillE = noff + kFastMaxOps + 1;
+  int32_t* argE = fillE + kFastMaxOps;
+  int32_t* argN = argE + kFastMaxOps;
+  int32_t* mc = argN + kFastMaxOps;
+  int32_t* mb = mc + kFastMaxOps;
+  int32_t* lho = mb + kFastMaxOps;        // list window: hit_op of each entry
+  int32_t* nwho = lho + kPlanWin;         // N entries: creating miss rank
+  int32_t* nsup = nwho + kPlanNew;        // N entries: evicted later in the program (superseded)
+  for (int o = t; o < n_ops; o += blockDim.x) {
+    fillE[o] = 0;
+    mc[o] = F.miss_cnt[o];
+    mb[o] = F.miss_base[o];
+    minE[o] = kNoKey;
+    minN[o] = kNoKey;
+    argE[o] = -1;
+    argN[o] = -1;
+  }
+  const int64_t W = min64(K, kPlanWin);
+  for (int64_t i = t; i < W; i += blockDim.x) {
+    const uint64_t k = S.victims[i];
+    lkey[i] = k;
+    lho[i] = F.hit_op[static_cast<int32_t>(k & P.idmask)];
   }
   __syncthreads();
+  for (int64_t i = t; i < npend; i += blockDim.x) atomicAdd(&fillE[F.pend_raw_op[i]], 1);
+  __syncthreads();
+  if (t == 0) {
+    int acc = 0, accn = 0;
+    for (int o = 0; o < n_ops; ++o) {
+      segE[o] = acc;
+      noff[o] = accn;
+      acc += fillE[o];
+      accn += ops[o].kind == PK_FINISH ? mc[o] : 0;
+      fillE[o] = 0;
+    }
+    segE[n_ops] = acc;
+    noff[n_ops] = accn;
+    if (accn > kPlanNew) fail_sh = 1;
+  }
+  __syncthreads();
+  if (fail_sh) return fast_fail(F);  // uniform
   for (int64_t i = t; i < npend; i += blockDim.x) {
     const int z = F.pend_raw_op[i];
-    const int at = seg_base[z] + atomicAdd(&seg_fill[z], 1);
-    F.pend_key[at] = F.pend_raw_key[i];
-    F.pend_who[at] = -1;
+    const uint64_t k = F.pend_raw_key[i];
+    const int at = segE[z] + atomicAdd(&fillE[z], 1);
+    F.pend_key[at] = k;
+    atomicMin(reinterpret_cast<unsigned long long*>(&minE[z]), static_cast<unsigned long long>(k));
+  }
+  // N entries: key without the id (tier of the position's tag, last_used now)
+  const uint64_t now_bits = static_cast<uint64_t>(now + P.lbias) << P.idb;
+  for (int i = t; i < noff[n_ops]; i += blockDim.x) {
+    int lo = 0, hi = n_ops;  // op z with noff[z] <= i < noff[z + 1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (noff[mid] <= i) lo = mid; else hi = mid;
+    }
+    while (noff[lo + 1] <= i) ++lo;  // (ops without N entries share an offset)
+    const ProgOp& op = ops[lo];
+    const int32_t pos = F.mpos[op.pos_off + (i - noff[lo])];
+    uint64_t key = now_bits;
+    if (P.policy == SB_POLICY_TIERED)
+      key |= static_cast<uint64_t>(tier_of(tag_at(op.ins_tags, op.n_ins_tags, static_cast<int64_t>(pos) * P.bs))) << 61;
+    nkey[i] = key;
+    nwho[i] = mb[lo] + (i - noff[lo]);
+    nsup[i] = 0;
+  }
+  __syncthreads();
+  for (int i = t; i < segE[n_ops]; i += blockDim.x) {  // argmin of every E segment
+    int lo = 0, hi = n_ops;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (segE[mid] <= i) lo = mid; else hi = mid;
+    }
+    while (segE[lo + 1] <= i) ++lo;
+    if (F.pend_key[i] == minE[lo]) argE[lo] = i;
   }
   __syncthreads();
   if (t >= 32) return;
+  const unsigned long long c1 = clock64();
   // ---- warp 0: the sequential decisions
-  const uint64_t now_bits = static_cast<uint64_t>(now + P.lbias) << P.idb;
-  uint64_t best = kNoKey;  // smallest available new candidate
-  int best_seg = -1;
+  uint64_t best = kNoKey;  // smallest available new candidate (segments of ops before the current one)
+  int best_op = -1;
   int64_t ptr = 0;  // next list entry
   bool failed = false;
-  auto seg_scan = [&](int o) {  // seg_min / seg_arg of segment o (warp)
+  auto rescan = [&](int o, bool part_n) {  // min / argmin of one part of op o's candidates (warp)
+    const int lo = part_n ? noff[o] : segE[o], hi = part_n ? noff[o + 1] : segE[o + 1];
     uint64_t mk = kNoKey;
     int ma = -1;
-    for (int i = seg_base[o] + lane; i < seg_base[o] + seg_fill[o]; i += 32) {
-      const uint64_t k = F.pend_key[i];
+    for (int i = lo + lane; i < hi; i += 32) {
+      const uint64_t k = part_n ? nkey[i] : F.pend_key[i];
       if (k < mk) {
         mk = k;
         ma = i;
@@ -385,19 +454,26 @@ __global__ void __launch_bounds__(kFastThreads) k_fast_plan(Pool P, Scratch S, c
       }
     }
     if (lane == 0) {
-      seg_min[o] = mk;
-      seg_arg[o] = ma;
+      if (part_n) {
+        minN[o] = mk;
+        argN[o] = ma;
+      } else {
+        minE[o] = mk;
+        argE[o] = ma;
+      }
     }
     __syncwarp();
   };
-  auto find_best = [&](int upto) {  // over segments [0, upto)
+  auto find_best = [&](int upto) {  // over ops [0, upto)
     uint64_t mk = kNoKey;
     int ms = -1;
-    for (int o = lane; o < upto; o += 32)
-      if (seg_min[o] < mk) {
-        mk = seg_min[o];
+    for (int o = lane; o < upto; o += 32) {
+      const uint64_t k = min(minE[o], minN[o]);
+      if (k < mk) {
+        mk = k;
         ms = o;
       }
+    }
 #pragma unroll
     for (int d = 16; d; d >>= 1) {
       const uint64_t ok = __shfl_xor_sync(0xffffffffu, mk, d);
@@ -408,30 +484,36 @@ __global__ void __launch_bounds__(kFastThreads) k_fast_plan(Pool P, Scratch S, c
       }
     }
     best = mk;
-    best_seg = ms;
+    best_op = ms;
+  };
+  // the id taken by miss k of op o (N entries of a FINISH op record it)
+  auto assign = [&](int o, int64_t base, int k, int32_t id, uint8_t fl) {
+    F.miss_id[base + k] = id;
+    F.mflag[base + k] = fl;
+    if (noff[o + 1] > noff[o]) nkey[noff[o] + k] |= static_cast<uint64_t>(id);
   };
   for (int o = 0; o < n_ops && !failed; ++o) {
-    const int m = F.miss_cnt[o];
-    const int64_t base = F.miss_base[o];
+    const int m = mc[o];
+    const int64_t base = mb[o];
     int k = 0;
     // free ids first (alloc_block_id, kv_cache.cpp:62-67)
     if (base < free_used) {
       const int nf = static_cast<int>(min64(m, free_used - base));
-      for (int i = lane; i < nf; i += 32) {
-        F.miss_id[base + i] = S.freel[base + i];
-        F.mflag[base + i] = 0;
-      }
+      for (int i = lane; i < nf; i += 32) assign(o, base, i, S.freel[base + i], 0);
       k = nf;
     }
-    while (k < m && !failed) {
+    while (k < m) {
       const int need = m - k;
-      // the next 32 list entries: S skip (hit by an earlier op: referenced),
-      // T take (key below every new candidate), else stop: X (list end or
-      // key above the best new candidate) / B (hit by this or a later op)
+      // the next 32 list entries: skip (hit by an earlier op: referenced),
+      // take (key below every new candidate), else stop: the list end, a key
+      // above the best new candidate, or a block this or a later op hits
       const int64_t e = ptr + lane;
       uint64_t key = kNoKey;
       int ho = kNoOp;
-      if (e < K) {
+      if (e < W) {
+        key = lkey[e];
+        ho = lho[e];
+      } else if (e < K) {
         key = S.victims[e];
         ho = F.hit_op[static_cast<int32_t>(key & P.idmask)];
       }
@@ -443,29 +525,24 @@ __global__ void __launch_bounds__(kFastThreads) k_fast_plan(Pool P, Scratch S, c
       const unsigned tm = __ballot_sync(0xffffffffu, take) & (f == 32 ? 0xffffffffu : ((1u << f) - 1u));
       const int c = __popc(tm);
       const int ntake = min(c, need);
-      if (take && ((1u << lane) & tm)) {
+      if ((tm >> lane) & 1u) {
         const int j = __popc(tm & ((1u << lane) - 1u));
-        if (j < ntake) {
-          F.miss_id[base + k + j] = static_cast<int32_t>(key & P.idmask);
-          F.mflag[base + k + j] = MF_EXISTING;
-        }
+        if (j < ntake) assign(o, base, k + j, static_cast<int32_t>(key & P.idmask), MF_EXISTING);
       }
       k += ntake;
+      __syncwarp();
       if (ntake < c) {  // satisfied before the stop: resume right after the last entry taken
         unsigned rest = tm;
         for (int j = 1; j < ntake; ++j) rest &= rest - 1u;
-        ptr += __ffs(rest);  // lowest remaining bit = the ntake-th entry taken; + 1
+        ptr += __ffs(rest);
         continue;
       }
       ptr += f;  // skipped and taken entries before the stop are consumed for good
       if (k == m || f == 32) continue;
-      // lane f stops the list: the end, a key above the best new candidate, or
-      // a candidate that this or a later op hits
       const int64_t ef = __shfl_sync(0xffffffffu, e, f);
       const uint64_t kf = __shfl_sync(0xffffffffu, key, f);
-      const int hf = __shfl_sync(0xffffffffu, ho, f);
       const bool list_end = ef >= K;
-      if (!list_end && kf < best) {  // (hf != kNoOp) would take or skip a block an op hits later
+      if (!list_end && kf < best) {  // a listed block that this or a later op hits
         failed = true;
         break;
       }
@@ -477,56 +554,50 @@ __global__ void __launch_bounds__(kFastThreads) k_fast_plan(Pool P, Scratch S, c
         failed = true;
         break;
       }
-      (void)hf;
       // take the best new candidate
-      const int at = seg_arg[best_seg];
+      const bool from_n = minN[best_op] <= minE[best_op];
+      const int at = from_n ? argN[best_op] : argE[best_op];
       if (lane == 0) {
-        const int who = F.pend_who[at];
-        F.miss_id[base + k] = static_cast<int32_t>(best & P.idmask);
-        F.mflag[base + k] = who < 0 ? MF_EXISTING : 0;
-        if (who >= 0) F.mflag[who] |= MF_SUPERSEDED;
-        F.pend_key[at] = kNoKey;
+        assign(o, base, k, static_cast<int32_t>(best & P.idmask), from_n ? 0 : MF_EXISTING);
+        if (from_n) {
+          nsup[at] = 1;
+          nkey[at] = kNoKey;
+        }
+        else F.pend_key[at] = kNoKey;
       }
       __syncwarp();
       ++k;
-      seg_scan(best_seg);
+      rescan(best_op, from_n);
       find_best(o);
     }
     if (failed) break;
-    // op o's segment becomes available: its pool blocks (already there) and,
-    // for FINISH, its own new blocks (tag of the position, last_used now)
-    const ProgOp op = ops[o];
-    if (op.kind == PK_FINISH && m > 0) {
-      const sb_tag_range* tg = op.ins_tags;
-      for (int i = lane; i < m; i += 32) {
-        const int32_t id = F.miss_id[base + i];
-        const int32_t pos = F.mpos[op.pos_off + i];
-        uint64_t key = now_bits | static_cast<uint64_t>(id);
-        if (P.policy == SB_POLICY_TIERED)
-          key |= static_cast<uint64_t>(tier_of(tag_at(tg, op.n_ins_tags, static_cast<int64_t>(pos) * P.bs))) << 61;
-        F.pend_key[seg_base[o] + seg_fill[o] + i] = key;
-        F.pend_who[seg_base[o] + seg_fill[o] + i] = static_cast<int32_t>(base + i);
-      }
-      __syncwarp();
-      if (lane == 0) seg_fill[o] += m;
-      __syncwarp();
-    }
-    seg_scan(o);
-    if (seg_min[o] < best) {
-      best = seg_min[o];
-      best_seg = o;
+    // op o's candidates become available (its N keys are complete now)
+    if (noff[o + 1] > noff[o]) rescan(o, true);
+    const uint64_t so = min(minE[o], minN[o]);
+    if (so < best) {
+      best = so;
+      best_op = o;
     }
   }
+  __syncwarp();
+  if (!failed)
+    for (int i = lane; i < noff[n_ops]; i += 32)
+      if (nsup[i]) F.mflag[nwho[i]] |= MF_SUPERSEDED;
   if (lane == 0) {
     if (failed) {
       fast_fail(F);
     } else {
-      const int64_t nv = M - free_used;  // every miss past the free ids is one eviction
       F.ctl[FC_M] = M;
       F.ctl[FC_FREE_USED] = free_used;
-      F.ctl[FC_NV] = nv;
+      F.ctl[FC_NV] = M - free_used;  // every miss past the free ids is one eviction
       F.ctl[FC_DIRECT] = 0;
       F.ctl[FC_DONE] = 1;
+    }
+    if (prof) {
+      const unsigned long long c2 = clock64();
+      prof[60] += c1 - c0;
+      prof[61] += c2 - c1;
+      prof[62] += 1;
     }
   }
 }

@@ -1,0 +1,7 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_program_fastpath_gpu.py tests/test_engine_gpu.py tests/test_engine_lifecycle_gpu.py tests/test_model_gpu.py -x -q > gpurun_out/pytest_fast.log 2>&1; echo pytest_rc=$?
+tail -3 gpurun_out/pytest_fast.log
+for i in 1 2; do timeout 300 python bench_engine_ops.py; done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ops_launches_fast2.csv \
+   python bench_engine_ops.py --steps 2 --warmup 1 > gpurun_out/ops_ncu.log 2>&1; echo ncu_rc=$?
