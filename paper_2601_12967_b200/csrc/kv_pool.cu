@@ -1119,6 +1119,7 @@ struct CoopBuf {
   int n_slices;
   int64_t slice;             // blocks per score slice (multiple of 4)
   int keys_in_smem;          // k_select_coop stages its slices' keys in shared memory (else reads them in place)
+  int64_t sort_keys;         // keys k_select_coop's dynamic shared memory holds (its final sort)
 };
 constexpr int kScoreThreads = 512;
 constexpr int kSlicesPerSm = 2;  // score slices per SM; k_score CTA c scans slices c and c + n_sm
@@ -1570,11 +1571,11 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
     int64_t n2 = 1;
     while (n2 < K) n2 <<= 1;
     uint64_t* dst = S.sortbuf;
-    const bool in_smem = K <= kSortSmemKeys;  // dynamic smem holds >= kSortSmemKeys keys
+    const bool in_smem = n2 <= G.sort_keys;  // dynamic smem holds G.sort_keys keys
     if (in_smem) {
       for (int64_t i = t; i < n2; i += blockDim.x) local_keys[i] = i < K ? S.sortbuf[i] : kNoKey;
       __syncthreads();
-      if (n2 >= 1024 && 2 * n2 <= kSortSmemKeys) {  // merge sort (faster from 1K keys), scratch after the keys
+      if (n2 >= 1024 && 2 * n2 <= G.sort_keys) {  // merge sort (faster from 1K keys), scratch after the keys
         dst = merge_sort_smem(local_keys, local_keys + n2, static_cast<int>(n2));
       } else {
         bitonic_smem(local_keys, static_cast<int>(n2));
@@ -1998,14 +1999,137 @@ static void check_now(const Pool& P, int64_t now) {
     throw Error(SB_ERR_UNSUPPORTED, "now outside +-2^" + std::to_string(60 - P.idb) + " for this pool size");
 }
 
+// Batched prefix probe for 16-token blocks, two phases per CTA of
+// kProbe2 consecutive positions of one sequence, so every memory access of a
+// phase is independent and all of them are in flight at once:
+//   A  one thread per position: the position's chain hash (and its parent's,
+//      the previous element), the 32 B index slot it hashes to (one random
+//      sector); a slot whose (chain hash, parent, ntok) match names the
+//      candidate block, an empty slot is a miss, anything else (tombstone,
+//      other entry: a longer probe sequence) is left to phase C;
+//   B  eight lanes per candidate position: the block's 128 B token row and
+//      the position's 128 B of query tokens, 16 B per lane, four positions
+//      per warp per round and four rounds in flight; the eight lanes vote;
+//   C  positions A or B could not decide (probe chains, a hash collision)
+//      run the full lane-pair walk (probe_find_g).
+// The old one-kernel state machine (k_probe_rows) issued the slot and the
+// token row of a position as two dependent round trips per lane pair; ncu
+// showed it latency bound (long_scoreboard 15.3 stalls per issue).
+constexpr int kProbe2 = 256;
+__global__ void __launch_bounds__(kProbe2, 4) k_probe_rows2(Pool P, const uint64_t* __restrict__ tokens,
+                                                            const int64_t* __restrict__ seq_off,
+                                                            const int64_t* __restrict__ blk_off,
+                                                            const uint64_t* __restrict__ hashes,
+                                                            int32_t* __restrict__ prehit,
+                                                            int64_t* __restrict__ first_miss, int full_only_check) {
+  __shared__ int32_t cand[kProbe2];
+  __shared__ int32_t slow[kProbe2];
+  __shared__ int n_slow;
+  __shared__ int64_t fm;
+  const int sq = blockIdx.x, t = threadIdx.x;
+  const int64_t b0 = blk_off[sq], np = blk_off[sq + 1] - b0;
+  const int64_t j0 = static_cast<int64_t>(blockIdx.y) * kProbe2;
+  if (j0 >= np) return;  // CTA-uniform
+  const int64_t t0 = seq_off[sq], t1 = seq_off[sq + 1];
+  const int nloc = static_cast<int>(min(static_cast<int64_t>(kProbe2), np - j0));
+  if (t == 0) {
+    n_slow = 0;
+    fm = INT64_MAX;
+  }
+  // ---- A
+  int32_t c = -1;
+  if (t < nloc) {
+    const int64_t j = j0 + t;
+    const int64_t base = t0 + j * 16;
+    const int len = static_cast<int>(min(static_cast<int64_t>(16), t1 - base));
+    if (!(full_only_check && len < 16)) {
+      const uint64_t h = hashes[b0 + j];
+      const uint64_t parent = j ? hashes[b0 + j - 1] : kRootHash;
+      uint64_t key, par;
+      int32_t id, nt;
+      ld_slot(P.idx + index_slot(h, P.tcap), key, par, id, nt);
+      c = id == -1 ? -1 : (id >= 0 && key == h && par == parent && nt == len) ? id : -2;
+    }
+  }
+  cand[t] = c;
+  __syncthreads();
+  // ---- B: position q = 32 r + (t >> 3), lane part p = t & 7 holds tokens [2p, 2p + 2)
+  const int part = t & 7, lane = t & 31;
+  for (int r0 = 0; r0 < kProbe2 / 32; r0 += 4) {
+    uint64_t x[4][2], y[4][2];
+    int lens[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = 32 * (r0 + u) + (t >> 3);
+      const int32_t id = q < nloc ? cand[q] : -1;
+      const int64_t base = t0 + (j0 + q) * 16;
+      const int len = q < nloc ? static_cast<int>(min(static_cast<int64_t>(16), t1 - base)) : 0;
+      lens[u] = id >= 0 ? len : 0;
+      x[u][0] = x[u][1] = y[u][0] = y[u][1] = 0;
+      if (id >= 0) {
+        ld_v2(P.tok + static_cast<int64_t>(id) * 16 + 2 * part, x[u][0], x[u][1]);
+        if (2 * part + 1 < len && ((base + 2 * part) & 1) == 0) {
+          const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(tokens + base + 2 * part));
+          y[u][0] = v.x;
+          y[u][1] = v.y;
+        } else {
+          if (2 * part < len) y[u][0] = __ldg(reinterpret_cast<const unsigned long long*>(tokens + base + 2 * part));
+          if (2 * part + 1 < len) y[u][1] = __ldg(reinterpret_cast<const unsigned long long*>(tokens + base + 2 * part + 1));
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = 32 * (r0 + u) + (t >> 3);
+      const bool eq = (2 * part >= lens[u] || x[u][0] == y[u][0]) && (2 * part + 1 >= lens[u] || x[u][1] == y[u][1]);
+      const unsigned vote = __ballot_sync(0xffffffffu, eq);
+      const bool all8 = ((vote >> (lane & ~7)) & 0xffu) == 0xffu;
+      if (part == 0 && q < nloc && cand[q] >= 0 && !all8) cand[q] = -2;  // a chain hash collision: full walk
+    }
+  }
+  __syncthreads();
+  if (t < nloc && cand[t] == -2) slow[atomicAdd(&n_slow, 1)] = t;
+  __syncthreads();
+  // ---- C: the full walk for the undecided positions (lane pairs)
+  for (int b = 0; b < n_slow; b += kProbe2 / kGroup) {
+    const int i = b + (t >> 1);
+    const bool active = i < n_slow;
+    const int q = active ? slow[i] : slow[0];
+    const int64_t j = j0 + q;
+    const int64_t base = t0 + j * 16;
+    const int len = static_cast<int>(min(static_cast<int64_t>(16), t1 - base));
+    const uint64_t h = hashes[b0 + j];
+    const uint64_t parent = j ? hashes[b0 + j - 1] : kRootHash;
+    const int32_t id = probe_find_g<true>(P, active, h, parent, tokens + base, len, t & 1);
+    if (active && (t & 1) == 0) cand[q] = id;
+  }
+  __syncthreads();
+  if (t < nloc) {
+    const int32_t id = cand[t];
+    prehit[b0 + j0 + t] = id;
+    if (id < 0) atomicMin(reinterpret_cast<unsigned long long*>(&fm), static_cast<unsigned long long>(j0 + t));
+  }
+  __syncthreads();
+  if (t == 0 && first_miss && fm != INT64_MAX)
+    atomicMin(reinterpret_cast<unsigned long long*>(first_miss + sq), static_cast<unsigned long long>(fm));
+}
+
 static void launch_probe_rows(const Pool& P, const uint64_t* tokens, const int64_t* seq_off, const int64_t* blk_off,
                               const uint64_t* hashes, int32_t* prehit, int64_t* first_miss, int full_only_check,
                               int n_seqs, int64_t max_np, cudaStream_t st) {
   static int per = -1;
   if (per < 0) {
     const char* e = getenv("SB_PROBE_PER");
-    per = e ? atoi(e) : 2;
+    per = e ? atoi(e) : 0;  // 0: the two-phase k_probe_rows2 (16-token blocks)
   }
+  if (per == 0 && P.bs == 16) {
+    const int64_t runs = (max_np + kProbe2 - 1) / kProbe2;
+    if (runs > 65535) throw Error(SB_ERR_UNSUPPORTED, "sequence too long for one lookup launch");
+    k_probe_rows2<<<dim3(n_seqs, static_cast<unsigned>(runs)), kProbe2, 0, st>>>(P, tokens, seq_off, blk_off, hashes,
+                                                                                 prehit, first_miss, full_only_check);
+    return;
+  }
+  if (per == 0) per = 2;
   const int run = kProbePairs * per;
   const int64_t runs = (max_np + run - 1) / run;
   if (runs > 65535) throw Error(SB_ERR_UNSUPPORTED, "sequence too long for one lookup launch");
@@ -2698,9 +2822,14 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
         SB_CUDA(cudaFuncGetAttributes(&fa, k_select_coop));
         int smem_optin = 0;
         SB_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-        const size_t staged = static_cast<size_t>(std::max<int64_t>(kSlicesPerSm * slice, kSortSmemKeys)) * sizeof(uint64_t);
+        // the final sort: merge sort of up to kSortSmemKeys keys (2x scratch) when it fits
+        const size_t sort_b = 2 * kSortSmemKeys * sizeof(uint64_t);
+        const size_t sort_min = sort_b + fa.sharedSizeBytes <= static_cast<size_t>(smem_optin) ? sort_b
+                                                                                               : kSortSmemKeys * sizeof(uint64_t);
+        const size_t staged = std::max<size_t>(static_cast<size_t>(kSlicesPerSm * slice) * sizeof(uint64_t), sort_min);
         c->G.keys_in_smem = staged + fa.sharedSizeBytes <= static_cast<size_t>(smem_optin);
-        c->coop_smem = c->G.keys_in_smem ? staged : kSortSmemKeys * sizeof(uint64_t);
+        c->coop_smem = c->G.keys_in_smem ? staged : sort_min;
+        c->G.sort_keys = static_cast<int64_t>(c->coop_smem / sizeof(uint64_t));
         SB_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScoreSmem)));
         {
           SB_CUDA(cudaFuncSetAttribute(k_select_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,

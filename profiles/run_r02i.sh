@@ -1,0 +1,8 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_program_fastpath_gpu.py tests/test_engine_gpu.py tests/test_kvcache_gpu.py -x -q > gpurun_out/pytest_fast.log 2>&1; echo pytest_rc=$?
+tail -3 gpurun_out/pytest_fast.log
+timeout 300 python bench_engine_ops.py
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ops_launches_fast3.csv \
+   python bench_engine_ops.py --steps 2 --warmup 1 > gpurun_out/ops_ncu.log 2>&1; echo ncu_rc=$?
+timeout 600 python bench_kv.py --only evict_small,evict > gpurun_out/kv_evict.jsonl 2>/dev/null; echo kv=$?
