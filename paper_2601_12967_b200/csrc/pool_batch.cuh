@@ -392,10 +392,8 @@ __global__ void __launch_bounds__(kFastThreads) k_fast_plan(Pool P, Scratch S, c
   if (fail_sh) return fast_fail(F);  // uniform
   for (int64_t i = t; i < npend; i += blockDim.x) {
     const int z = F.pend_raw_op[i];
-    const uint64_t k = F.pend_raw_key[i];
     const int at = segE[z] + atomicAdd(&fillE[z], 1);
-    F.pend_key[at] = k;
-    atomicMin(reinterpret_cast<unsigned long long*>(&minE[z]), static_cast<unsigned long long>(k));
+    F.pend_key[at] = F.pend_raw_key[i];
   }
   // N entries: key without the id (tier of the position's tag, last_used now)
   const uint64_t now_bits = static_cast<uint64_t>(now + P.lbias) << P.idb;
@@ -416,14 +414,30 @@ __global__ void __launch_bounds__(kFastThreads) k_fast_plan(Pool P, Scratch S, c
     nsup[i] = 0;
   }
   __syncthreads();
-  for (int i = t; i < segE[n_ops]; i += blockDim.x) {  // argmin of every E segment
-    int lo = 0, hi = n_ops;
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (segE[mid] <= i) lo = mid; else hi = mid;
+  __syncthreads();
+  for (int o = t >> 5; o < n_ops; o += blockDim.x >> 5) {  // min / argmin of every E segment: a warp each
+    uint64_t mk = kNoKey;
+    int ma = -1;
+    for (int i = segE[o] + lane; i < segE[o + 1]; i += 32) {
+      const uint64_t k = F.pend_key[i];
+      if (k < mk) {
+        mk = k;
+        ma = i;
+      }
     }
-    while (segE[lo + 1] <= i) ++lo;
-    if (F.pend_key[i] == minE[lo]) argE[lo] = i;
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+      const uint64_t ok = __shfl_xor_sync(0xffffffffu, mk, d);
+      const int oa = __shfl_xor_sync(0xffffffffu, ma, d);
+      if (ok < mk) {
+        mk = ok;
+        ma = oa;
+      }
+    }
+    if (lane == 0) {
+      minE[o] = mk;
+      argE[o] = ma;
+    }
   }
   __syncthreads();
   if (t >= 32) return;
