@@ -584,13 +584,15 @@ struct sb_batch {
   sb_model* model = nullptr;
   ModelWorkspace* mw = nullptr;
   ~sb_batch() {
+    cudaSetDevice(eng->device);
     for (auto e : evp)
       if (e) cudaEventDestroy(e);
     for (auto e : {ev_side_in, ev_side_out[0], ev_side_out[1]})
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
-    if (hbuf[1]) cudaFree(hbuf[1]);
-    cudaSetDevice(eng->device);
+    for (auto* h : hbuf)  // (hashes aliases one of them)
+      if (h) cudaFree(h);
+    hashes = nullptr;
     model_workspace_destroy(mw);
     void* ptrs[] = {tokens, hashes, suffix, keys, ids, chain, pinned, tags, suffix_off, slot_off, resp_pos, chain_off, hits,
                     seg_pre, seg_sfx, seg_resp, blk_pre, blk_sfx, blk_resp, par_sfx, par_resp, n_blocks, table, q_off,

@@ -326,7 +326,7 @@ __device__ int32_t probe_find_g(const Pool& P, bool active, uint64_t h, uint64_t
   int32_t found = -1;
   // query tokens are only needed once a slot matches: loaded in the same
   // round trip as the block's tokens (no registers held across the walk)
-  const bool q_vec = kVec && (reinterpret_cast<uintptr_t>(t + R * part) & 15) == 0;
+  const bool q_vec = kVec && len == 16 && (reinterpret_cast<uintptr_t>(t + R * part) & 15) == 0;  // (a partial block must not read past its tokens)
   while (__any_sync(0xffffffffu, !done)) {
     bool eq = false, empty = false;
     int32_t id = -1;
