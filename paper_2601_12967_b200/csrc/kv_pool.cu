@@ -2114,6 +2114,135 @@ __global__ void __launch_bounds__(kProbe2, 4) k_probe_rows2(Pool P, const uint64
     atomicMin(reinterpret_cast<unsigned long long*>(first_miss + sq), static_cast<unsigned long long>(fm));
 }
 
+// The same three phases per WARP (32 consecutive positions, no shared memory
+// and no CTA barrier, so warps of one CTA never wait for each other — ncu of
+// the per-CTA version showed barrier stalls (8.2 per issue) next to the
+// memory latency): A one lane per position; B four positions per round with
+// eight lanes each, all rounds' loads issued before any compare; C lane pairs
+// walk the undecided positions.
+constexpr int kProbe3Warps = 8;
+__global__ void __launch_bounds__(32 * kProbe3Warps, 4) k_probe_rows3(Pool P, const uint64_t* __restrict__ tokens,
+                                                                      const int64_t* __restrict__ seq_off,
+                                                                      const int64_t* __restrict__ blk_off,
+                                                                      const uint64_t* __restrict__ hashes,
+                                                                      int32_t* __restrict__ prehit,
+                                                                      int64_t* __restrict__ first_miss,
+                                                                      int full_only_check, int speculate) {
+  const int sq = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t b0 = blk_off[sq], np = blk_off[sq + 1] - b0;
+  const int64_t jw = (static_cast<int64_t>(blockIdx.y) * kProbe3Warps + w) * 32;  // this warp's first position
+  if (jw >= np) return;  // warp-uniform
+  const int64_t t0 = seq_off[sq], t1 = seq_off[sq + 1];
+  const int nloc = static_cast<int>(min(static_cast<int64_t>(32), np - jw));
+  // ---- A: lane 0 probes the index; the blocks of one chain are usually
+  // consecutive ids (an insert allocates the lowest free ids in order), so
+  // lane l first tries block anchor + l and verifies it from the block's own
+  // metadata (chain hash, parent hash, ntok: coalesced reads); only lanes
+  // whose guess fails probe the index (a random 32 B sector each).  The
+  // verified block is the one find_chain_block returns: at most one resident
+  // block matches a (chain hash, parent, tokens) — an insert that finds one
+  // reuses it.
+  int32_t c = -1;
+  const int64_t j = jw + lane;
+  const int64_t tbase = t0 + j * 16;
+  const int tlen = static_cast<int>(min(static_cast<int64_t>(16), t1 - tbase));
+  const bool valid = lane < nloc && !(full_only_check && tlen < 16);
+  uint64_t h = 0, parent = kRootHash;
+  if (valid) {
+    h = hashes[b0 + j];
+    if (j) parent = hashes[b0 + j - 1];
+  }
+  auto idx_probe = [&]() {
+    uint64_t key, par;
+    int32_t id, nt;
+    ld_slot(P.idx + index_slot(h, P.tcap), key, par, id, nt);
+    return id == -1 ? -1 : (id >= 0 && key == h && par == parent && nt == tlen) ? id : -2;
+  };
+  int32_t a = -1;
+  if (lane == 0 && valid && speculate) a = idx_probe();
+  a = __shfl_sync(0xffffffffu, a, 0);
+  bool need_idx = false;
+  if (lane == 0 && speculate) {
+    c = a;
+  } else if (valid) {
+    need_idx = true;
+    if (a >= 0 && a + lane < P.cap) {
+      const int32_t g = a + lane;
+      if (P.ntok[g] == tlen && P.chain[g] == h && P.parent[g] == parent) {
+        c = g;
+        need_idx = false;
+      }
+    }
+  }
+  if (need_idx) c = idx_probe();
+  // ---- B: round r covers positions 4r .. 4r+3 of the warp (q = 4r + lane / 8), lane part p = lane % 8
+  const int part = lane & 7, sub = lane >> 3;
+  uint32_t bad = 0;  // bit q: position q's block tokens differ (a chain hash collision)
+#pragma unroll
+  for (int r0 = 0; r0 < 8; r0 += 4) {
+    uint64_t x[4][2], y[4][2];
+    int lens[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = 4 * (r0 + u) + sub;
+      const int32_t id = __shfl_sync(0xffffffffu, c, q);
+      const int64_t base = t0 + (jw + q) * 16;
+      const int len = q < nloc ? static_cast<int>(min(static_cast<int64_t>(16), t1 - base)) : 0;
+      lens[u] = id >= 0 ? len : 0;
+      x[u][0] = x[u][1] = y[u][0] = y[u][1] = 0;
+      if (id >= 0) {
+        ld_v2(P.tok + static_cast<int64_t>(id) * 16 + 2 * part, x[u][0], x[u][1]);
+        if (2 * part + 1 < len && ((base + 2 * part) & 1) == 0) {
+          const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(tokens + base + 2 * part));
+          y[u][0] = v.x;
+          y[u][1] = v.y;
+        } else {
+          if (2 * part < len) y[u][0] = __ldg(reinterpret_cast<const unsigned long long*>(tokens + base + 2 * part));
+          if (2 * part + 1 < len) y[u][1] = __ldg(reinterpret_cast<const unsigned long long*>(tokens + base + 2 * part + 1));
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool eq = (2 * part >= lens[u] || x[u][0] == y[u][0]) && (2 * part + 1 >= lens[u] || x[u][1] == y[u][1]);
+      const unsigned vote = __ballot_sync(0xffffffffu, !eq);  // lanes whose 2 tokens differ
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((vote >> (8 * k)) & 0xffu) bad |= 1u << (4 * (r0 + u) + k);
+    }
+  }
+  if (c >= 0 && ((bad >> lane) & 1u)) c = -2;
+  // ---- C: lane pairs walk the undecided positions, 16 at a time
+  unsigned slow = __ballot_sync(0xffffffffu, lane < nloc && c == -2);
+  while (slow) {
+    // the pair's position: the (lane / 2)-th set bit of slow
+    unsigned m = slow;
+    for (int k = 0; k < (lane >> 1) && m; ++k) m &= m - 1u;
+    const bool active = m != 0;
+    const int q = active ? __ffs(m) - 1 : __ffs(slow) - 1;
+    const int64_t j = jw + q;
+    const int64_t base = t0 + j * 16;
+    const int len = static_cast<int>(min(static_cast<int64_t>(16), t1 - base));
+    const uint64_t h = hashes[b0 + j];
+    const uint64_t parent = j ? hashes[b0 + j - 1] : kRootHash;
+    __syncwarp();
+    const int32_t id = probe_find_g<true>(P, active, h, parent, tokens + base, len, lane & 1);
+    // hand the result to the position's own lane
+    const unsigned got = __ballot_sync(0xffffffffu, active && (lane & 1) == 0);
+    for (int pr = 0; pr < 16; ++pr) {
+      if (!((got >> (2 * pr)) & 1u)) continue;  // warp-uniform
+      const int qq = __shfl_sync(0xffffffffu, q, 2 * pr);
+      const int32_t v = __shfl_sync(0xffffffffu, id, 2 * pr);
+      if (lane == qq) c = v;
+      slow &= ~(1u << qq);
+    }
+  }
+  if (lane < nloc) prehit[b0 + jw + lane] = c;
+  const unsigned miss = __ballot_sync(0xffffffffu, lane < nloc && c < 0);
+  if (lane == 0 && miss && first_miss)
+    atomicMin(reinterpret_cast<unsigned long long*>(first_miss + sq), static_cast<unsigned long long>(jw + __ffs(miss) - 1));
+}
+
 static void launch_probe_rows(const Pool& P, const uint64_t* tokens, const int64_t* seq_off, const int64_t* blk_off,
                               const uint64_t* hashes, int32_t* prehit, int64_t* first_miss, int full_only_check,
                               int n_seqs, int64_t max_np, cudaStream_t st) {
@@ -2122,7 +2251,19 @@ static void launch_probe_rows(const Pool& P, const uint64_t* tokens, const int64
     const char* e = getenv("SB_PROBE_PER");
     per = e ? atoi(e) : 0;  // 0: the two-phase k_probe_rows2 (16-token blocks)
   }
-  if (per == 0 && P.bs == 16) {
+  if (per == 0 && P.bs == 16) {  // warp-granular two-phase probe
+    const int64_t runs = (max_np + 32 * kProbe3Warps - 1) / (32 * kProbe3Warps);
+    if (runs > 65535) throw Error(SB_ERR_UNSUPPORTED, "sequence too long for one lookup launch");
+    static int spec = -1;  // SB_PROBE_SPEC=0: every position probes the index (no consecutive-id guess)
+    if (spec < 0) {
+      const char* e = getenv("SB_PROBE_SPEC");
+      spec = e && e[0] == '0' ? 0 : 1;
+    }
+    k_probe_rows3<<<dim3(n_seqs, static_cast<unsigned>(runs)), 32 * kProbe3Warps, 0, st>>>(
+        P, tokens, seq_off, blk_off, hashes, prehit, first_miss, full_only_check, spec);
+    return;
+  }
+  if (per == 3 && P.bs == 16) {  // the per-CTA two-phase probe
     const int64_t runs = (max_np + kProbe2 - 1) / kProbe2;
     if (runs > 65535) throw Error(SB_ERR_UNSUPPORTED, "sequence too long for one lookup launch");
     k_probe_rows2<<<dim3(n_seqs, static_cast<unsigned>(runs)), kProbe2, 0, st>>>(P, tokens, seq_off, blk_off, hashes,
