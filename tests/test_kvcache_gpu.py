@@ -264,3 +264,58 @@ def test_batched_block_readback_matches_block():
         for f in ("block_id", "chain_hash", "parent_hash", "tag", "tier", "ref_count", "last_used", "pinned"):
             assert getattr(b, f) == getattr(ref, f), (i, f)
     assert c.blocks([]) == []
+
+
+@pytest.mark.gpu
+def test_batched_lookup_consecutive_id_guess_and_fallbacks():
+    """The batched lookup guesses that a chain's blocks are consecutive ids
+    (k_probe_rows3) and falls back to the index per position: chains built
+    by interleaved growing inserts (ids strided by the number of chains),
+    chains with holes re-filled after evictions, chains allocated in one
+    insert (consecutive), partial hits (a differing block mid-chain) and
+    partial last blocks — hit lengths and the dump equal the oracle's."""
+    import ctypes as C
+    import torch
+    from paper_2601_12967_b200 import _lib
+
+    bs, cap = 16, 3000
+    rng = np.random.default_rng(31)
+    o = O.OracleCache(bs, cap, 1)
+    c = product(bs, cap, 1)
+    n_chains, n_blk = 20, 40
+    chains = [O.materialize(1, n_blk * bs, 900 + k) for k in range(n_chains)]
+    now = 1
+    for k in range(1, n_blk + 1):  # round k extends every chain by one block: ids strided by n_chains
+        for ch in chains[: n_chains // 2]:
+            t = ch[: k * bs]
+            a, b = o.insert(t, [(0, len(t), 2)], now), c.insert(t, [(0, len(t), 2)], now)
+            assert a == b
+            assert o.release(a[1]) == c.release(b[1]) == 0
+        now += 1
+    for ch in chains[n_chains // 2:]:  # one insert per chain: consecutive ids
+        a, b = o.insert(ch, [(0, len(ch), 3)], now), c.insert(ch, [(0, len(ch), 3)], now)
+        assert a == b
+        assert o.release(a[1]) == c.release(b[1]) == 0
+    assert o.evict(150) == c.evict(150)  # holes
+    for k in range(4):  # re-filled with new chains
+        t = O.materialize(2, int(rng.integers(100, 900)), 7000 + k)
+        a, b = o.insert(t, [(0, len(t), 1)], now), c.insert(t, [(0, len(t), 1)], now)
+        assert a == b
+    queries = []
+    for ch in chains:
+        queries.append(ch)
+        q = ch.copy()
+        q[int(rng.integers(0, len(q)))] ^= np.uint64(1)  # a partial hit
+        queries.append(q)
+        queries.append(ch[: int(rng.integers(1, len(ch)))])  # a partial last block
+    exp = [o.lookup_prefix(q, now + 1) for q in queries]
+    dev = torch.device("cuda")
+    tok = torch.from_numpy(np.concatenate(queries).view(np.int64)).to(dev)
+    off = torch.tensor(np.cumsum([0] + [len(q) for q in queries]), dtype=torch.int64, device=dev)
+    hits = torch.zeros(len(queries), dtype=torch.int64, device=dev)
+    p = lambda t: C.c_void_p(t.data_ptr())
+    _lib.check(_lib.lib().sb_kv_lookup_prefix_batch(c.c.handle, p(tok),
+                                                    p(off), None, None, None, len(queries), now + 1, p(hits), None))
+    torch.cuda.synchronize()
+    assert hits.cpu().tolist() == exp
+    assert c.dump() == o.dump()
