@@ -113,6 +113,68 @@ def ragged_batches():
     return res, stats
 
 
+def insert_batches():
+    """sb_kv_insert_batch programs (PK_INSERT ops) under pressure: batches of
+    prompts sharing prefixes (hits on blocks that are eviction candidates,
+    misses that evict), random tag ranges (some invalid: CacheError), releases
+    of random earlier inserts between batches, tight pools, both policies."""
+    import ctypes as C
+    import torch
+    from paper_2601_12967_b200 import _lib
+    from paper_2601_12967_b200.kv_cache import CacheConfig, KvCache
+
+    L = _lib.lib()
+    p = lambda t: C.c_void_p(t.data_ptr())
+    dev = torch.device("cuda")
+    out_all, stats = [], []
+    for seed in range(5):
+        rng = np.random.default_rng(700 + seed)
+        cap = int(rng.integers(60, 400))
+        cache = KvCache(CacheConfig(16, cap, int(seed % 2)))
+        bases = [rng.integers(1, 2**62, int(rng.integers(16, 300)), dtype=np.uint64) for _ in range(4)]
+        held, out = [], []
+        for rnd in range(8):
+            n = int(rng.integers(2, 12))
+            seqs, tags = [], []
+            for _ in range(n):
+                b = bases[int(rng.integers(0, len(bases)))]
+                tail = rng.integers(1, 2**62, int(rng.integers(0, 120)), dtype=np.uint64)
+                s_ = np.concatenate([b[: int(rng.integers(1, len(b) + 1))], tail])
+                seqs.append(s_)
+                cut = int(rng.integers(0, len(s_) + 1))
+                if rng.random() < 0.1:  # a gap: CacheError for this sequence
+                    tags.append([(0, max(cut - 1, 0), 1), (cut, len(s_), 2)])
+                else:
+                    tags.append([(0, cut, int(rng.integers(6))), (cut, len(s_), int(rng.integers(6)))])
+            tok = torch.from_numpy(np.concatenate(seqs).view(np.int64)).to(dev)
+            off = torch.tensor(np.cumsum([0] + [len(x) for x in seqs]), dtype=torch.int64, device=dev)
+            blk = torch.tensor(np.cumsum([0] + [(len(x) + 15) // 16 for x in seqs]), dtype=torch.int64, device=dev)
+            flat = [r for t in tags for r in t]
+            tarr = (_lib.TagRange * len(flat))()
+            for i, (b_, e_, g_) in enumerate(flat):
+                tarr[i].begin, tarr[i].end, tarr[i].tag = b_, e_, g_
+            tag_dev = torch.frombuffer(bytearray(tarr), dtype=torch.uint8).to(dev)
+            tag_off = torch.tensor(np.cumsum([0] + [len(t) for t in tags]), dtype=torch.int64, device=dev)
+            ids = torch.full((int(blk[-1]),), -1, dtype=torch.int32, device=dev)
+            status = torch.zeros(n, dtype=torch.int32, device=dev)
+            _lib.check(L.sb_kv_insert_batch(cache.handle, p(tok), p(off), p(tag_dev), p(tag_off), p(blk), None, None,
+                                            n, 10 + rnd, p(ids), p(status), None))
+            torch.cuda.synchronize()
+            st, idl, b = status.cpu().tolist(), ids.cpu().tolist(), blk.cpu().tolist()
+            for i in range(n):
+                if st[i] == 0:
+                    held.append(idl[b[i]:b[i + 1]])
+            rel = []
+            for _ in range(int(rng.integers(0, len(held) + 1))):  # release random held inserts
+                rel.append(held.pop(int(rng.integers(0, len(held)))))
+            for r in rel:
+                cache.release(r)
+            out.append([st, digest(",".join(map(str, idl))), digest(cache.dump()), cache.total_evicted()])
+        out_all.append(out)
+        stats.append(cache.program_stats())
+    return out_all, stats
+
+
 def percall_sequences():
     """Random interleavings of the per-call engine API (one op per program)."""
     from paper_2601_12967_b200.engine import ContinuationEngine
@@ -171,7 +233,9 @@ def main():
     a, sa = configs1_batches()
     b, sb = ragged_batches()
     c, sc = percall_sequences()
-    print(json.dumps({"configs1": a, "ragged": b, "percall": c, "stats": {"configs1": sa, "ragged": sb, "percall": sc}}))
+    d, sd = insert_batches()
+    print(json.dumps({"configs1": a, "ragged": b, "percall": c, "inserts": d,
+                      "stats": {"configs1": sa, "ragged": sb, "percall": sc, "inserts": sd}}))
 
 
 if __name__ == "__main__":
