@@ -597,16 +597,19 @@ def pool_rooflines():
 
     bench_kv.QUIET = True
     bench_kv.ROWS.clear()
-    bench_kv.main("hash,probe_big,evict_small,evict,append")
+    bench_kv.main("hash,probe_big,evict_small,evict,evict_big,append")
     keep = []
     for r in bench_kv.ROWS:
         keep.append({k: r[k] for k in ("kernel", "config", "achieved_gbs", "peak_gbs", "frac", "seconds",
-                                        "algorithmic_bytes", "timing") if k in r} | (
+                                        "algorithmic_bytes", "timing", "note") if k in r} | (
             {"parts_us": r["parts_us"]} if "parts_us" in r else {}))
     return {"bound": "hbm", "unit": "GB/s", "rows": keep,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
             "bytes": "algorithmic bytes per launch (bench_kv.py docstring / DESIGN.md), CUPTI device time, L2 "
-                     "flushed between launches"}
+                     "flushed between launches",
+            "size_ceiling": "a plain streaming read of 25 / 100 / 400 MB takes 12 / 27 / 80 us on this part "
+                            "(profiles/r01/stream_probe.jsonl): one pass over that much data reaches at most "
+                            "0.33 / 0.60 / 0.80 of the copy bandwidth"}
 
 
 # ----------------------------------------------------------- CPU reference

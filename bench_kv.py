@@ -94,7 +94,7 @@ ROWS = []  # every emitted row (bench.py collects them as roofline_pool)
 QUIET = False
 
 
-def emit(kernel, config, bytes_, api_s, dev_s, hbm, launches=1, parts=None):
+def emit(kernel, config, bytes_, api_s, dev_s, hbm, launches=1, parts=None, note=None):
     """frac uses the kernel's own device time when the profiler saw it."""
     sec = dev_s * launches if dev_s else api_s
     gbs = bytes_ / sec / 1e9
@@ -103,6 +103,8 @@ def emit(kernel, config, bytes_, api_s, dev_s, hbm, launches=1, parts=None):
            "achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm}
     if parts:
         row["parts_us"] = {k: round(v * 1e6, 2) for k, v in parts.items() if v}
+    if note:
+        row["note"] = note
     ROWS.append(row)
     if not QUIET:
         print(json.dumps(row), flush=True)
@@ -179,7 +181,9 @@ def main(only=None):
         api, kt = timed(lambda: L.sb_chain_hash_batch(p(tokens), p(seq_off), p(blk_off), None, n_seqs, 16, p(out), st),
                          kernels=("k_chain_hash16",), flush=True)
         emit("k_chain_hash16", f"{n_seqs} seqs x {toks} tokens", 8 * n + 8 * (n // 16), api,
-             kt.get("k_chain_hash16"), hbm)
+             kt.get("k_chain_hash16"), hbm,
+             note="one dependent 64-bit splitmix chain per sequence (~90 clk per token): fewer sequences than "
+                  "resident lanes are latency bound, many sequences ALU-pipe bound" if n_seqs < 65536 else None)
         del tokens
 
     if "probe" in only:
