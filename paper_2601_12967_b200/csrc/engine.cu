@@ -823,14 +823,14 @@ int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention
       b->hready[b->hsel] = false;
     } else {
       chk(sb_chain_hash_segments(b->tokens, b->seg_pre, b->blk_pre, nullptr, n, 16, b->hashes, st));
+      n_launch += 1;
     }
     SB_CUDA(cudaEventRecord(b->ev_side_in, st));  // the other buffer's last readers (previous step) are done
+    const uint64_t pool_l0 = pool_launches(e->cache);
     pool_lookup(e->cache, b->lookup_ops.data(), n, now, b->hits, st);
-    n_launch += 4;
     // 2. the prefix prefill completes: pin_partial x n (program)
     for (auto& o : b->pin_ops) o.n_chain = o.n_pinned = 0;
     pool_run_ops(e->cache, b->pin_ops.data(), n, e->d_pin_cnt, e->d_real_tag, now, st, b->res.data());
-    n_launch += 4;
     if (time_attention) SB_CUDA(cudaEventRecord(b->evp[1], st));
     b->pin_outcome.assign(static_cast<size_t>(n), 0);
     for (int i = 0; i < n; ++i) {
@@ -846,7 +846,6 @@ int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention
     n_launch += 2;
     // 4. complete_prefill x n (program)
     pool_run_ops(e->cache, b->complete_ops.data(), n, e->d_pin_cnt, e->d_real_tag, now, st, b->res.data());
-    n_launch += 4;
     if (time_attention) SB_CUDA(cudaEventRecord(b->evp[3], st));
     b->complete_status.assign(static_cast<size_t>(n), 0);
     for (int i = 0; i < n; ++i) {
@@ -909,7 +908,7 @@ int sb_batch_run(sb_batch* b, int64_t now, uint64_t seed, int32_t time_attention
     n_launch += 3;
     pool_run_ops(e->cache, b->finish_ops.data(), n, e->d_pin_cnt, e->d_real_tag, now, st, b->res.data());
     if (time_attention) SB_CUDA(cudaEventRecord(b->evp[5], st));
-    n_launch += 4;
+    n_launch += static_cast<int>(pool_launches(e->cache) - pool_l0);  // lookups + op programs, counted by the pool
     b->hsel ^= 1;
     if (launches) *launches = n_launch;
     return int(SB_OK);

@@ -1908,6 +1908,14 @@ __global__ void k_priority_apply(Pool P, const int32_t* ids, int64_t n, int pinn
   }
 }
 __global__ void k_set_scal(int64_t* scal, int idx, int64_t v) { scal[idx] = v; }
+// the op program's bound accumulators (k_prog_bound adds to them)
+__global__ void k_init_bound(int64_t* scal) {
+  if (threadIdx.x == 0) {
+    scal[S_BOUND] = 64;
+    scal[S_NMISS] = 0;
+    scal[S_NLATEHIT] = 0;
+  }
+}
 __global__ void k_release_status(Pool P, const int32_t* ids, int64_t n, const int64_t* scal, int32_t* status) {
   if (threadIdx.x) return;
   const int64_t e = scal[S_ERRIDX];
@@ -2353,6 +2361,7 @@ struct sb_kv_cache {
   FastBuf FB{};
   int64_t fb_ops_cap = 0, fb_pos_cap = 0, fb_ev_cap = 0, fb_dup_cap = 0;
   unsigned long long fast_runs = 0, fast_taken = 0;
+  uint64_t launches = 0;  // kernels the op programs / lookups launched (sb_batch_run reports them)
   std::vector<int32_t> last_evicted;  // ids evicted by the last per-op insert / evict (sb_kv_last_evicted)
 
   bool use_coop() const { return P.cap >= kCoopMinCap && coop_grid > 0; }
@@ -2468,12 +2477,10 @@ struct sb_kv_cache {
       cudaFree(FB.pend_raw_key);
       cudaFree(FB.pend_raw_op);
       cudaFree(FB.pend_key);
-      cudaFree(FB.pend_who);
       fb_ev_cap = std::max<int64_t>(events + 1, 2 * fb_ev_cap);
       FB.pend_raw_key = dalloc<uint64_t>(fb_ev_cap);
       FB.pend_raw_op = dalloc<int32_t>(fb_ev_cap);
       FB.pend_key = dalloc<uint64_t>(fb_ev_cap);
-      FB.pend_who = dalloc<int32_t>(fb_ev_cap);
     }
     int64_t dc = 1024;
     while (dc < 2 * total_pos + 64) dc <<= 1;
@@ -2486,19 +2493,20 @@ struct sb_kv_cache {
   }
   // the parallel path for ops [0, n_ops); stream-ordered, decides on the device
   void launch_fast(int64_t n_ops, int64_t max_pos, int64_t total_pos, int64_t pushes, int32_t* pin_cnt,
-                   int8_t* real_tag, int64_t now, cudaStream_t st) {
+                   int8_t* real_tag, int64_t now, cudaStream_t st, bool has_pin) {
     ensure_fast(n_ops, total_pos, std::max(pushes, total_pos) + total_pos + 64);
     SB_CUDA(cudaMemsetAsync(FB.ctl, 0, sizeof(int64_t) * FC_N, st));
     SB_CUDA(cudaMemsetAsync(FB.dup, 0, sizeof(unsigned long long) * (FB.dup_mask + 1), st));
     const unsigned no = static_cast<unsigned>(n_ops);
     const dim3 g2(no, static_cast<unsigned>(std::min<int64_t>(64, std::max<int64_t>(1, (max_pos + 255) / 256))));
+    launches += 7 + ((pin_cnt && has_pin) ? 3 : 0);
     k_fast_events<<<no, kFastThreads, 0, st>>>(P, d_ops, d_pre_all, pin_cnt, FB);
     k_fast_blocks<<<no, 256, 0, st>>>(P, d_ops, d_pre_all, pin_cnt, real_tag, now, FB);
     k_fast_plan<<<1, kFastThreads, kPlanSmem, st>>>(P, S, d_ops, static_cast<int>(n_ops), now, FB, prof_buf());
     k_fast_touch<<<g2, 256, 0, st>>>(P, d_ops, d_pre_all, pin_cnt, real_tag, now, FB);
     k_fast_evict<<<grid_for(std::max<int64_t>(total_pos, 1)), 256, 0, st>>>(P, FB);
     k_fast_create<<<g2, 256, 0, st>>>(P, d_ops, d_pre_all, now, FB);
-    if (pin_cnt) {
+    if (pin_cnt && has_pin) {
       if (!d_first_op) {
         d_first_op = dalloc<int32_t>(P.cap);
         k_fill_i32<<<grid_for(P.cap), 256, 0, st>>>(d_first_op, P.cap, kNoOp);
@@ -2507,14 +2515,13 @@ struct sb_kv_cache {
       k_fast_pin_b<<<g2, 256, 0, st>>>(P, d_ops, pin_cnt, d_first_op, real_tag, FB);
       k_fast_pin_c<<<g2, 256, 0, st>>>(P, d_ops, pin_cnt, d_first_op, FB);
     }
-    k_fast_reset<<<g2, 256, 0, st>>>(P, d_ops, d_pre_all, FB);
-    k_fast_finish<<<no, 256, 0, st>>>(P, S, d_ops, d_res, static_cast<int>(n_ops), d_pout, FB);
+    k_fast_finish<<<no, 256, 0, st>>>(P, S, d_ops, d_pre_all, d_res, static_cast<int>(n_ops), d_pout, FB);
     SB_CHECK_LAUNCH();
   }
 
   int64_t run_program(int64_t n_ops, int64_t max_pos, int64_t total_pos, int64_t pushes, int32_t* pin_cnt,
                       int8_t* real_tag, int64_t now, cudaStream_t st, int64_t* evictions = nullptr,
-                      bool all_pin = false) {
+                      bool all_pin = false, bool has_pin = true) {
     if (max_pos > kProgMaxPos)
       throw Error(SB_ERR_UNSUPPORTED, "insert longer than " + std::to_string(kProgMaxPos) + " blocks");
     ensure_positions(std::max<int64_t>({max_pos, 2 * total_pos + 64, 64}));
@@ -2547,12 +2554,12 @@ struct sb_kv_cache {
     while (first < n_ops) {
       SB_CUDA(cudaMemsetAsync(d_pout, 0, 8 * sizeof(int64_t), st));
       SB_CUDA(cudaMemsetAsync(d_created, 0, sizeof(unsigned long long) * ccap, st));
-      k_set_scal<<<1, 1, 0, st>>>(S.scal, S_BOUND, 64);
-      k_set_scal<<<1, 1, 0, st>>>(S.scal, S_NMISS, 0);
-      k_set_scal<<<1, 1, 0, st>>>(S.scal, S_NLATEHIT, 0);
+      k_init_bound<<<1, 32, 0, st>>>(S.scal);
+      launches += 2;
       k_prog_bound<<<dim3(static_cast<unsigned>(n_ops - first), gy), 256, 0, st>>>(
           P, d_ops, static_cast<int>(first), static_cast<int>(n_ops), S.scal, d_pre_all);
       if (force) {  // the bound left the program short once: list every candidate
+        launches += 2;
         k_set_scal<<<1, 1, 0, st>>>(S.scal, S_NMISS, 1);
         k_set_scal<<<1, 1, 0, st>>>(S.scal, S_BOUND, 2 * total_pos + 64);
       }
@@ -2566,6 +2573,7 @@ struct sb_kv_cache {
             SB_CUDA(cudaMemsetAsync(d_first_op, 0x7f, sizeof(int32_t) * P.cap, st));
           }
           const dim3 g(static_cast<unsigned>(n_ops), static_cast<unsigned>(std::min<int64_t>(gy * 128 / 256 + 1, 64)));
+          launches += 3;
           k_pin_nomiss_a<<<g, 256, 0, st>>>(P, d_ops, 0, d_pre_all, d_first_op, now);
           k_pin_nomiss_b<<<g, 256, 0, st>>>(P, d_ops, 0, pin_cnt, d_first_op, real_tag);
           k_pin_nomiss_c<<<g, 256, 0, st>>>(P, d_ops, 0, pin_cnt, d_first_op, d_res);
@@ -2585,11 +2593,12 @@ struct sb_kv_cache {
       }
       stream = saved;
       const bool fast = first == 0 && !force && fast_enabled();
-      if (fast) launch_fast(n_ops, max_pos, total_pos, pushes, pin_cnt, real_tag, now, st);
+      if (fast) launch_fast(n_ops, max_pos, total_pos, pushes, pin_cnt, real_tag, now, st, has_pin);
       ProgState G{d_ops, d_res, static_cast<int32_t>(n_ops), static_cast<int32_t>(first), pin_cnt, real_tag,
                   d_runk, runk_cap, d_pout, now, d_pre_all, d_created, ccap - 1, prof_buf(),
                   fast ? FB.ctl + FC_DONE : nullptr};
       k_program<<<1, kProgThreads, kProgSmem, st>>>(P, S, G);
+      ++launches;
       SB_CHECK_LAUNCH();
       SB_CUDA(cudaMemcpyAsync(h_pout, d_pout, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
       if (fast) SB_CUDA(cudaMemcpyAsync(h_pout + 6, FB.ctl + FC_DONE, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -2623,8 +2632,10 @@ struct sb_kv_cache {
   void launch_select(const InsertArgs& A, int s, int mode, int64_t needed) {
     if (!use_coop()) {
       k_select<<<1, kSelectThreads, select_smem(), stream>>>(P, S, A, s, mode, needed);
+      ++launches;
       return;
     }
+    launches += 3;
     k_plan<<<1, kSelectThreads, 0, stream>>>(P, S, A, s, mode, G);
     k_score<<<coop_grid, kScoreThreads, kScoreSmem, stream>>>(P, S, G);
     Pool p_ = P;
@@ -2657,7 +2668,7 @@ struct sb_kv_cache {
       if (p) cudaFree(p);
     void* fptrs[] = {FB.hit_op, FB.hit_max, FB.dref, FB.ev_max, FB.nrel, FB.nunp, FB.flags, FB.miss_cnt, FB.miss_base,
                      FB.mrank, FB.mpos, FB.miss_id, FB.mflag, FB.pend_raw_key, FB.pend_raw_op, FB.pend_key,
-                     FB.pend_who, FB.dup, FB.ctl};
+                     FB.dup, FB.ctl};
     for (void* p : fptrs)
       if (p) cudaFree(p);
     if (d_prof) {
@@ -2810,9 +2821,13 @@ int64_t pool_run_ops(sb_kv_cache* c, const ProgOp* h_ops, int64_t n, int32_t* d_
   c->ensure_ops(n);
   c->join_in(st);
   SB_CUDA(cudaMemcpyAsync(c->d_ops, ops.data(), sizeof(ProgOp) * n, cudaMemcpyHostToDevice, st));
-  bool all_pin = d_pin_cnt != nullptr;
-  for (int64_t i = 0; i < n; ++i) all_pin = all_pin && h_ops[i].kind == PK_PIN;
-  const int64_t done = c->run_program(n, max_pos, total, pushes, d_pin_cnt, d_real_tag, now, st, nullptr, all_pin);
+  bool all_pin = d_pin_cnt != nullptr, has_pin = false;
+  for (int64_t i = 0; i < n; ++i) {
+    all_pin = all_pin && h_ops[i].kind == PK_PIN;
+    has_pin = has_pin || h_ops[i].kind == PK_PIN;
+  }
+  const int64_t done =
+      c->run_program(n, max_pos, total, pushes, d_pin_cnt, d_real_tag, now, st, nullptr, all_pin, has_pin);
   c->join_out(st);
   SB_CUDA(cudaMemcpyAsync(h_res, c->d_res, sizeof(ProgRes) * n, cudaMemcpyDeviceToHost, st));
   SB_CUDA(cudaStreamSynchronize(st));
@@ -2830,6 +2845,7 @@ void pool_lookup(sb_kv_cache* c, const ProgOp* h_ops, int64_t n, int64_t now, in
   c->ensure_batch(n);
   c->join_in(st);
   SB_CUDA(cudaMemcpyAsync(c->d_ops, h_ops, sizeof(ProgOp) * n, cudaMemcpyHostToDevice, st));
+  c->launches += max_full > 0 ? 3 : 2;
   k_lookup_ops_init<<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(c->P, c->d_ops, static_cast<int>(n),
                                                                              c->d_batch_first);
   if (max_full > 0)
@@ -2842,6 +2858,7 @@ void pool_lookup(sb_kv_cache* c, const ProgOp* h_ops, int64_t n, int64_t now, in
 }
 
 cudaStream_t pool_stream(sb_kv_cache* c) { return c->stream; }
+uint64_t pool_launches(const sb_kv_cache* c) { return c->launches; }
 int pool_device(sb_kv_cache* c) { return c->device; }
 }  // namespace sb
 

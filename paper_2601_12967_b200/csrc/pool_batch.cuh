@@ -77,8 +77,7 @@ struct FastBuf {
   // new candidates: (key, op z) from k_fast_blocks; per-op segments in k_fast_plan
   uint64_t* pend_raw_key;
   int32_t* pend_raw_op;
-  uint64_t* pend_key;
-  int32_t* pend_who;  // creating miss rank (a program-created block) or -1 (a pool block)
+  uint64_t* pend_key;  // the pool blocks' new candidates by op (k_fast_plan)
   unsigned long long* dup;  // chain hashes of missing positions (open addressing, 0 = empty)
   int64_t dup_mask;
   int64_t* ctl;
@@ -764,35 +763,32 @@ __global__ void __launch_bounds__(256) k_fast_pin_c(Pool P, const ProgOp* __rest
   }
 }
 
-// ---- 8. neutral per-block scratch again (always runs, before any chain is rewritten)
-__global__ void __launch_bounds__(256) k_fast_reset(Pool P, const ProgOp* __restrict__ ops,
-                                                    const int32_t* __restrict__ pre_all, FastBuf F) {
+// ---- 8. one CTA per op: the per-block scratch neutral again (always, also
+// when the program falls back: before any chain is rewritten), then the
+// op's results and chain
+__global__ void __launch_bounds__(256) k_fast_finish(Pool P, Scratch S, const ProgOp* __restrict__ ops,
+                                                     const int32_t* __restrict__ pre_all, ProgRes* res, int n_ops,
+                                                     int64_t* out, FastBuf F) {
   const int o = blockIdx.x;
   const ProgOp op = ops[o];
   const int64_t Pn = op_positions(P, op);
-  const int64_t nc = op_releases_chain(op.kind) ? op.n_chain : 0;
-  const int64_t np = op_unpins(op.kind) ? op.n_pinned : 0;
-  for (int64_t e = blockIdx.y * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < Pn + nc + np;
-       e += static_cast<int64_t>(gridDim.y) * blockDim.x) {
-    const int32_t b = e < Pn ? pre_all[op.pos_off + e] : e < Pn + nc ? op.chain[e - Pn] : op.pinned[e - Pn - nc];
-    if (b < 0 || b >= P.cap) continue;
-    F.hit_op[b] = kNoOp;
-    F.hit_max[b] = -1;
-    F.dref[b] = 0;
-    F.ev_max[b] = -1;
-    F.nrel[b] = 0;
-    F.nunp[b] = 0;
-    F.flags[b] = 0;
+  {
+    const int64_t nc = op_releases_chain(op.kind) ? op.n_chain : 0;
+    const int64_t np = op_unpins(op.kind) ? op.n_pinned : 0;
+    for (int64_t e = threadIdx.x; e < Pn + nc + np; e += blockDim.x) {
+      const int32_t b = e < Pn ? pre_all[op.pos_off + e] : e < Pn + nc ? op.chain[e - Pn] : op.pinned[e - Pn - nc];
+      if (b < 0 || b >= P.cap) continue;
+      F.hit_op[b] = kNoOp;
+      F.hit_max[b] = -1;
+      F.dref[b] = 0;
+      F.ev_max[b] = -1;
+      F.nrel[b] = 0;
+      F.nunp[b] = 0;
+      F.flags[b] = 0;
+    }
   }
-}
-
-// ---- 9. results, chains, counters
-__global__ void __launch_bounds__(256) k_fast_finish(Pool P, Scratch S, const ProgOp* __restrict__ ops, ProgRes* res,
-                                                     int n_ops, int64_t* out, FastBuf F) {
-  if (!F.ctl[FC_DONE]) return;
-  const int o = blockIdx.x;
-  const ProgOp op = ops[o];
-  const int64_t Pn = op_positions(P, op);
+  if (!F.ctl[FC_DONE]) return;  // uniform
+  __syncthreads();  // this op's chain entries were read above
   if (op.kind == PK_COMPLETE)
     for (int64_t p = threadIdx.x; p < Pn; p += blockDim.x) op.chain[p] = op.ids[p];
   if (threadIdx.x == 0) {

@@ -55,6 +55,8 @@ void pool_lookup(sb_kv_cache* c, const ProgOp* h_ops, int64_t n, int64_t now, in
 
 // The pool's own stream (per-op C-ABI calls run there).
 cudaStream_t pool_stream(sb_kv_cache* c);
+// Kernels the pool's op programs and batched lookups have launched so far.
+uint64_t pool_launches(const sb_kv_cache* c);
 int pool_device(sb_kv_cache* c);
 
 }  // namespace sb
