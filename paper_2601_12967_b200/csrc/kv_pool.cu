@@ -2504,7 +2504,7 @@ struct sb_kv_cache {
     k_fast_blocks<<<no, 256, 0, st>>>(P, d_ops, d_pre_all, pin_cnt, real_tag, now, FB);
     k_fast_plan<<<1, kFastThreads, kPlanSmem, st>>>(P, S, d_ops, static_cast<int>(n_ops), now, FB, prof_buf());
     k_fast_touch<<<g2, 256, 0, st>>>(P, d_ops, d_pre_all, pin_cnt, real_tag, now, FB);
-    k_fast_evict<<<grid_for(std::max<int64_t>(total_pos, 1)), 256, 0, st>>>(P, FB);
+    k_fast_evict<<<grid_for(std::max<int64_t>(total_pos, 1)), 256, 0, st>>>(P, S, FB);
     k_fast_create<<<g2, 256, 0, st>>>(P, d_ops, d_pre_all, now, FB);
     if (pin_cnt && has_pin) {
       if (!d_first_op) {

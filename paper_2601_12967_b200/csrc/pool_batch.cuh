@@ -658,11 +658,15 @@ __global__ void __launch_bounds__(256) k_fast_touch(Pool P, const ProgOp* __rest
 }
 
 // ---- 5. evictions: the index slots of evicted pool blocks become tombstones
-__global__ void k_fast_evict(Pool P, FastBuf F) {
+// Also the evicted ids in eviction order into S.evicted, as the sequential
+// program leaves them (sb_kv_insert reports them: sb_kv_last_evicted, which
+// the drop-in binding's residency mirror consumes).
+__global__ void k_fast_evict(Pool P, Scratch S, FastBuf F) {
   if (!F.ctl[FC_DONE]) return;
-  const int64_t M = F.ctl[FC_M];
+  const int64_t M = F.ctl[FC_M], fu = F.ctl[FC_FREE_USED];
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < M;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (r >= fu) S.evicted[r - fu] = F.miss_id[r];
     if (!(F.mflag[r] & MF_EXISTING)) continue;
     const int32_t v = F.miss_id[r];
     P.idx[P.slot[v]].id = -2;

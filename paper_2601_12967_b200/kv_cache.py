@@ -184,6 +184,15 @@ class KvCache:
         keys = ["lookups", "hit_tokens", "looked_up_tokens", "inserted_blocks", "evicted_blocks", "cache_full"]
         return dict(zip(keys, [int(x) for x in out]))
 
+    def last_evicted(self) -> list:
+        """Block ids the last insert / evict evicted, in eviction order (sb_kv_last_evicted)."""
+        n = C.c_int64(0)
+        _lib.check(self._L.sb_kv_last_evicted(self._h, None, 0, C.byref(n)), "last_evicted")
+        out = np.zeros(max(n.value, 1), dtype=np.int32)
+        _lib.check(self._L.sb_kv_last_evicted(self._h, out.ctypes.data_as(_lib.I32P), n.value, C.byref(n)),
+                   "last_evicted")
+        return out[: n.value].tolist()
+
     def program_stats(self) -> dict:
         """Op programs run on this pool and how many the parallel path applied."""
         out = (C.c_uint64 * 2)()

@@ -175,6 +175,37 @@ def insert_batches():
     return out_all, stats
 
 
+def single_inserts():
+    """Per-call KvCache.insert (one PK_INSERT op per program) under pressure,
+    with releases in between: status, ids and the evicted ids the call
+    reports (sb_kv_last_evicted — the drop-in binding's residency mirror
+    consumes them)."""
+    from paper_2601_12967_b200.kv_cache import CacheConfig, KvCache
+
+    out_all = []
+    for seed in range(3):
+        rng = np.random.default_rng(900 + seed)
+        cache = KvCache(CacheConfig(16, int(rng.integers(40, 200)), int(seed % 2)))
+        bases = [rng.integers(1, 2**62, int(rng.integers(16, 400)), dtype=np.uint64) for _ in range(3)]
+        held, out = [], []
+        for k in range(60):
+            b = bases[int(rng.integers(0, len(bases)))]
+            t = np.concatenate([b[: int(rng.integers(1, len(b) + 1))],
+                                rng.integers(1, 2**62, int(rng.integers(0, 200)), dtype=np.uint64)])
+            try:
+                ids = cache.insert(t, [(0, len(t), int(rng.integers(6)))], 5 + k)
+                held.append(ids)
+                rec = [list(map(int, ids)), cache.last_evicted()]
+            except Exception as e:
+                rec = ["E:" + type(e).__name__]
+            if held and rng.random() < 0.6:
+                cache.release(held.pop(int(rng.integers(0, len(held)))))
+            rec.append(digest(cache.dump()))
+            out.append(rec)
+        out_all.append(out)
+    return out_all
+
+
 def percall_sequences():
     """Random interleavings of the per-call engine API (one op per program)."""
     from paper_2601_12967_b200.engine import ContinuationEngine
@@ -234,7 +265,8 @@ def main():
     b, sb = ragged_batches()
     c, sc = percall_sequences()
     d, sd = insert_batches()
-    print(json.dumps({"configs1": a, "ragged": b, "percall": c, "inserts": d,
+    e = single_inserts()
+    print(json.dumps({"configs1": a, "ragged": b, "percall": c, "inserts": d, "single": e,
                       "stats": {"configs1": sa, "ragged": sb, "percall": sc, "inserts": sd}}))
 
 

@@ -41,3 +41,24 @@ def test_paper_scenarios_pass_on_b200_pool():
     for tiered, expect0 in ((0, 0), (1, 512)):
         assert O.b200_lib().refrun_thrashing(tiered, hits.ctypes.data_as(O.I64P)) == 0
         assert hits[0] == expect0
+
+
+@pytest.mark.gpu
+def test_bench_trace_shard_on_b200_pool_is_identical():
+    """The bench's configs[3] generator (trace_gen default workload, seed 1,
+    an 8192-block pool) through the drop-in library the bench uses
+    (integration/_build/libagentsim_b200.so via dropin.py) vs the pure
+    reference simulator: every request's FTR, hits and the eviction total.
+    (Long enough that the binding's residency mirror, fed by
+    sb_kv_last_evicted after every insert, decides admissions.)"""
+    from paper_2601_12967_b200 import dropin as D
+
+    ref_lib = os.path.join(O.REF_DIR, "libagentsim_ref.so")
+    if not os.path.exists(ref_lib):
+        pytest.skip("oracle/_ref not built")
+    for preset in ("sutradhara", "baseline"):
+        ref = D.run_shard(32, 1, preset, 8192, shard=0, n_shards=1, lib_path=ref_lib)
+        got = D.run_shard(32, 1, preset, 8192, shard=0, n_shards=1)
+        assert np.array_equal(ref.ftr_ms, got.ftr_ms), preset
+        assert np.array_equal(ref.hit_tokens, got.hit_tokens), preset
+        assert ref.evictions == got.evictions, (preset, ref.evictions, got.evictions)

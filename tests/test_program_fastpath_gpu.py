@@ -29,7 +29,7 @@ def _run(fast: str) -> dict:
 def test_parallel_program_path_equals_sequential():
     seq = _run("0")
     par = _run("1")
-    for k in ("configs1", "ragged", "percall", "inserts"):
+    for k in ("configs1", "ragged", "percall", "inserts", "single"):
         assert len(seq[k]) == len(par[k])
         for i, (a, b) in enumerate(zip(seq[k], par[k])):
             assert a == b, (k, i)
