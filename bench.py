@@ -284,6 +284,8 @@ def run_ours(args, rank, world, local_rank):
     extra = {}
     if not args.no_trace:  # configs[3] sharded over the ranks, [4] points spread over the ranks, [0]
         extra = dropin_metrics(args, rank, world, local_rank, dev)
+        if rank == 0 and not args.no_dense:
+            extra["toy_model"] = run_toy(local_rank)
     roof_pool = None
     if not args.no_pool_roofline and rank == 0:
         roof_pool = pool_rooflines()
@@ -474,6 +476,79 @@ def run_dense(args, rank, world, local_rank):
     }
     del batch, eng, model
     torch.cuda.empty_cache()
+    return out
+
+
+def run_toy(local_rank):
+    """BASELINE configs[0] on the B200 path with a real (toy) model: ONE agentic
+    request, 3 tool iterations, a 2-layer d_model=256 Llama-style decoder
+    (random-init), 16-token KV blocks, LRU vs hint-aware eviction.  Per
+    iteration the tool-independent prefix is admitted (lookup) and its
+    uncached tokens are prefilled through the model, then the tool output is
+    continued over the cached pages (sb_batch_run with the model attached).
+    Between iterations, while the request's tool runs, other calls' tool
+    outputs and responses pass through the same small pool: under LRU they
+    push out the request's older system / user blocks, the hint-aware policy
+    evicts the low-tier blocks first (paper section 4.4, the reference's
+    kv_thrashing scenario at configs[0] scale)."""
+    import torch
+    from paper_2601_12967_b200.engine import TOY_2L_256, ContinuationEngine, DenseModel, DenseShape
+    from paper_2601_12967_b200.kv_cache import LRU, RESPONSE, SYSTEM_PROMPT, TIERED, TOOL_OUTPUT, USER_QUERY
+
+    dev = torch.device("cuda", gpu_of(local_rank))
+    shape = DenseShape(n_layers=2, d_model=256, n_q_heads=2, n_kv_heads=1, d_ff=768, vocab=32000)
+    rng = np.random.default_rng(5)
+    sys_t = rng.integers(1, 32000, 256, dtype=np.uint64)
+    user_t = rng.integers(1, 32000, 256, dtype=np.uint64)
+    tools = [rng.integers(1, 32000, 64, dtype=np.uint64) for _ in range(3)]
+    noise = [[rng.integers(1, 32000, 320, dtype=np.uint64) for _ in range(2)] for _ in range(3)]
+    out = {}
+    for name, pol in (("lru", LRU), ("hint_aware", TIERED)):
+        eng = ContinuationEngine(TOY_2L_256, 64, pol, device=dev.index or 0, seed=0)
+        model = DenseModel(shape, seed=0, device=dev.index or 0)
+        prefix, tags = np.concatenate([sys_t, user_t]), [(0, 256, SYSTEM_PROMPT), (256, 512, USER_QUERY)]
+        its, now = [], 10
+        for i in range(3):
+            now += 1
+            h = eng.submit_partial_prefill(prefix, tags, now)
+            cached = eng.cached_at_submit(h)
+            assert eng.prefill_done(h, now) == eng.PINNED
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            eng.prefill_partials([h], model)  # the uncached prefix, while the tool would run
+            e1.record()
+            batch = eng.make_batch([prefix], [tags], [len(tools[i])])
+            batch.set_model(model)
+            batch.stage_suffix_device(torch.from_numpy(tools[i].view(np.int64)).to(dev))
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record()
+            batch.run(now, seed=i)
+            c1.record()
+            torch.cuda.synchronize()
+            first = int(batch.model_result()[0])
+            its.append({"prefix_tokens": int(len(prefix)), "cached_at_submit": int(cached),
+                        "prefilled_tokens": int(len(prefix) - cached), "prefix_prefill_ms": e0.elapsed_time(e1),
+                        "continuation_ms": c0.elapsed_time(c1), "first_token": first})
+            del batch
+            eng.abandon_partial(h)
+            # the next prompt: this one + the tool output + the response token
+            tags = tags + [(len(prefix), len(prefix) + len(tools[i]), TOOL_OUTPUT),
+                           (len(prefix) + len(tools[i]), len(prefix) + len(tools[i]) + 1, RESPONSE)]
+            prefix = np.concatenate([prefix, tools[i], np.array([first], np.uint64)])
+            for t in noise[i]:  # other calls through the pool while this request's next tool runs
+                now += 1
+                c = eng.submit_call(t, [(0, len(t), TOOL_OUTPUT)], 1, now)
+                eng.prefill_done(c, now)
+                eng.finish_decode(c, np.array([7], np.uint64), now)
+        st = eng.cache.stats()
+        out[name] = {"iterations": its, "evicted_blocks": st["evicted_blocks"],
+                     "prefix_hit_rate": sum(x["cached_at_submit"] for x in its) / sum(x["prefix_tokens"] for x in its)}
+        del eng, model
+        torch.cuda.empty_cache()
+    out["workload"] = ("configs[0]: 1 agentic request, 3 tool iterations, toy 2-layer d_model=256 decoder "
+                       "(random-init bf16), 16-token blocks, a 64-block pool shared with other calls' tool "
+                       "outputs between iterations; LRU vs hint-aware; the model runs every uncached prefix "
+                       "token and every tool-output token")
     return out
 
 
