@@ -56,6 +56,7 @@ constexpr int kSelectThreads = 1024;
 constexpr int kSortSmemKeys = 8192;
 constexpr int kCandSmem = 16384;  // candidate keys staged in shared memory (128 KB)
 constexpr int64_t kCoopMinCap = 16384;  // pools at least this large use the all-SM scorer
+constexpr int64_t kProgCoopMinCap = 65536;  // ... for op programs (see use_coop)
 
 enum Ctr { C_NRES = 0, C_EVICTED, C_LOOKUPS, C_HIT_TOK, C_LOOK_TOK, C_INS_BLOCKS, C_EV_BLOCKS, C_FULL, C_N };
 enum Scal { S_F = 0, S_K, S_FREE, S_NEV, S_STATUS, S_FAILPOS, S_NNEW, S_NCAND, S_ERRIDX, S_NLATE, S_BOUND, S_NMISS, S_NLATEHIT, S_N };
@@ -2364,7 +2365,21 @@ struct sb_kv_cache {
   uint64_t launches = 0;  // kernels the op programs / lookups launched (sb_batch_run reports them)
   std::vector<int32_t> last_evicted;  // ids evicted by the last per-op insert / evict (sb_kv_last_evicted)
 
-  bool use_coop() const { return P.cap >= kCoopMinCap && coop_grid > 0; }
+  // k_score + k_select_coop (all SMs, three launches incl. a cooperative one)
+  // vs the one-CTA k_select (one launch).  Op programs (mode 2) run between
+  // host synchronisations, where launch count is latency, so they keep the
+  // one-CTA select up to kProgCoopMinCap blocks (the configs[1] engine step,
+  // 27K-block pool: 1.61 vs 1.88 ms per step of pool work).
+  bool use_coop(int mode) const {
+    static int64_t min_cap = -1, prog_min_cap = -1;  // SB_COOP_MIN_CAP / SB_PROG_COOP_MIN_CAP override
+    if (min_cap < 0) {
+      const char* e = getenv("SB_COOP_MIN_CAP");
+      min_cap = e ? atoll(e) : kCoopMinCap;
+      const char* f = getenv("SB_PROG_COOP_MIN_CAP");
+      prog_min_cap = f ? atoll(f) : kProgCoopMinCap;
+    }
+    return P.cap >= (mode == 2 ? std::max(min_cap, prog_min_cap) : min_cap) && coop_grid > 0;
+  }
 
   // SB_PROG_PROFILE=1: per-phase cycle counters of the op program, printed
   // to stderr at destruction (phases: 0 setup, 1 hints, 2 re-probe, 3 flags,
@@ -2630,7 +2645,7 @@ struct sb_kv_cache {
   }
 
   void launch_select(const InsertArgs& A, int s, int mode, int64_t needed) {
-    if (!use_coop()) {
+    if (!use_coop(mode)) {
       k_select<<<1, kSelectThreads, select_smem(), stream>>>(P, S, A, s, mode, needed);
       ++launches;
       return;
