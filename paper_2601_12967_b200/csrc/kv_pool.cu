@@ -179,6 +179,59 @@ __global__ void k_chain_hash(const uint64_t* __restrict__ tokens, const int64_t*
   }
 }
 
+// Few sequences (the engine's tool-output and prefix hashes: tens of
+// sequences of thousands of tokens): the kernel time is the dependent chain
+// of the longest sequence, so each lane runs its own sequence with nothing
+// but the fold on its critical path — the next block's 16 tokens are loaded
+// into registers (16 B vector loads) while the current block is folded, no
+// shared-memory staging or warp synchronisation per block.
+__global__ void __launch_bounds__(32) k_chain_hash_lat(const uint64_t* __restrict__ tokens,
+                                                        const int64_t* __restrict__ seq_off,
+                                                        const int64_t* __restrict__ blk_off,
+                                                        const uint64_t* __restrict__ parent0, int n_seqs,
+                                                        int full_only, uint64_t* __restrict__ out, int segs) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_seqs) return;
+  const int64_t b = seq_off[segs ? 2 * s : s], e = seq_off[segs ? 2 * s + 1 : s + 1];
+  uint64_t h = parent0 ? parent0[s] : kRootHash;
+  const int64_t ob = blk_off[s];
+  const int64_t nblk = full_only ? (e - b) / 16 : (e - b + 15) / 16;
+  const int64_t nfull = (e - b) / 16;
+  const bool vec = (reinterpret_cast<uintptr_t>(tokens + b) & 15) == 0;
+  uint64_t cur[16], nxt[16];
+  auto load = [&](int64_t j, uint64_t (&v)[16]) {
+    const uint64_t* p = tokens + b + 16 * j;
+    if (j < nfull && vec) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2*>(p) + r);
+        v[2 * r] = w.x;
+        v[2 * r + 1] = w.y;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        v[r] = b + 16 * j + r < e ? __ldg(reinterpret_cast<const unsigned long long*>(p + r)) : 0ull;
+    }
+  };
+  if (nblk > 0) load(0, cur);
+  for (int64_t j = 0; j < nblk; ++j) {
+    if (j + 1 < nblk) load(j + 1, nxt);
+    const int len = static_cast<int>(min(static_cast<int64_t>(16), e - (b + 16 * j)));
+    if (len == 16) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) h = chain_step(h, cur[r] + kGolden);
+    } else {  // the partial last block (registers, no dynamic indexing)
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if (r < len) h = chain_step(h, cur[r] + kGolden);
+    }
+    out[ob + j] = h;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) cur[r] = nxt[r];
+  }
+}
+
 // 16-token blocks: a warp hashes 32 sequences (one per lane) but loads their
 // tokens cooperatively — each warp load instruction covers the current block
 // of two sequences (16 lanes x 8 B, contiguous), staged through shared memory
@@ -281,6 +334,16 @@ static void launch_chain_hash(const uint64_t* tokens, const int64_t* seq_off, co
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kHashWarps, 0);
       grid_cap = std::max(1, sms * std::max(per_sm, 1));
+    }
+    static int lat_max = -1;  // SB_HASH_LAT_MAX: the per-lane latency kernel up to this many sequences
+    if (lat_max < 0) {
+      const char* e = getenv("SB_HASH_LAT_MAX");
+      lat_max = e ? atoi(e) : 2048;
+    }
+    if (n_seqs <= lat_max) {
+      k_chain_hash_lat<<<(n_seqs + 31) / 32, 32, 0, st>>>(tokens, seq_off, blk_off, parent0, n_seqs, full_only, out,
+                                                         segs);
+      return;
     }
     const int groups = (n_seqs + 31) / 32;
     const int grid = std::min(grid_cap, (groups + kHashWarps - 1) / kHashWarps);
