@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes as C
 import json
+import re
 import os
 import sys
 
@@ -45,6 +46,8 @@ def flush_l2():
     import torch
 
     global _FLUSH, _CLEAN
+    if os.environ.get("SB_FLUSH") == "none":  # diagnostics only: warm L2
+        return
     if _FLUSH is None:
         _FLUSH = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
         _CLEAN = torch.ones(64 << 20, dtype=torch.int32, device="cuda")
@@ -80,9 +83,29 @@ def timed(fn, reps=10, warm=3, kernels=(), flush=False):
                     flush_l2()
                 fn()
             torch.cuda.synchronize()
+        # the device span of one call: first matched kernel's start to the last
+        # one's end (launch gaps between a call's kernels included); calls are
+        # separated by the L2 flush
+        try:
+            evs = sorted((e.time_range.start, e.time_range.end) for e in prof.events()
+                         if e.device_type.name == "CUDA" and any(re.search(r"\b" + k + r"\b", e.name) for k in kernels))
+        except AttributeError:
+            evs = []
+        spans, cur = [], None
+        for a, b in evs:
+            if cur and a - cur[1] < 20:  # us
+                cur[1] = max(cur[1], b)
+            else:
+                if cur:
+                    spans.append(cur[1] - cur[0])
+                cur = [a, b]
+        if cur:
+            spans.append(cur[1] - cur[0])
+        if spans:
+            dev["span"] = [float(np.median(spans)) * 1e-6, 1]
         for e in prof.key_averages():
             for k in kernels:
-                if k in e.key and e.count:
+                if re.search(r"\b" + k + r"\b", e.key) and e.count:  # k_select must not match k_select_coop
                     d = dev.setdefault(k, [0.0, 0])
                     d[0] += e.device_time_total * 1e-6
                     d[1] += e.count
@@ -144,13 +167,19 @@ def evict_bench(L, cache, cap, hbm):
             k = C.c_int64(0)
             L.sb_kv_evict(cache.handle, needed, out.ctypes.data_as(_lib.I32P), C.byref(k))
         res = cache.resident_blocks()
-        api, kt = timed(ev, reps=5, warm=1, kernels=("k_plan", "k_score", "k_select_coop"), flush=True)
+        names = ("k_plan", "k_score", "k_select_coop", "k_evict_fused", "k_select")
+        api, kt = timed(ev, reps=5, warm=1, kernels=names, flush=True)
         cfg = f"pool {cap} blocks, ~{res} resident (all candidates), evict {needed}"
         # scoring: 24 B of metadata read per pool block (ntok/ref/pinned/tag + last) + one 8 B key per candidate
-        emit("k_score (hint-aware eviction scoring)", cfg, cap * 24 + res * 8, api, kt.get("k_score"), hbm)
-        tot = sum(kt.get(k, 0.0) for k in ("k_plan", "k_score", "k_select_coop"))
-        emit("evict total (k_plan + k_score + k_select_coop)", cfg, cap * 24 + res * 8, api, tot or None, hbm,
-             parts={k: kt.get(k) for k in ("k_plan", "k_score", "k_select_coop")})
+        if kt.get("k_score"):
+            emit("k_score (hint-aware eviction scoring)", cfg, cap * 24 + res * 8, api, kt.get("k_score"), hbm)
+        # evict total = the device span of one evict (first kernel start to last
+        # kernel end, launch gaps included); parts = per-kernel durations
+        tot = kt.get("span") or sum(kt.get(k, 0.0) for k in names)
+        label = ("evict total (k_evict_fused: scoring + select, one cooperative launch)" if kt.get("k_evict_fused")
+                 else "evict total (k_plan + k_score + k_select_coop)")
+        emit(label, cfg, cap * 24 + res * 8, api, tot or None, hbm, parts={k: kt.get(k) for k in names},
+             note="device span of the evict's kernels incl. launch gaps" if kt.get("span") else None)
 
 
 def main(only=None):
@@ -178,10 +207,12 @@ def main(only=None):
         seq_off = torch.arange(0, n + 1, toks, dtype=torch.int64, device=dev)
         blk_off = torch.arange(0, n // 16 + 1, toks // 16, dtype=torch.int64, device=dev)
         out = torch.empty(n // 16, dtype=torch.int64, device=dev)
+        names = ("k_chain_hash16", "k_chain_hash_lat")  # the latency kernel takes <= 2048 sequences
         api, kt = timed(lambda: L.sb_chain_hash_batch(p(tokens), p(seq_off), p(blk_off), None, n_seqs, 16, p(out), st),
-                         kernels=("k_chain_hash16",), flush=True)
-        emit("k_chain_hash16", f"{n_seqs} seqs x {toks} tokens", 8 * n + 8 * (n // 16), api,
-             kt.get("k_chain_hash16"), hbm,
+                         kernels=names, flush=True)
+        kn = next((k for k in names if kt.get(k)), names[0])
+        emit(kn, f"{n_seqs} seqs x {toks} tokens", 8 * n + 8 * (n // 16), api,
+             kt.get(kn), hbm,
              note="one dependent 64-bit splitmix chain per sequence (~90 clk per token): fewer sequences than "
                   "resident lanes are latency bound, many sequences ALU-pipe bound" if n_seqs < 65536 else None)
         del tokens
@@ -234,12 +265,14 @@ def probe_bench(L, dev, st, hbm, cap, n_seqs, toks, evict):
     _lib.check(L.sb_kv_release_batch(cache.handle, p(ids), n // 16, None, st))
     torch.cuda.synchronize()
     hits = torch.empty(n_seqs, dtype=torch.int64, device=dev)
+    names = ("k_probe_rows3", "k_probe_rows2", "k_probe_rows")  # SB_PROBE_PER selects the variant
     api, kt = timed(lambda: L.sb_kv_lookup_prefix_batch(cache.handle, p(tokens), p(seq_off), p(blk_off),
                                                          blk_off_h.ctypes.data_as(_lib.I64P), p(hashes), n_seqs, 2,
-                                                         p(hits), st), kernels=("k_probe_rows",), flush=True)
+                                                         p(hits), st), kernels=names, flush=True)
     assert int(hits.sum()) == n
-    emit("k_probe_rows", f"{n_seqs} seqs x {toks} tokens, pool {cap} blocks, all hit",
-         (n // 16) * (128 + 128 + 24 + 8), api, kt.get("k_probe_rows"), hbm)
+    kn = next((k for k in names if kt.get(k)), names[0])
+    emit(kn, f"{n_seqs} seqs x {toks} tokens, pool {cap} blocks, all hit",
+         (n // 16) * (128 + 128 + 24 + 8), api, kt.get(kn), hbm)
 
     if evict:
         evict_bench(L, cache, cap, hbm)

@@ -1184,7 +1184,25 @@ struct CoopBuf {
   int64_t slice;             // blocks per score slice (multiple of 4)
   int keys_in_smem;          // k_select_coop stages its slices' keys in shared memory (else reads them in place)
   int64_t sort_keys;         // keys k_select_coop's dynamic shared memory holds (its final sort)
+  unsigned long long* tprof; // SB_SELECT_PROF=1: phase timestamps (%globaltimer) of the last evict, else null
 };
+// SB_SELECT_PROF slots: 0/1 k_plan start/end, 2/3 k_score first/last CTA entry, 4 k_score last exit,
+// 5/6 k_select_coop first/last entry, 7 CTA 0 after the prologue, 8+2p / 9+2p last arrival at / CTA 0
+// leaving grid barrier p (p < 6), 20 CTA 0 sort start, 21 CTA 0 end
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tp_set(const CoopBuf& G, int slot) {
+  if (G.tprof && threadIdx.x == 0) G.tprof[slot] = gtimer();
+}
+__device__ __forceinline__ void tp_max(const CoopBuf& G, int slot) {
+  if (G.tprof && threadIdx.x == 0) atomicMax(G.tprof + slot, gtimer());
+}
+__device__ __forceinline__ void tp_min(const CoopBuf& G, int slot) {
+  if (G.tprof && threadIdx.x == 0) atomicMin(G.tprof + slot, gtimer());
+}
 constexpr int kScoreThreads = 512;
 constexpr int kSlicesPerSm = 2;  // score slices per SM; k_score CTA c scans slices c and c + n_sm
 // k_score streams the metadata through shared memory with 1-D bulk copies
@@ -1200,6 +1218,8 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
     k_plan(Pool P, Scratch S, InsertArgs A, int s, int mode, CoopBuf G) {
   __shared__ int64_t first;
   const int t = threadIdx.x;
+  if (G.tprof && t < 32) G.tprof[t] = (t == 2 || t == 5) ? ~0ull : 0ull;
+  tp_set(G, 0);
   for (int i = t; i < 6 * 2048; i += blockDim.x) G.hist[i] = 0;
   if (t < 3) G.ctr[t] = 0;
   if (t == 3) G.ctr[3] = ~0ull;
@@ -1209,6 +1229,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
       S.scal[S_F] = 0;
       S.scal[S_STATUS] = 0;
     }
+    tp_set(G, 1);
     return;
   }
   const int64_t b0 = A.blk_off[s];
@@ -1258,9 +1279,14 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
 // score a landed chunk from shared memory and append the candidates' keys
 // to the slice's own region of the key list (one shared atomic per warp and
 // element slot).  The metadata of a pool block is read from HBM exactly once.
-__global__ void __launch_bounds__(kScoreThreads, 1) k_score(Pool P, Scratch S, CoopBuf G) {
-  extern __shared__ __align__(128) uint8_t stage_mem[];
+// The scoring pass over kScoreThreads threads (the fused kernel's other
+// threads skip it).
+__device__ __forceinline__ void score_body(const Pool& P, const CoopBuf& G, uint8_t* stage_mem) {
   __shared__ uint64_t full[kScoreStages];
+  // named barrier over the kScoreThreads scoring threads: the fused kernel's
+  // other warps go straight to its grid barrier instead of polling the ring
+  auto score_sync = []() { asm volatile("bar.sync 1, %0;" ::"n"(kScoreThreads) : "memory"); };
+  if (threadIdx.x >= kScoreThreads) return;
   __shared__ unsigned int n_c, n_free;
   __shared__ unsigned long long kmin, kmax;
   const int t = threadIdx.x;
@@ -1274,6 +1300,8 @@ __global__ void __launch_bounds__(kScoreThreads, 1) k_score(Pool P, Scratch S, C
     n = s_hi - lo < 0 ? 0 : (s_hi - lo < kScoreChunk ? s_hi - lo : int64_t(kScoreChunk));
   };
   const int64_t n_chunks = n_my * chunks_per_slice;
+  tp_min(G, 2);
+  tp_max(G, 3);
   auto issue = [&](int64_t c) {
     int64_t lo, n;
     range(c, lo, n);
@@ -1300,7 +1328,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) k_score(Pool P, Scratch S, C
     kmin = ~0ull;
     kmax = 0;
   }
-  __syncthreads();
+  score_sync();
   if (t == 0)
     for (int64_t c = 0; c < n_chunks && c < kScoreStages; ++c) issue(c);
   const bool tiered = P.policy == SB_POLICY_TIERED;
@@ -1355,7 +1383,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) k_score(Pool P, Scratch S, C
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (cm >> u & 1) out[base++] = key[u];
-    __syncthreads();  // stage consumed by every thread
+    score_sync();  // stage consumed by every thread
     if (t == 0 && c + kScoreStages < n_chunks) {
       fence_proxy_async();
       issue(c + kScoreStages);
@@ -1372,7 +1400,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1) k_score(Pool P, Scratch S, C
         atomicMin(&kmin, mn);
         atomicMax(&kmax, mx);
       }
-      __syncthreads();
+      score_sync();
       if (t == 0) {
         G.fcnt[sl] = n_free;
         G.ncnt[sl] = n_c;
@@ -1383,23 +1411,37 @@ __global__ void __launch_bounds__(kScoreThreads, 1) k_score(Pool P, Scratch S, C
         kmin = ~0ull;
         kmax = 0;
       }
-      __syncthreads();
+      score_sync();
       mn = ~0ull;
       mx = 0;
       nf = 0;
     }
   }
+  tp_max(G, 4);
 }
 
-__global__ void __launch_bounds__(kSelectThreads, 1)
-    k_select_coop(Pool P, Scratch S, InsertArgs A, int s, int mode, int64_t needed, CoopBuf G) {
+__global__ void __launch_bounds__(kScoreThreads, 1) k_score(Pool P, Scratch S, CoopBuf G) {
+  extern __shared__ __align__(128) uint8_t stage_mem[];
+  score_body(P, G, stage_mem);
+}
+
+__device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, const InsertArgs& A, int s, int mode,
+                                            int64_t needed, const CoopBuf& G, uint64_t* local_keys) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t warp_sums[33];
   __shared__ int64_t sh[8];
   __shared__ uint32_t cnt_b;
-  extern __shared__ uint64_t local_keys[];
+  tp_min(G, 5);
+  tp_max(G, 6);
+  int n_sync = 0;
+  auto gsync = [&]() {
+    if (n_sync < 6) tp_max(G, 8 + 2 * n_sync);
+    grid.sync();
+    if (blockIdx.x == 0 && n_sync < 6) tp_set(G, 9 + 2 * n_sync);
+    ++n_sync;
+  };
   if (S.scal[S_STATUS] != 0) return;  // uniform across the grid
   __shared__ unsigned long long red[3];
   const int t = threadIdx.x;
@@ -1435,6 +1477,7 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
   __syncthreads();
   const int64_t ncand = static_cast<int64_t>(red[0]);
   const uint64_t key_lo = red[1], key_hi = red[2];
+  if (cta == 0) tp_set(G, 7);
   if (cta == 0 && mode == 0) {  // drop the exclusion marks (k_score has read them)
     const int64_t f = S.scal[S_F], b0 = A.blk_off[s];
     for (int64_t p = t; p < f; p += blockDim.x) P.pinned[S.prehit[b0 + p]] &= ~2;
@@ -1504,7 +1547,20 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
     for (int sl = cta; sl < G.n_slices; sl += n_cta) {
       const int64_t c = G.ncnt[sl];
       const uint64_t* src = G.keys + sl * G.slice;
-      for (int64_t i = t; i < c; i += blockDim.x) local_keys[nl + i] = src[i];
+      constexpr int kSU = 8;  // all loads of a thread's share issued before the stores
+      for (int64_t i0 = t; i0 < c; i0 += kSU * static_cast<int64_t>(blockDim.x)) {
+        uint64_t v[kSU];
+#pragma unroll
+        for (int u = 0; u < kSU; ++u) {
+          const int64_t i = i0 + static_cast<int64_t>(u) * blockDim.x;
+          v[u] = i < c ? __ldcg(src + i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kSU; ++u) {
+          const int64_t i = i0 + static_cast<int64_t>(u) * blockDim.x;
+          if (i < c) local_keys[nl + i] = v[u];
+        }
+      }
       nl += c;
     }
   }
@@ -1522,23 +1578,27 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
     } else if (G.keys_in_smem) {
       for (int64_t i = t; i < nl; i += blockDim.x) f(local_keys[i]);
     } else {
-      // in place (L2/HBM): eight loads in flight per thread before the
-      // keys are consumed, so a pass streams instead of waiting one load
-      // latency per key
-      constexpr int kU = 8;
+      // in place (L2/HBM): key pairs as 16 B loads, four in flight per
+      // thread before the keys are consumed, so a pass streams instead of
+      // waiting one load latency per key (a slice's keys start 32 B aligned)
+      constexpr int kU = 4;
       for (int sl = cta; sl < G.n_slices; sl += n_cta) {
         const int64_t c = G.ncnt[sl];
         const uint64_t* src = G.keys + sl * G.slice;
-        for (int64_t i0 = t; i0 < c; i0 += kU * static_cast<int64_t>(blockDim.x)) {
-          uint64_t v[kU];
+        const ulonglong2* src2 = reinterpret_cast<const ulonglong2*>(src);
+        for (int64_t p0 = t; 2 * p0 < c; p0 += kU * static_cast<int64_t>(blockDim.x)) {
+          ulonglong2 v[kU];
 #pragma unroll
           for (int u = 0; u < kU; ++u) {
-            const int64_t i = i0 + static_cast<int64_t>(u) * blockDim.x;
-            v[u] = i < c ? __ldcg(src + i) : 0;
+            const int64_t p = p0 + static_cast<int64_t>(u) * blockDim.x;
+            v[u] = 2 * p + 1 < c ? __ldcg(src2 + p) : make_ulonglong2(2 * p < c ? __ldcg(src + 2 * p) : 0ull, 0ull);
           }
 #pragma unroll
-          for (int u = 0; u < kU; ++u)
-            if (i0 + static_cast<int64_t>(u) * blockDim.x < c) f(v[u]);
+          for (int u = 0; u < kU; ++u) {
+            const int64_t p = p0 + static_cast<int64_t>(u) * blockDim.x;
+            if (2 * p < c) f(v[u].x);
+            if (2 * p + 1 < c) f(v[u].y);
+          }
         }
       }
     }
@@ -1559,13 +1619,27 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
       hist[2 * t + 1] = 0;
       __syncthreads();
       for_keys([&](uint64_t k) {
-        if ((k & mask) == prefix) atomicAdd(&hist[(k >> sh_) & bmask], 1u);
+        // keys of a warp usually share the bin (consecutive ids of one slice):
+        // one shared atomic for the warp instead of 32 on one address
+        const bool in = (k & mask) == prefix;
+        const unsigned b = static_cast<unsigned>((k >> sh_) & bmask);
+        const unsigned am = __activemask();
+        const int leader = __ffs(am) - 1;
+        const unsigned b_lead = __shfl_sync(am, b, leader);
+        if (__all_sync(am, in && b == b_lead)) {
+          if ((threadIdx.x & 31) == leader) atomicAdd(&hist[b_lead], static_cast<unsigned>(__popc(am)));
+        } else if (in) {
+          atomicAdd(&hist[b], 1u);
+        }
       });
       __syncthreads();
+      if (pass < 2) tp_max(G, 22 + pass);
+      if (pass < 2 && cta == 0) tp_set(G, 26 + pass);
+      if (pass == 0 && G.tprof && t == 0) G.tprof[32 + cta] = gtimer();  // per-CTA pass-0 finish
       uint32_t* gh = G.hist + pass * 2048;
       if (hist[2 * t]) atomicAdd(&gh[2 * t], hist[2 * t]);
       if (hist[2 * t + 1]) atomicAdd(&gh[2 * t + 1], hist[2 * t + 1]);
-      grid.sync();
+      gsync();
       hist[2 * t] = gh[2 * t];
       hist[2 * t + 1] = gh[2 * t + 1];
       __syncthreads();
@@ -1606,7 +1680,10 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
           append(km < prefix, k, &G.ctr[1], S.sortbuf);  // lower bins: selected
           append(km == prefix, k, &G.ctr[5], S.keys);    // the chosen bin
         });
-        grid.sync();
+        tp_max(G, 24);
+        if (cta == 0) tp_set(G, 28);
+        if (G.tprof && t == 0) G.tprof[32 + 160 + cta] = gtimer();  // per-CTA compaction finish
+        gsync();
         n_bin = static_cast<int64_t>(*reinterpret_cast<volatile unsigned long long*>(&G.ctr[5]));
         compacted = true;
       }
@@ -1628,8 +1705,39 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
       if (sel) S.sortbuf[base + __popc(b & ((1u << lane) - 1u))] = k;
     });
   }
-  grid.sync();
+  tp_max(G, 25);
+  gsync();
+  if (K > 0 && K <= G.sort_keys) {
+    // every CTA: the K selected keys into shared memory; CTA c ranks its
+    // share of them (rank = selected keys below it; keys are unique), one
+    // warp per key, lanes splitting the comparisons
+    tp_set(G, 20);
+    for (int64_t i = t; i < K; i += blockDim.x) local_keys[i] = __ldcg(S.sortbuf + i);
+    __syncthreads();
+    const int64_t per = (K + n_cta - 1) / n_cta, r_lo = cta * per, r_hi = min(K, r_lo + per);
+    const int lane = t & 31, nw = blockDim.x >> 5;
+    for (int64_t i = r_lo + (t >> 5); i < r_hi; i += nw) {
+      const uint64_t k = local_keys[i];
+      unsigned c = 0;
+      for (int64_t j = lane; j < K; j += 32) c += local_keys[j] < k;
+      c = __reduce_add_sync(0xffffffffu, c);
+      if (lane == 0) {
+        S.victims[c] = k;
+        S.taken[c] = 0;
+        S.rank_of[k & P.idmask] = static_cast<int32_t>(c);
+      }
+    }
+    if (cta == 0 && t == 0) {
+      S.scal[S_K] = K;
+      S.scal[S_FREE] = Fp;
+      S.scal[S_STATUS] = 0;
+      S.scal[S_NCAND] = ncand;
+    }
+    tp_set(G, 21);
+    return;
+  }
   if (cta != 0) return;
+  tp_set(G, 20);
   // ---- CTA 0: sort the K selected keys, publish them with their ranks
   if (K > 0) {
     int64_t n2 = 1;
@@ -1663,6 +1771,40 @@ __global__ void __launch_bounds__(kSelectThreads, 1)
     S.scal[S_STATUS] = 0;
     S.scal[S_NCAND] = ncand;
   }
+  tp_set(G, 21);
+}
+
+__global__ void __launch_bounds__(kSelectThreads, 1)
+    k_select_coop(Pool P, Scratch S, InsertArgs A, int s, int mode, int64_t needed, CoopBuf G) {
+  extern __shared__ __align__(128) uint64_t local_keys[];
+  select_body(P, S, A, s, mode, needed, G, local_keys);
+}
+
+// k_score + k_select_coop as ONE cooperative kernel (one CTA per SM): the
+// select reuses the scoring ring's shared memory, and the score -> select
+// hand-off is a grid barrier instead of a kernel boundary (a launch gap of
+// ~4 us and the select's ramp).  Modes 1 / 2 also take over k_plan's reset
+// of the histograms and counters, so evict() is one launch.
+__global__ void __launch_bounds__(kSelectThreads, 1)
+    k_evict_fused(Pool P, Scratch S, InsertArgs A, int s, int mode, int64_t needed, CoopBuf G) {
+  extern __shared__ __align__(128) uint8_t dyn_smem[];
+  if (mode != 0 && blockIdx.x == 0) {  // k_plan's work for modes 1 / 2 (read only after the grid barrier)
+    const int t = threadIdx.x;
+    if (G.tprof && t < 32) G.tprof[t] = (t == 2 || t == 5) ? ~0ull : 0ull;
+    __syncthreads();
+    tp_set(G, 0);
+    for (int i = t; i < 6 * 2048; i += blockDim.x) G.hist[i] = 0;
+    if (t < 3) G.ctr[t] = 0;
+    if (t == 3) G.ctr[3] = ~0ull;
+    if (t == 4 || t == 5) G.ctr[t] = 0;
+    if (t == 0) {
+      S.scal[S_F] = 0;
+      S.scal[S_STATUS] = 0;
+    }
+  }
+  score_body(P, G, dyn_smem);
+  cooperative_groups::this_grid().sync();
+  select_body(P, S, A, s, mode, needed, G, reinterpret_cast<uint64_t*>(dyn_smem));
 }
 
 constexpr int kWalkSmemVictims = 4096;
@@ -2407,6 +2549,15 @@ struct sb_kv_cache {
   CoopBuf G{};
   int coop_grid = 0;
   size_t coop_smem = 0;
+  size_t fused_smem = 0;  // k_evict_fused's dynamic shared memory (0: not launchable, three kernels instead)
+  static bool fused_enabled() {  // SB_EVICT_FUSED=0 selects k_plan + k_score + k_select_coop
+    static int on = -1;
+    if (on < 0) {
+      const char* e = getenv("SB_EVICT_FUSED");
+      on = e ? atoi(e) != 0 : 1;
+    }
+    return on;
+  }
 
   // op program (pool_program.cuh)
   ProgOp* d_ops = nullptr;
@@ -2713,9 +2864,6 @@ struct sb_kv_cache {
       ++launches;
       return;
     }
-    launches += 3;
-    k_plan<<<1, kSelectThreads, 0, stream>>>(P, S, A, s, mode, G);
-    k_score<<<coop_grid, kScoreThreads, kScoreSmem, stream>>>(P, S, G);
     Pool p_ = P;
     Scratch s_ = S;
     InsertArgs a_ = A;
@@ -2723,8 +2871,43 @@ struct sb_kv_cache {
     int64_t nv = needed;
     CoopBuf g_ = G;
     void* args[] = {&p_, &s_, &a_, &sv, &mv, &nv, &g_};
-    SB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_select_coop), dim3(coop_grid), dim3(kSelectThreads),
-                                        args, coop_smem, stream));
+    if (fused_smem > 0 && fused_enabled()) {
+      if (mode == 0) {
+        k_plan<<<1, kSelectThreads, 0, stream>>>(P, S, A, s, mode, G);
+        ++launches;
+      }
+      ++launches;
+      SB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_evict_fused), dim3(coop_grid),
+                                          dim3(kSelectThreads), args, fused_smem, stream));
+    } else {
+      launches += 3;
+      k_plan<<<1, kSelectThreads, 0, stream>>>(P, S, A, s, mode, G);
+      k_score<<<coop_grid, kScoreThreads, kScoreSmem, stream>>>(P, S, G);
+      SB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_select_coop), dim3(coop_grid),
+                                          dim3(kSelectThreads), args, coop_smem, stream));
+    }
+    if (G.tprof) {  // SB_SELECT_PROF=1: phase times of this evict, relative to k_plan's start (us)
+      unsigned long long h[32] = {};
+      SB_CUDA(cudaStreamSynchronize(stream));
+      SB_CUDA(cudaMemcpy(h, G.tprof, sizeof(h), cudaMemcpyDeviceToHost));
+      auto us = [&](int i) { return h[i] ? (static_cast<double>(h[i]) - static_cast<double>(h[0])) * 1e-3 : -1.0; };
+      fprintf(stderr, "SB_SELECT_PROF mode %d plan_end %.2f score_entry %.2f..%.2f score_exit %.2f select_entry %.2f..%.2f "
+              "prologue %.2f", mode, us(1), us(2), us(3), us(4), us(5), us(6), us(7));
+      for (int p = 0; p < 6; ++p)
+        if (h[8 + 2 * p]) fprintf(stderr, " sync%d %.2f->%.2f", p, us(8 + 2 * p), us(9 + 2 * p));
+      fprintf(stderr, " sort %.2f end %.2f | hist0 %.2f hist1 %.2f compact %.2f gather %.2f | cta0 %.2f %.2f %.2f\n",
+              us(20), us(21), us(22), us(23), us(24), us(25), us(26), us(27), us(28));
+      {
+        unsigned long long hc[2 * 160] = {};
+        SB_CUDA(cudaMemcpy(hc, G.tprof + 32, sizeof(hc), cudaMemcpyDeviceToHost));
+        for (int w = 0; w < 2; ++w) {
+          fprintf(stderr, "SB_SELECT_PROF_CTA %s:", w ? "compact" : "pass0");
+          for (int c = 0; c < coop_grid; ++c)
+            fprintf(stderr, " %.1f", hc[w * 160 + c] ? (static_cast<double>(hc[w * 160 + c]) - static_cast<double>(h[0])) * 1e-3 : -1.0);
+          fprintf(stderr, "\n");
+        }
+      }
+    }
   }
 
   void ensure_batch(int64_t n) {
@@ -2741,7 +2924,7 @@ struct sb_kv_cache {
     // S.prehit aliases d_prehit_all: freed once below
     void* ptrs[] = {P.tok, P.ntok, P.chain, P.parent, P.tag, P.ref, P.pinned, P.last, P.idx, P.slot, P.ctr,
                     S.hashes, S.chain_out, S.kind, S.freel, S.evicted, S.victims, S.taken, S.rank_of, S.keys,
-                    S.sortbuf, S.scal, S.late, d_ops, d_res, d_runk, d_pout, d_pre_all, d_created, d_first_op, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first, G.hist, G.ctr, G.keys, G.fcnt, G.ncnt, G.kmin, G.kmax};
+                    S.sortbuf, S.scal, S.late, d_ops, d_res, d_runk, d_pout, d_pre_all, d_created, d_first_op, d_tok, d_tags, d_meta, d_ids, d_status, d_first, d_hit, d_hash_all, d_prehit_all, d_batch_blk, d_batch_first, G.hist, G.ctr, G.keys, G.fcnt, G.ncnt, G.kmin, G.kmax, G.tprof};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     void* fptrs[] = {FB.hit_op, FB.hit_max, FB.dref, FB.ev_max, FB.nrel, FB.nunp, FB.flags, FB.miss_cnt, FB.miss_base,
@@ -3072,6 +3255,18 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
                                        static_cast<int>(c->coop_smem)));
           SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_coop, kSelectThreads, c->coop_smem));
           if (per_sm >= 1) c->coop_grid = n_sm;
+          {  // the fused kernel: the scoring ring and the select's buffers share its dynamic shared memory
+            cudaFuncAttributes ff{};
+            SB_CUDA(cudaFuncGetAttributes(&ff, k_evict_fused));
+            const size_t fs = std::max(kScoreSmem, c->coop_smem);
+            int per_sm_f = 0;
+            if (ff.sharedSizeBytes + fs <= static_cast<size_t>(smem_optin)) {
+              SB_CUDA(cudaFuncSetAttribute(k_evict_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(fs)));
+              SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_f, k_evict_fused, kSelectThreads, fs));
+            }
+            if (per_sm_f >= 1 && per_sm >= 1) c->fused_smem = fs;
+          }
           c->G.hist = dalloc<uint32_t>(6 * 2048);
           c->G.ctr = dalloc<unsigned long long>(8);
           c->G.n_slices = n_slices;
@@ -3081,6 +3276,8 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
           c->G.ncnt = dalloc<uint32_t>(n_slices);
           c->G.kmin = dalloc<uint64_t>(n_slices);
           c->G.kmax = dalloc<uint64_t>(n_slices);
+          const char* tp = getenv("SB_SELECT_PROF");
+          if (tp && atoi(tp)) c->G.tprof = dalloc<unsigned long long>(32 + 2 * 160);
         }
       }
       SB_CHECK_LAUNCH();
