@@ -171,7 +171,7 @@ def reduce_over_ranks(values, device=None):
         device = None  # the CPU test backend reduces host tensors
     v = torch.tensor(values, dtype=torch.float64, device=device)
     mx, sm = v.clone(), v.clone()
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
     return mx.cpu().tolist(), sm.cpu().tolist()
@@ -572,8 +572,9 @@ def gather_rows(rows: np.ndarray, world: int, dev=None) -> np.ndarray:
     import torch
     import torch.distributed as dist
 
-    if world <= 1 or not (dist.is_available() and dist.is_initialized()):
+    if not (dist.is_available() and dist.is_initialized()):
         return rows
+    world = dist.get_world_size()
     gloo = dist.get_backend() == "gloo"
     n = torch.tensor([rows.shape[0]], dtype=torch.int64, device=None if gloo else dev)
     ns = [torch.zeros_like(n) for _ in range(world)]

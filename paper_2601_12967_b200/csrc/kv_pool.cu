@@ -1618,20 +1618,14 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
       hist[2 * t] = 0;
       hist[2 * t + 1] = 0;
       __syncthreads();
+      if (pass == 0 && G.tprof && cta == 5 && t == 0) G.tprof[32 + 320 + 32] = gtimer();
+      // (a warp-aggregated add for warps whose keys share a bin measured
+      // slower than these plain shared atomics; the pass is bound by the key
+      // loads, profiles/README.md)
       for_keys([&](uint64_t k) {
-        // keys of a warp usually share the bin (consecutive ids of one slice):
-        // one shared atomic for the warp instead of 32 on one address
-        const bool in = (k & mask) == prefix;
-        const unsigned b = static_cast<unsigned>((k >> sh_) & bmask);
-        const unsigned am = __activemask();
-        const int leader = __ffs(am) - 1;
-        const unsigned b_lead = __shfl_sync(am, b, leader);
-        if (__all_sync(am, in && b == b_lead)) {
-          if ((threadIdx.x & 31) == leader) atomicAdd(&hist[b_lead], static_cast<unsigned>(__popc(am)));
-        } else if (in) {
-          atomicAdd(&hist[b], 1u);
-        }
+        if ((k & mask) == prefix) atomicAdd(&hist[(k >> sh_) & bmask], 1u);
       });
+      if (pass == 0 && G.tprof && cta == 5 && (t & 31) == 0) G.tprof[32 + 320 + (t >> 5)] = gtimer();
       __syncthreads();
       if (pass < 2) tp_max(G, 22 + pass);
       if (pass < 2 && cta == 0) tp_set(G, 26 + pass);
@@ -2898,7 +2892,7 @@ struct sb_kv_cache {
       fprintf(stderr, " sort %.2f end %.2f | hist0 %.2f hist1 %.2f compact %.2f gather %.2f | cta0 %.2f %.2f %.2f\n",
               us(20), us(21), us(22), us(23), us(24), us(25), us(26), us(27), us(28));
       {
-        unsigned long long hc[2 * 160] = {};
+        unsigned long long hc[2 * 160 + 33] = {};
         SB_CUDA(cudaMemcpy(hc, G.tprof + 32, sizeof(hc), cudaMemcpyDeviceToHost));
         for (int w = 0; w < 2; ++w) {
           fprintf(stderr, "SB_SELECT_PROF_CTA %s:", w ? "compact" : "pass0");
@@ -2906,6 +2900,9 @@ struct sb_kv_cache {
             fprintf(stderr, " %.1f", hc[w * 160 + c] ? (static_cast<double>(hc[w * 160 + c]) - static_cast<double>(h[0])) * 1e-3 : -1.0);
           fprintf(stderr, "\n");
         }
+        fprintf(stderr, "SB_SELECT_PROF_WARPS cta5 start %.2f:", hc[320 + 32] ? (double(hc[320 + 32]) - double(h[0])) * 1e-3 : -1.0);
+        for (int w = 0; w < 32; ++w) fprintf(stderr, " %.2f", hc[320 + w] ? (double(hc[320 + w]) - double(h[0])) * 1e-3 : -1.0);
+        fprintf(stderr, "\n");
       }
     }
   }
@@ -3277,7 +3274,7 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
           c->G.kmin = dalloc<uint64_t>(n_slices);
           c->G.kmax = dalloc<uint64_t>(n_slices);
           const char* tp = getenv("SB_SELECT_PROF");
-          if (tp && atoi(tp)) c->G.tprof = dalloc<unsigned long long>(32 + 2 * 160);
+          if (tp && atoi(tp)) c->G.tprof = dalloc<unsigned long long>(32 + 2 * 160 + 33);
         }
       }
       SB_CHECK_LAUNCH();

@@ -168,6 +168,55 @@ def test_batch_apis_match_sequential_oracle():
 
 
 @pytest.mark.gpu
+def test_insert_batch_on_cooperative_pool_under_pressure():
+    """sb_kv_insert_batch op programs on a pool large enough (>= 64K blocks)
+    for their eviction to go through the all-SM cooperative select (mode 2),
+    under pressure: statuses, block ids and the dump equal sequential
+    reference inserts."""
+    import ctypes as C
+
+    import torch
+    from paper_2601_12967_b200 import _lib
+    from paper_2601_12967_b200.kv_cache import CacheConfig, KvCache
+
+    bs, cap = 1, 70000
+    rng = np.random.default_rng(41)
+    o = O.OracleCache(bs, cap, 1)
+    c = KvCache(CacheConfig(bs, cap, 1))
+    dev = torch.device("cuda")
+    p = lambda t: C.c_void_p(t.data_ptr())
+    for rnd in range(3):
+        seqs = [O.materialize(int(rng.integers(4)), int(rng.integers(800, 2000)), 50 * rnd + k) for k in range(20)]
+        tags = [[(0, len(s) // 2, int(rng.integers(6))), (len(s) // 2, len(s), int(rng.integers(6)))] for s in seqs]
+        now = 10 + rnd
+        exp = [o.insert(s, t, now) for s, t in zip(seqs, tags)]
+        tok = torch.from_numpy(np.concatenate(seqs).view(np.int64)).to(dev)
+        off = torch.tensor(np.cumsum([0] + [len(s) for s in seqs]), dtype=torch.int64, device=dev)
+        blk = torch.tensor(np.cumsum([0] + [len(s) for s in seqs]), dtype=torch.int64, device=dev)
+        tag_arr = (_lib.TagRange * (2 * len(seqs)))()
+        for i, t in enumerate(tags):
+            for j, (b0, e0, tg) in enumerate(t):
+                tag_arr[2 * i + j].begin, tag_arr[2 * i + j].end, tag_arr[2 * i + j].tag = b0, e0, tg
+        tag_dev = torch.frombuffer(bytearray(tag_arr), dtype=torch.uint8).to(dev)
+        tag_off = torch.arange(0, 2 * len(seqs) + 1, 2, dtype=torch.int64, device=dev)
+        out_ids = torch.full((int(blk[-1]),), -1, dtype=torch.int32, device=dev)
+        status = torch.zeros(len(seqs), dtype=torch.int32, device=dev)
+        _lib.check(_lib.lib().sb_kv_insert_batch(c.handle, p(tok), p(off), p(tag_dev), p(tag_off), p(blk), None,
+                                                 None, len(seqs), now, p(out_ids), p(status), None))
+        torch.cuda.synchronize()
+        st, ids, b = status.cpu().tolist(), out_ids.cpu().tolist(), blk.cpu().tolist()
+        for i, (est, eids) in enumerate(exp):
+            assert st[i] == est, (rnd, i)
+            if est == 0:
+                assert ids[b[i]:b[i + 1]] == eids, (rnd, i)
+        for i, (est, eids) in enumerate(exp):  # release two of every three inserted chains
+            if est == 0 and i % 3:
+                assert o.release(eids) == 0
+                c.release(eids)
+    assert o.dump() == c.dump()
+
+
+@pytest.mark.gpu
 def test_large_pool_cooperative_scorer():
     """Pools of >= 16384 blocks use the all-SM cooperative scorer
     (k_select_coop): eviction order, insert ids under pressure and the full
@@ -193,6 +242,50 @@ def test_large_pool_cooperative_scorer():
         assert o.insert(t, tags, 100 + k) == c.insert(t, tags, 100 + k)
     assert o.dump() == c.dump()
     assert o.total_evicted() == c.total_evicted()
+
+
+@pytest.mark.gpu
+def test_cooperative_evict_beyond_shared_memory_sort():
+    """evict(K) with K above what the cooperative select ranks in shared
+    memory (16K keys): CTA 0 sorts the winners in global memory instead.
+    Every tier and several timestamps, so the radix passes run over the
+    tier and last_used bits of the keys as well as the ids."""
+    bs, cap = 1, 70000
+    c = product(bs, cap, 1)
+    o = O.OracleCache(bs, cap, 1)
+    rng = np.random.default_rng(33)
+    live = []
+    for k in range(30):
+        t = O.materialize(int(rng.integers(4)), 2200, 300 + k)
+        tags = [(0, 700, int(rng.integers(6))), (700, 2200, int(rng.integers(6)))]
+        now = int(rng.integers(0, 40))
+        a, b = o.insert(t, tags, now), c.insert(t, tags, now)
+        assert a == b, k
+        live.append(a[1])
+    for ids in live[::3]:
+        assert o.release(ids) == c.release(ids) == 0
+    for ids in live[1::3]:
+        assert o.release(ids) == c.release(ids) == 0
+    for needed in (20000, 3, 17000):
+        assert o.evict(needed) == c.evict(needed), needed
+    assert o.dump() == c.dump()
+
+
+@pytest.mark.gpu
+def test_three_kernel_evict_path():
+    """SB_EVICT_FUSED=0 selects k_plan + k_score + k_select_coop instead of
+    the fused cooperative kernel: the same parity tests through that path
+    (a subprocess: the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SB_EVICT_FUSED="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_kvcache_gpu.py", "-k",
+                        "cooperative_scorer or beyond_shared_memory or in_place"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0 and "3 passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
 
 
 @pytest.mark.gpu
