@@ -1182,7 +1182,6 @@ struct CoopBuf {
   uint64_t* kmax;
   int n_slices;
   int64_t slice;             // blocks per score slice (multiple of 4)
-  int keys_in_smem;          // k_select_coop stages its slices' keys in shared memory (else reads them in place)
   int64_t sort_keys;         // keys k_select_coop's dynamic shared memory holds (its final sort)
   unsigned long long* tprof; // SB_SELECT_PROF=1: phase timestamps (%globaltimer) of the last evict, else null
 };
@@ -1205,6 +1204,7 @@ __device__ __forceinline__ void tp_min(const CoopBuf& G, int slot) {
 }
 constexpr int kScoreThreads = 512;
 constexpr int kSlicesPerSm = 2;  // score slices per SM; k_score CTA c scans slices c and c + n_sm
+constexpr int kMaxSlicesPerCta = 4;  // k_select_coop's staging table (kSlicesPerSm, grids of >= n_sm / 2 CTAs)
 // k_score streams the metadata through shared memory with 1-D bulk copies
 // (TMA engine): per stage, kScoreChunk blocks of ntok/ref/pinned/tag (4 B)
 // and last (8 B) = 48 KB; kScoreStages stages in flight per SM.
@@ -1542,27 +1542,42 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
   // ---- radix select of the K smallest candidate keys (keys are unique).
   // The CTA's keys: its score slices' regions of G.keys, staged in shared
   // memory when they fit, else read in place each pass (L2-resident).
-  int64_t nl = 0;
-  if (G.keys_in_smem) {
-    for (int sl = cta; sl < G.n_slices; sl += n_cta) {
-      const int64_t c = G.ncnt[sl];
-      const uint64_t* src = G.keys + sl * G.slice;
-      constexpr int kSU = 8;  // all loads of a thread's share issued before the stores
-      for (int64_t i0 = t; i0 < c; i0 += kSU * static_cast<int64_t>(blockDim.x)) {
-        uint64_t v[kSU];
-#pragma unroll
-        for (int u = 0; u < kSU; ++u) {
-          const int64_t i = i0 + static_cast<int64_t>(u) * blockDim.x;
-          v[u] = i < c ? __ldcg(src + i) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < kSU; ++u) {
-          const int64_t i = i0 + static_cast<int64_t>(u) * blockDim.x;
-          if (i < c) local_keys[nl + i] = v[u];
-        }
-      }
-      nl += c;
+  // Staged when EVERY CTA's keys fit (a grid-uniform decision: the
+  // compaction below is a grid-wide step): one bulk copy per slice into
+  // shared memory, each slice's run padded to an even count (16 B aligned).
+  __shared__ unsigned max_cta_keys;
+  __shared__ uint64_t stage_bar;
+  __shared__ int64_t seg_off[kMaxSlicesPerCta], seg_n[kMaxSlicesPerCta];
+  if (t == 0) max_cta_keys = 0;
+  __syncthreads();
+  for (int c2 = t; c2 < n_cta; c2 += blockDim.x) {
+    unsigned n2 = 0;
+    for (int sl = c2; sl < G.n_slices; sl += n_cta) n2 += (G.ncnt[sl] + 1u) & ~1u;
+    atomicMax(&max_cta_keys, n2);
+  }
+  __syncthreads();
+  const bool staged = static_cast<int64_t>(max_cta_keys) <= G.sort_keys;
+  int nseg = 0;
+  if (staged) {
+    int64_t off = 0;
+    for (int sl = cta; sl < G.n_slices; sl += n_cta, ++nseg) {
+      seg_off[nseg] = off;
+      seg_n[nseg] = G.ncnt[sl];
+      off += (G.ncnt[sl] + 1) & ~int64_t(1);
     }
+    if (t == 0) {
+      mbar_init(&stage_bar, 1);
+      fence_barrier_init();
+      fence_proxy_async();  // earlier generic accesses of this shared memory before the async writes
+      fence_proxy_async_global();  // the keys were stored through the generic proxy
+      mbar_arrive_expect_tx(&stage_bar, static_cast<uint32_t>(off * 8));
+      for (int j = 0, sl = cta; j < nseg; ++j, sl += n_cta)
+        if (seg_n[j] > 0)
+          bulk_g2s(local_keys + seg_off[j], G.keys + sl * G.slice,
+                   static_cast<uint32_t>(((seg_n[j] + 1) & ~int64_t(1)) * 8), &stage_bar);
+    }
+    __syncthreads();
+    mbar_wait_suspend(&stage_bar, 0);
   }
   // Large pools (keys read in place): after the first radix pass the keys of
   // the chosen bin are compacted into S.keys (unused by this path) and the
@@ -1575,8 +1590,11 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
       for (int64_t i = static_cast<int64_t>(cta) * blockDim.x + t; i < n_bin;
            i += static_cast<int64_t>(n_cta) * blockDim.x)
         f(S.keys[i]);
-    } else if (G.keys_in_smem) {
-      for (int64_t i = t; i < nl; i += blockDim.x) f(local_keys[i]);
+    } else if (staged) {
+      for (int j = 0; j < nseg; ++j) {
+        const uint64_t* src = local_keys + seg_off[j];
+        for (int64_t i = t; i < seg_n[j]; i += blockDim.x) f(src[i]);
+      }
     } else {
       // in place (L2/HBM): key pairs as 16 B loads, four in flight per
       // thread before the keys are consumed, so a pass streams instead of
@@ -1657,7 +1675,7 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
       const bool done = static_cast<int64_t>(cnt_b) == need;
       __syncthreads();
       if (done) break;
-      if (!G.keys_in_smem && !compacted && hi_bit > 0) {
+      if (!staged && !compacted && hi_bit > 0) {
         const int lane = t & 31;
         auto append = [&](bool take, uint64_t k, unsigned long long* ctr, uint64_t* dst) {
           const unsigned am = __activemask();
@@ -3242,9 +3260,11 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
         const size_t sort_b = 2 * kSortSmemKeys * sizeof(uint64_t);
         const size_t sort_min = sort_b + fa.sharedSizeBytes <= static_cast<size_t>(smem_optin) ? sort_b
                                                                                                : kSortSmemKeys * sizeof(uint64_t);
-        const size_t staged = std::max<size_t>(static_cast<size_t>(kSlicesPerSm * slice) * sizeof(uint64_t), sort_min);
-        c->G.keys_in_smem = staged + fa.sharedSizeBytes <= static_cast<size_t>(smem_optin);
-        c->coop_smem = c->G.keys_in_smem ? staged : sort_min;
+        // dynamic shared memory: the final ranks / sort, and the CTA's candidate keys when every CTA's fit
+        // (a CTA's full slices plus one pad key each), as much as the part allows
+        const size_t full = static_cast<size_t>(kSlicesPerSm * (slice + 1)) * sizeof(uint64_t);
+        const size_t avail = (static_cast<size_t>(smem_optin) - fa.sharedSizeBytes) & ~size_t(15);
+        c->coop_smem = std::min(avail, std::max(full, sort_min));
         c->G.sort_keys = static_cast<int64_t>(c->coop_smem / sizeof(uint64_t));
         SB_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScoreSmem)));
         {
@@ -3263,6 +3283,7 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
               SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_f, k_evict_fused, kSelectThreads, fs));
             }
             if (per_sm_f >= 1 && per_sm >= 1) c->fused_smem = fs;
+            if (c->fused_smem && sb_kv_cache::fused_enabled()) c->G.sort_keys = static_cast<int64_t>(fs / sizeof(uint64_t));
           }
           c->G.hist = dalloc<uint32_t>(6 * 2048);
           c->G.ctr = dalloc<unsigned long long>(8);
