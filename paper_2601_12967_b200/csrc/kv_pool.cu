@@ -1675,6 +1675,9 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
       const bool done = static_cast<int64_t>(cnt_b) == need;
       __syncthreads();
       if (done) break;
+      // the chosen bin plus the lower bins fit the rank buffer: gather them
+      // all and let the rank step pick the K smallest (no further pass)
+      if ((K - need) + static_cast<int64_t>(cnt_b) <= G.sort_keys) break;
       if (!staged && !compacted && hi_bit > 0) {
         const int lane = t & 31;
         auto append = [&](bool take, uint64_t k, unsigned long long* ctr, uint64_t* dst) {
@@ -1719,21 +1722,23 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
   }
   tp_max(G, 25);
   gsync();
-  if (K > 0 && K <= G.sort_keys) {
-    // every CTA: the K selected keys into shared memory; CTA c ranks its
-    // share of them (rank = selected keys below it; keys are unique), one
-    // warp per key, lanes splitting the comparisons
+  // gathered keys: K, or the K plus the rest of the chosen bin after an early exit
+  const int64_t M = K > 0 ? static_cast<int64_t>(*reinterpret_cast<volatile unsigned long long*>(&G.ctr[1])) : 0;
+  if (K > 0 && M <= G.sort_keys) {
+    // every CTA: the M gathered keys into shared memory; CTA c ranks its
+    // share of them (rank = gathered keys below it; keys are unique), one
+    // warp per key, lanes splitting the comparisons; ranks < K are the victims
     tp_set(G, 20);
-    for (int64_t i = t; i < K; i += blockDim.x) local_keys[i] = __ldcg(S.sortbuf + i);
+    for (int64_t i = t; i < M; i += blockDim.x) local_keys[i] = __ldcg(S.sortbuf + i);
     __syncthreads();
-    const int64_t per = (K + n_cta - 1) / n_cta, r_lo = cta * per, r_hi = min(K, r_lo + per);
+    const int64_t per = (M + n_cta - 1) / n_cta, r_lo = cta * per, r_hi = min(M, r_lo + per);
     const int lane = t & 31, nw = blockDim.x >> 5;
     for (int64_t i = r_lo + (t >> 5); i < r_hi; i += nw) {
       const uint64_t k = local_keys[i];
       unsigned c = 0;
-      for (int64_t j = lane; j < K; j += 32) c += local_keys[j] < k;
+      for (int64_t j = lane; j < M; j += 32) c += local_keys[j] < k;
       c = __reduce_add_sync(0xffffffffu, c);
-      if (lane == 0) {
+      if (lane == 0 && c < K) {
         S.victims[c] = k;
         S.taken[c] = 0;
         S.rank_of[k & P.idmask] = static_cast<int32_t>(c);
