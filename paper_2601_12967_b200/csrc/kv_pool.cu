@@ -335,10 +335,13 @@ static void launch_chain_hash(const uint64_t* tokens, const int64_t* seq_off, co
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kHashWarps, 0);
       grid_cap = std::max(1, sms * std::max(per_sm, 1));
     }
-    static int lat_max = -1;  // SB_HASH_LAT_MAX: the per-lane latency kernel up to this many sequences
+    // the per-lane kernel up to this many sequences (SB_HASH_LAT_MAX); measured
+    // (profiles/run_r02aw.sh): 4096 x 1024 tokens 60 vs 72 us, 65536 x 512
+    // 73 vs 82 us; the staged kernel wins from ~8K warps (262144 sequences)
+    static int lat_max = -1;
     if (lat_max < 0) {
       const char* e = getenv("SB_HASH_LAT_MAX");
-      lat_max = e ? atoi(e) : 2048;
+      lat_max = e ? atoi(e) : 65536;
     }
     if (n_seqs <= lat_max) {
       k_chain_hash_lat<<<(n_seqs + 31) / 32, 32, 0, st>>>(tokens, seq_off, blk_off, parent0, n_seqs, full_only, out,
