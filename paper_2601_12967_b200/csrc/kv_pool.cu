@@ -1559,7 +1559,8 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
     atomicMax(&max_cta_keys, n2);
   }
   __syncthreads();
-  const bool staged = static_cast<int64_t>(max_cta_keys) <= G.sort_keys;
+  const bool staged = static_cast<int64_t>(max_cta_keys) <= G.sort_keys &&
+                      (G.n_slices + n_cta - 1) / n_cta <= kMaxSlicesPerCta;
   int nseg = 0;
   if (staged) {
     int64_t off = 0;
