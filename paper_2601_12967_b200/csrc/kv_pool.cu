@@ -1207,7 +1207,9 @@ __device__ __forceinline__ void tp_min(const CoopBuf& G, int slot) {
 }
 constexpr int kScoreThreads = 512;
 constexpr int kSlicesPerSm = 2;  // score slices per SM; k_score CTA c scans slices c and c + n_sm
-constexpr int kMaxSlicesPerCta = 4;  // k_select_coop's staging table (kSlicesPerSm, grids of >= n_sm / 2 CTAs)
+constexpr int kMaxSlicesPerCta = 4;
+constexpr int kMaxLiveSlices = 1024;
+constexpr int64_t kRankEarlyMax = 6144;  // k_select_coop stops its radix passes at this many candidate winners  // k_select_coop's list of slices a filtered pass visits (>= n_slices)  // k_select_coop's staging table (kSlicesPerSm, grids of >= n_sm / 2 CTAs)
 // k_score streams the metadata through shared memory with 1-D bulk copies
 // (TMA engine): per stage, kScoreChunk blocks of ntok/ref/pinned/tag (4 B)
 // and last (8 B) = 48 KB; kScoreStages stages in flight per SM.
@@ -1589,6 +1591,29 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
   // the final gather touch only the bin instead of every candidate.
   bool compacted = false;
   int64_t n_bin = 0;
+  // Radix state, and a per-slice filter from the slice's key range: a pass
+  // counting keys equal to the prefix (1) or taking keys up to it (2) skips
+  // slices that cannot hold such a key (often most of them: ids are handed
+  // out in order, so last_used and ids correlate).
+  uint64_t prefix = 0, mask = 0;
+  int slice_filter = 0;
+  __shared__ int live[kMaxLiveSlices];
+  __shared__ int n_live;
+  auto slice_skip = [&](int sl) {
+    if (!slice_filter || G.ncnt[sl] == 0) return slice_filter != 0;
+    const uint64_t lo = G.kmin[sl] & mask, hi = G.kmax[sl] & mask;
+    return lo > prefix || (slice_filter == 1 && hi < prefix);
+  };
+  // the slices passing the filter, listed in shared memory (the same list on
+  // every CTA: it depends on global data only); returns their count
+  auto live_slices = [&]() {
+    if (t == 0) n_live = 0;
+    __syncthreads();
+    for (int sl = t; sl < G.n_slices; sl += blockDim.x)
+      if (!slice_skip(sl)) live[atomicAdd(&n_live, 1)] = sl;
+    __syncthreads();
+    return n_live;
+  };
   auto for_keys = [&](auto&& f) {
     if (compacted) {
       for (int64_t i = static_cast<int64_t>(cta) * blockDim.x + t; i < n_bin;
@@ -1596,15 +1621,31 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
         f(S.keys[i]);
     } else if (staged) {
       for (int j = 0; j < nseg; ++j) {
+        if (slice_skip(cta + j * n_cta)) continue;
         const uint64_t* src = local_keys + seg_off[j];
         for (int64_t i = t; i < seg_n[j]; i += blockDim.x) f(src[i]);
       }
+    } else if (slice_filter && live_slices() * 4 <= G.n_slices) {
+      // in place, few slices can hold a wanted key (the smallest keys often
+      // sit in one slice, not spread over the CTAs' own slices): the whole
+      // grid strides over each listed slice
+      const int nl2 = n_live;
+      for (int q = 0; q < nl2; ++q) {
+        const int sl = live[q];
+        const int64_t c = G.ncnt[sl];
+        const uint64_t* src = G.keys + sl * G.slice;
+        for (int64_t i = static_cast<int64_t>(cta) * blockDim.x + t; i < c;
+             i += static_cast<int64_t>(n_cta) * blockDim.x)
+          f(__ldcg(src + i));
+      }
+      __syncthreads();  // the list is rebuilt by the next pass
     } else {
       // in place (L2/HBM): key pairs as 16 B loads, four in flight per
       // thread before the keys are consumed, so a pass streams instead of
       // waiting one load latency per key (a slice's keys start 32 B aligned)
       constexpr int kU = 4;
       for (int sl = cta; sl < G.n_slices; sl += n_cta) {
+        if (slice_skip(sl)) continue;
         const int64_t c = G.ncnt[sl];
         const uint64_t* src = G.keys + sl * G.slice;
         const ulonglong2* src2 = reinterpret_cast<const ulonglong2*>(src);
@@ -1626,7 +1667,6 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
     }
   };
   __syncthreads();
-  uint64_t prefix = 0, mask = 0;
   if (K > 0 && K < ncand) {
     const uint64_t kmin = key_lo, diff = key_lo ^ key_hi;
     int hi_bit = 64 - __clzll(static_cast<long long>(diff));  // bits above are shared by every candidate
@@ -1644,9 +1684,11 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
       // (a warp-aggregated add for warps whose keys share a bin measured
       // slower than these plain shared atomics; the pass is bound by the key
       // loads, profiles/README.md)
+      slice_filter = pass > 0 ? 1 : 0;  // pass 1's prefix is the bits every key shares
       for_keys([&](uint64_t k) {
         if ((k & mask) == prefix) atomicAdd(&hist[(k >> sh_) & bmask], 1u);
       });
+      slice_filter = 0;
       if (pass == 0 && G.tprof && cta == 5 && (t & 31) == 0) G.tprof[32 + 320 + (t >> 5)] = gtimer();
       __syncthreads();
       if (pass < 2) tp_max(G, 22 + pass);
@@ -1679,9 +1721,11 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
       const bool done = static_cast<int64_t>(cnt_b) == need;
       __syncthreads();
       if (done) break;
-      // the chosen bin plus the lower bins fit the rank buffer: gather them
-      // all and let the rank step pick the K smallest (no further pass)
-      if ((K - need) + static_cast<int64_t>(cnt_b) <= G.sort_keys) break;
+      // the chosen bin plus the lower bins are few enough for the rank step
+      // (O(M^2) compares spread over the grid: ~2 us at 4K keys, ~7 us at
+      // 8K, where another radix pass costs ~3-4 us): gather them all and let
+      // the rank step pick the K smallest
+      if ((K - need) + static_cast<int64_t>(cnt_b) <= min(G.sort_keys, kRankEarlyMax)) break;
       if (!staged && !compacted && hi_bit > 0) {
         const int lane = t & 31;
         auto append = [&](bool take, uint64_t k, unsigned long long* ctr, uint64_t* dst) {
@@ -1694,11 +1738,13 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
           base = __shfl_sync(am, base, leader);
           if (take) dst[base + __popc(b & ((1u << lane) - 1u))] = k;
         };
+        slice_filter = 2;
         for_keys([&](uint64_t k) {
           const uint64_t km = k & mask;
           append(km < prefix, k, &G.ctr[1], S.sortbuf);  // lower bins: selected
           append(km == prefix, k, &G.ctr[5], S.keys);    // the chosen bin
         });
+        slice_filter = 0;
         tp_max(G, 24);
         if (cta == 0) tp_set(G, 28);
         if (G.tprof && t == 0) G.tprof[32 + 160 + cta] = gtimer();  // per-CTA compaction finish
@@ -1712,6 +1758,7 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
     // gather the selected keys (after a compaction only the chosen bin's:
     // the lower bins are listed already): one global atomic per warp
     const int lane = t & 31;
+    slice_filter = 2;
     for_keys([&](uint64_t k) {
       const bool sel = K == ncand || (k & mask) <= prefix;
       const unsigned am = __activemask();
@@ -1725,6 +1772,7 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
     });
   }
   tp_max(G, 25);
+  if (G.tprof && t == 0 && !compacted) G.tprof[32 + 160 + cta] = gtimer();  // per-CTA gather finish
   gsync();
   // gathered keys: K, or the K plus the rest of the chosen bin after an early exit
   const int64_t M = K > 0 ? static_cast<int64_t>(*reinterpret_cast<volatile unsigned long long*>(&G.ctr[1])) : 0;
@@ -1733,7 +1781,20 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
     // share of them (rank = gathered keys below it; keys are unique), one
     // warp per key, lanes splitting the comparisons; ranks < K are the victims
     tp_set(G, 20);
-    for (int64_t i = t; i < M; i += blockDim.x) local_keys[i] = __ldcg(S.sortbuf + i);
+    constexpr int kLU = 8;  // eight loads in flight per thread, not one round trip per key
+    for (int64_t i0 = t; i0 < M; i0 += kLU * static_cast<int64_t>(blockDim.x)) {
+      uint64_t v[kLU];
+#pragma unroll
+      for (int u = 0; u < kLU; ++u) {
+        const int64_t i = i0 + static_cast<int64_t>(u) * blockDim.x;
+        v[u] = i < M ? __ldcg(S.sortbuf + i) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < kLU; ++u) {
+        const int64_t i = i0 + static_cast<int64_t>(u) * blockDim.x;
+        if (i < M) local_keys[i] = v[u];
+      }
+    }
     __syncthreads();
     const int64_t per = (M + n_cta - 1) / n_cta, r_lo = cta * per, r_hi = min(M, r_lo + per);
     const int lane = t & 31, nw = blockDim.x >> 5;
@@ -3280,7 +3341,7 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
           SB_CUDA(cudaFuncSetAttribute(k_select_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(c->coop_smem)));
           SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_select_coop, kSelectThreads, c->coop_smem));
-          if (per_sm >= 1) c->coop_grid = n_sm;
+          if (per_sm >= 1 && n_slices <= kMaxLiveSlices) c->coop_grid = n_sm;
           {  // the fused kernel: the scoring ring and the select's buffers share its dynamic shared memory
             cudaFuncAttributes ff{};
             SB_CUDA(cudaFuncGetAttributes(&ff, k_evict_fused));
