@@ -247,7 +247,8 @@ def test_large_pool_cooperative_scorer():
 @pytest.mark.gpu
 def test_cooperative_evict_beyond_shared_memory_sort():
     """evict(K) with K above what the cooperative select ranks in shared
-    memory (16K keys): CTA 0 sorts the winners in global memory instead.
+    memory (24K keys in the fused kernel, 16K in k_select_coop): CTA 0 sorts
+    the winners in global memory instead.
     Every tier and several timestamps, so the radix passes run over the
     tier and last_used bits of the keys as well as the ids."""
     bs, cap = 1, 70000
@@ -266,8 +267,35 @@ def test_cooperative_evict_beyond_shared_memory_sort():
         assert o.release(ids) == c.release(ids) == 0
     for ids in live[1::3]:
         assert o.release(ids) == c.release(ids) == 0
-    for needed in (20000, 3, 17000):
+    for needed in (30000, 3, 9000):  # 30000: above the fused kernel's 24K-key rank buffer
         assert o.evict(needed) == c.evict(needed), needed
+    assert o.dump() == c.dump()
+
+
+@pytest.mark.gpu
+def test_cooperative_select_keys_in_place():
+    """A 16M-block pool whose candidates crowd into the first score slices:
+    one CTA holds more keys than shared memory, so the select reads them in
+    place (compaction after pass 1, slice filters, the grid striding over the
+    few live slices), for K below and above the rank-step and shared-memory
+    limits."""
+    bs, cap = 1, 1 << 24
+    c = product(bs, cap, 1)
+    o = O.OracleCache(bs, cap, 1)
+    rng = np.random.default_rng(77)
+    live = []
+    for k in range(10):
+        t = O.materialize(int(rng.integers(4)), 4000, 1200 + k)
+        tags = [(0, 1300, int(rng.integers(6))), (1300, 4000, int(rng.integers(6)))]
+        now = int(rng.integers(0, 20))
+        a, b = o.insert(t, tags, now), c.insert(t, tags, now)
+        assert a == b, k
+        live.append(a[1])
+    for ids in live:
+        assert o.release(ids) == c.release(ids) == 0
+    for needed in (64, 5000, 3, 20000, 9000):
+        assert o.evict(needed) == c.evict(needed), needed
+    assert o.total_evicted() == c.total_evicted()
     assert o.dump() == c.dump()
 
 
@@ -285,7 +313,7 @@ def test_three_kernel_evict_path():
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_kvcache_gpu.py", "-k",
                         "cooperative_scorer or beyond_shared_memory or in_place"], cwd=root, env=env,
                        capture_output=True, text=True, timeout=1200)
-    assert r.returncode == 0 and "3 passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
+    assert r.returncode == 0 and "4 passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
 
 
 @pytest.mark.gpu
