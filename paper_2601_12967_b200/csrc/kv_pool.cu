@@ -1567,8 +1567,10 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
   if (staged) {
     int64_t off = 0;
     for (int sl = cta; sl < G.n_slices; sl += n_cta, ++nseg) {
-      seg_off[nseg] = off;
-      seg_n[nseg] = G.ncnt[sl];
+      if (t == 0) {  // the segment table (read by all after the barrier below)
+        seg_off[nseg] = off;
+        seg_n[nseg] = G.ncnt[sl];
+      }
       off += (G.ncnt[sl] + 1) & ~int64_t(1);
     }
     if (t == 0) {
