@@ -674,11 +674,24 @@ def pool_rooflines():
     bench_kv.QUIET = True
     bench_kv.ROWS.clear()
     bench_kv.main("hash,probe_big,evict_small,evict,evict_big,append")
+    keys = ("kernel", "config", "achieved_gbs", "peak_gbs", "frac", "seconds", "algorithmic_bytes", "timing", "note")
     keep = []
     for r in bench_kv.ROWS:
-        keep.append({k: r[k] for k in ("kernel", "config", "achieved_gbs", "peak_gbs", "frac", "seconds",
-                                        "algorithmic_bytes", "timing", "note") if k in r} | (
-            {"parts_us": r["parts_us"]} if "parts_us" in r else {}))
+        keep.append({k: r[k] for k in keys if k in r} | ({"parts_us": r["parts_us"]} if "parts_us" in r else {}))
+    # the scoring pass alone: only the three-kernel path launches it as its
+    # own kernel (a subprocess: the path switch is read once per process)
+    try:
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "bench_kv.py"), "--only", "evict,evict_big"],
+                             env=dict(os.environ, SB_EVICT_FUSED="0"), capture_output=True, text=True,
+                             timeout=600).stdout
+        for line in out.splitlines():
+            if line.startswith("{"):
+                r = json.loads(line)
+                if r["kernel"].startswith("k_score"):
+                    r["kernel"] = "k_score (the scoring pass alone; three-kernel path, SB_EVICT_FUSED=0)"
+                    keep.append({k: r[k] for k in keys if k in r})
+    except Exception as e:  # evidence only: the fused rows above stand
+        keep.append({"kernel": "k_score (three-kernel path)", "error": repr(e)[:200]})
     return {"bound": "hbm", "unit": "GB/s", "rows": keep,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
             "bytes": "algorithmic bytes per launch (bench_kv.py docstring / DESIGN.md), CUPTI device time, L2 "
