@@ -64,7 +64,7 @@ def parse():
     return ap.parse_args()
 
 
-ATTN_NCU = os.path.join(ROOT, "profiles", "r01", "attention_v5_metrics.json")
+ATTN_NCU = os.path.join(ROOT, "profiles", "r02", "attention_r2_metrics.json")
 
 
 def ncu_traffic(path):
@@ -336,7 +336,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "kernel": "k_continuation_attention", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": ncu_traffic(ATTN_NCU),
-                     "traffic_source": "profiles/r01/attention_v5_metrics.json (ncu --set full, one launch, bytes)",
+                     "traffic_source": "profiles/r02/attention_r2_metrics.json (ncu --set full, one launch, bytes)",
                      "peak_source": f"{peak_kind} bf16_tflops_sustained (kernel timed inside a long step)",
                      "flops_per_launch": flops_attn, "avg_launch_ms": attn_avg_ms,
                      "launches_timed": len(attn_ms)},
