@@ -2547,7 +2547,7 @@ static void launch_probe_rows(const Pool& P, const uint64_t* tokens, const int64
   static int per = -1;
   if (per < 0) {
     const char* e = getenv("SB_PROBE_PER");
-    per = e ? atoi(e) : 0;  // 0: the two-phase k_probe_rows2 (16-token blocks)
+    per = e ? atoi(e) : 0;  // 0: the warp-granular k_probe_rows3 (16-token blocks)
   }
   if (per == 0 && P.bs == 16) {  // warp-granular two-phase probe
     const int64_t runs = (max_np + 32 * kProbe3Warps - 1) / (32 * kProbe3Warps);
