@@ -383,7 +383,9 @@ def run_dense(args, rank, world, local_rank):
     step (embedding, 32 x {RMSNorm, QKV GEMM, RoPE + KV scatter, paged
     continuation attention, O GEMM, SwiGLU MLP}, LM head + greedy token on
     each sequence's last token) plus the pool ops (hash, lookup, insert with
-    eviction, release).  GEMMs are cuBLAS; everything else is ours."""
+    eviction, release).  Every kernel is ours: the projections run on the
+    tcgen05 GEMM of csrc/gemm.cu (SwiGLU and the residual adds fused into its
+    epilogue); SB_GEMM_CUBLAS=1 is the cuBLAS A/B arm."""
     import torch
     import torch.distributed as dist
     from paper_2601_12967_b200 import workload as W
@@ -464,7 +466,9 @@ def run_dense(args, rank, world, local_rank):
         "attention_ms_per_step": attn_ms, "attention_share": attn_ms / step_ms,
         "attention_tflops": attn / (attn_ms * 1e-3) / 1e12,
         "rest_tflops": dense / ((step_ms - attn_ms) * 1e-3) / 1e12,
-        "rest": "cuBLAS bf16 GEMMs (QKV/O/gate-up/down/LM head) + our RMSNorm/RoPE/SwiGLU/pool kernels",
+        "rest": ("cuBLAS bf16 GEMMs (SB_GEMM_CUBLAS=1 A/B arm) + our SwiGLU" if os.environ.get("SB_GEMM_CUBLAS") == "1"
+                 else "our tcgen05 GEMMs (csrc/gemm.cu: QKV, O + residual, gate/up + SwiGLU, down + residual, "
+                      "LM head)") + " + our RMSNorm/RoPE/pool kernels",
         "partial_prefill": {"tokens": int(prefix_tokens), "ms": prefix_ms,
                             "tokens_per_s": prefix_tokens / (prefix_ms * 1e-3),
                             "note": "uncached prefix tokens of the 8 requests through the full model "

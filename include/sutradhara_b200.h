@@ -388,6 +388,15 @@ int sb_batch_info(const sb_batch* batch, int64_t* total_q, int64_t* total_blocks
  * configs[2]); the reference charges this compute as a cost
  * (CostModel::chunk_ms, engine.cpp:35-39).  d_model = 128 * n_q_heads. */
 typedef struct sb_model sb_model;
+
+/* The projections' GEMM (csrc/gemm.cu, tcgen05 + TMA, persistent):
+ * Y[rows, n] (op)= X[rows, k] W[n, k]^T, row-major bf16, fp32 accumulate.
+ * mode 0: Y = acc (bf16); 1: Y += acc (bf16 residual); 2: Y = acc (fp32);
+ * 3: SwiGLU — W is [2n, k] (gate rows, then up rows), Y[rows, n] =
+ * silu(gate) * up.  n and k multiples of 8. */
+int sb_gemm_bf16(const void* x, const void* w, void* y, int64_t rows, int64_t n, int64_t k,
+                 int32_t mode, void* stream);
+
 int sb_model_create(int32_t n_layers, int32_t d_model, int32_t n_q_heads, int32_t n_kv_heads,
                     int32_t d_ff, int64_t vocab, float rope_theta, uint64_t seed, int32_t device,
                     sb_model** out);

@@ -106,6 +106,7 @@ SIGNATURES = {
     "sb_batch_copy_output": (C.c_int, [VP, C.c_int64, C.c_int64, VP, VP]),
     "sb_batch_info": (C.c_int, [VP, I64P, I64P, I64P, C.POINTER(C.c_double), C.POINTER(VP)]),
     "sb_kv_append": (C.c_int, [VP, VP, VP, VP, VP, VP, VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, VP]),
+    "sb_gemm_bf16": (C.c_int, [VP, VP, VP, C.c_int64, C.c_int64, C.c_int64, C.c_int32, VP]),
     "sb_model_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_float,
                                   C.c_uint64, C.c_int32, C.POINTER(VP)]),
     "sb_model_destroy": (None, [VP]),

@@ -22,10 +22,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
 #include "common.h"
+#include "gemm.h"
 #include "hash.cuh"
 
 namespace sb {
@@ -225,6 +227,9 @@ struct sb_model {
   };
   std::vector<Layer> layers;
   __nv_bfloat16 *emb = nullptr, *lm_head = nullptr, *final_norm = nullptr;
+  // A/B switch only (SB_GEMM_CUBLAS=1): the projections on cuBLAS instead of
+  // the hand-written tcgen05 GEMM (gemm.cu), for the measured comparison
+  bool use_cublas = false;
   cublasHandle_t blas = nullptr;
   ~sb_model() {
     cudaSetDevice(device);
@@ -257,14 +262,23 @@ __nv_bfloat16* alloc_const(int64_t n, float v) {
 
 int grid_n(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16))); }
 
-// Y[rows, n] (+)= X[rows, k] W[n, k]^T, row-major bf16 (nn.Linear layout)
-void linear(cublasHandle_t h, const __nv_bfloat16* x, const __nv_bfloat16* w, void* y, int64_t rows, int64_t n,
-            int64_t k, float beta, bool y_fp32) {
-  const float alpha = 1.f;
-  SB_BLAS(cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(n), static_cast<int>(rows), static_cast<int>(k),
-                       &alpha, w, CUDA_R_16BF, static_cast<int>(k), x, CUDA_R_16BF, static_cast<int>(k), &beta, y,
-                       y_fp32 ? CUDA_R_32F : CUDA_R_16BF, static_cast<int>(n), CUBLAS_COMPUTE_32F,
-                       CUBLAS_GEMM_DEFAULT));
+// Y[rows, n] (+)= X[rows, k] W[n, k]^T, row-major bf16 (nn.Linear layout):
+// the tcgen05 GEMM of gemm.cu with its fused epilogue (`mode`); cuBLAS only
+// under the SB_GEMM_CUBLAS=1 A/B switch (kSwiGLU then writes [gate | up] to
+// gu and k_swiglu follows, as before the fused epilogue)
+void linear(sb_model* m, cudaStream_t st, const __nv_bfloat16* x, const __nv_bfloat16* w, void* y, int64_t rows,
+            int64_t n, int64_t k, int mode) {
+  if (!m->use_cublas) {
+    gemm_bf16(x, w, y, rows, n, k, mode, st);
+    return;
+  }
+  SB_BLAS(cublasSetStream(m->blas, st));
+  const float alpha = 1.f, beta = mode == kAddBf16 ? 1.f : 0.f;
+  const int64_t cols = mode == kSwiGLU ? 2 * n : n;
+  SB_BLAS(cublasGemmEx(m->blas, CUBLAS_OP_T, CUBLAS_OP_N, static_cast<int>(cols), static_cast<int>(rows),
+                       static_cast<int>(k), &alpha, w, CUDA_R_16BF, static_cast<int>(k), x, CUDA_R_16BF,
+                       static_cast<int>(k), &beta, y, mode == kStoreF32 ? CUDA_R_32F : CUDA_R_16BF,
+                       static_cast<int>(cols), CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT));
 }
 
 }  // namespace
@@ -305,7 +319,9 @@ int sb_model_create(int32_t n_layers, int32_t d_model, int32_t n_q_heads, int32_
         L.n2 = alloc_const(d, 1.f);
         m->layers.push_back(L);
       }
-      SB_BLAS(cublasCreate(&m->blas));
+      const char* ab = std::getenv("SB_GEMM_CUBLAS");
+      m->use_cublas = ab && ab[0] == '1';
+      if (m->use_cublas) SB_BLAS(cublasCreate(&m->blas));
       SB_CUDA(cudaDeviceSynchronize());
     } catch (...) {
       delete m;
@@ -448,9 +464,8 @@ void model_layer_pre(sb_model* m, ModelWorkspace* w, int l, void* k_pool, void* 
                      cudaStream_t st) {
   const auto& L = m->layers[l];
   const int64_t T = w->rows, d = m->d, qkv = static_cast<int64_t>(m->hq + 2 * m->hkv) * 128;
-  SB_BLAS(cublasSetStream(m->blas, st));
   model::k_rmsnorm<<<static_cast<unsigned>((T + 7) / 8), 256, 0, st>>>(w->x, L.n1, w->xn, T, m->d, m->eps, nullptr);
-  linear(m->blas, w->xn, L.wqkv, w->qkv, T, qkv, d, 0.f, false);
+  linear(m, st, w->xn, L.wqkv, w->qkv, T, qkv, d, kStoreBf16);
   model::k_rope_scatter<<<grid_n(T * (m->hq + 2 * m->hkv) * 8), 256, 0, st>>>(
       w->qkv, w->rope, w->q, static_cast<__nv_bfloat16*>(k_pool), static_cast<__nv_bfloat16*>(v_pool), q_off, kv_len,
       table, n_seqs, max_blocks, m->hq, m->hkv);
@@ -461,19 +476,23 @@ void model_layer_pre(sb_model* m, ModelWorkspace* w, int l, void* k_pool, void* 
 void model_layer_post(sb_model* m, ModelWorkspace* w, int l, cudaStream_t st) {
   const auto& L = m->layers[l];
   const int64_t T = w->rows, d = m->d;
-  linear(m->blas, w->a, L.wo, w->x, T, d, d, 1.f, false);
+  linear(m, st, w->a, L.wo, w->x, T, d, d, kAddBf16);
   model::k_rmsnorm<<<static_cast<unsigned>((T + 7) / 8), 256, 0, st>>>(w->x, L.n2, w->xn, T, m->d, m->eps, nullptr);
-  linear(m->blas, w->xn, L.wgu, w->gu, T, 2 * static_cast<int64_t>(m->dff), d, 0.f, false);
-  model::k_swiglu<<<grid_n(T * m->dff / 8), 256, 0, st>>>(w->gu, w->h, T, m->dff);
-  SB_CHECK_LAUNCH();
-  linear(m->blas, w->h, L.wd, w->x, T, d, m->dff, 1.f, false);
+  if (m->use_cublas) {
+    linear(m, st, w->xn, L.wgu, w->gu, T, m->dff, d, kSwiGLU);
+    model::k_swiglu<<<grid_n(T * m->dff / 8), 256, 0, st>>>(w->gu, w->h, T, m->dff);
+    SB_CHECK_LAUNCH();
+  } else {
+    linear(m, st, w->xn, L.wgu, w->h, T, m->dff, d, kSwiGLU);  // gate/up GEMM + SwiGLU in one kernel
+  }
+  linear(m, st, w->h, L.wd, w->x, T, d, m->dff, kAddBf16);
 }
 
 // Final norm of every sequence's last token, LM head (fp32 logits), argmax.
 void model_head(sb_model* m, ModelWorkspace* w, cudaStream_t st) {
   model::k_rmsnorm<<<static_cast<unsigned>((w->n_seqs + 7) / 8), 256, 0, st>>>(w->x, m->final_norm, w->xl, w->n_seqs,
                                                                               m->d, m->eps, w->last_rows);
-  linear(m->blas, w->xl, m->lm_head, w->logits, w->n_seqs, m->vocab, m->d, 0.f, true);
+  linear(m, st, w->xl, m->lm_head, w->logits, w->n_seqs, m->vocab, m->d, kStoreF32);
   model::k_argmax<<<w->n_seqs, 256, 0, st>>>(w->logits, m->vocab, w->next_tok);
   SB_CHECK_LAUNCH();
 }
