@@ -125,3 +125,16 @@ def test_unsupported_shape_is_an_error():
     with pytest.raises(ValueError):
         _gemm(x, w, y, 16, 16, 16, 9)  # unknown mode
     del _lib
+
+
+def test_one_cta_kernel_at_every_shape():
+    """Rows above 128 run on the CTA-pair kernel; the same tests with
+    SB_GEMM_PAIR=0 put every shape through the 1-CTA kernel."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SB_GEMM_PAIR="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.abspath(__file__), "-k",
+                        "not one_cta_kernel"], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
