@@ -477,10 +477,64 @@ def run_dense(args, rank, world, local_rank):
         "ttft_after_tool_monolithic_ms": prefix_ms + step_ms,
         "ttft_speedup_from_splitting": (prefix_ms + step_ms) / step_ms,
         "first_tokens_sample": batch.model_result()[:4].tolist(),
+        "gemm_roofline": gemm_roofline(batch.total_q, LLAMA3_8B_DENSE, len(reqs)),
     }
     del batch, eng, model
     torch.cuda.empty_cache()
     return out
+
+
+def gemm_roofline(rows, shape, n_last, iters=10):
+    """The projections' GEMM (csrc/gemm.cu through sb_gemm_bf16) at the
+    configs[2] step's shapes — `rows` suffix tokens, the model's dimensions,
+    the LM head over the `n_last` last tokens — each launch timed alone with
+    CUDA events on its stream (median of `iters`, L2 flushed between
+    launches); 2*rows*n*k FLOP per launch (gate/up: n = 2*d_ff) against the
+    measured dense bf16 peak (burst: a kernel timed alone)."""
+    import ctypes as C
+
+    import torch
+    from paper_2601_12967_b200 import _lib
+
+    L = _lib.lib()
+    st = torch.cuda.current_stream()
+    peaks, src = load_peaks()
+    peak = peaks.get("bf16_tflops")
+    d, dff, vocab = shape.d_model, shape.d_ff, shape.vocab
+    qkv = (shape.n_q_heads + 2 * shape.n_kv_heads) * 128
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    out = []
+    for name, r, n, k, mode in (("qkv", rows, qkv, d, 0), ("o+residual", rows, d, d, 1),
+                                ("gate_up+swiglu", rows, dff, d, 3), ("down+residual", rows, d, dff, 1),
+                                ("lm_head (fp32 logits)", n_last, vocab, d, 2)):
+        wr = 2 * n if mode == 3 else n
+        x = torch.randn(r, k, device="cuda").to(torch.bfloat16)
+        w = (torch.randn(wr, k, device="cuda") / k ** 0.5).to(torch.bfloat16)
+        y = torch.zeros(r, n, device="cuda", dtype=torch.float32 if mode == 2 else torch.bfloat16)
+        ts = []
+        for i in range(iters + 2):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            _lib.check(L.sb_gemm_bf16(C.c_void_p(x.data_ptr()), C.c_void_p(w.data_ptr()), C.c_void_p(y.data_ptr()),
+                                      r, n, k, mode, C.c_void_p(st.cuda_stream)), "sb_gemm_bf16")
+            e1.record(st)
+            e1.synchronize()
+            if i >= 2:
+                ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        tf = 2.0 * r * wr * k / (ms * 1e-3) / 1e12
+        nbytes = 2 * (r * k + wr * k) + (4 if mode == 2 else 2) * r * n * (2 if mode == 1 else 1)
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        out.append({"gemm": name, "rows": r, "n": wr, "k": k, "us": ms * 1e3, "tflops": tf,
+                    "frac": tf / peak if peak else None, "bytes": nbytes, "gbs": gbs,
+                    "hbm_frac": gbs / peaks["hbm_gbs"],
+                    "bound": "tensor" if 2.0 * r * wr * k / nbytes > 300 else "hbm (weights streamed once)",
+                    "kernel": "k_gemm_pair (cta_group::2)" if r > 128 else "k_gemm (1 CTA)"})
+        del x, w, y
+    del flush
+    return {"bound": "tensor", "peak_tflops": peak, "peak_source": f"{src}: bf16_tflops (burst)",
+            "rows": out}
 
 
 def run_toy(local_rank):
