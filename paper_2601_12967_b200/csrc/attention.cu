@@ -30,6 +30,7 @@
 #include <cmath>
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 
 #include "common.h"
@@ -396,6 +397,344 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2, SB_ATTN_PAIR=1): a cluster of two CTAs takes a
+// quad of query tiles — CTA r the pair 2*quad + r — and the leader issues
+// every MMA with M = 256 over both CTAs' rows.  The K/V tiles are split
+// across the pair: for S = Q K^T (N = 128 keys) CTA r stages keys
+// [64r, 64r + 64) of the tile; for O += P V (N = 128 dims) CTA r stages dims
+// [64r, 64r + 64) of every key.  Each SM so moves half the K/V bytes from L2
+// and reads a third fewer operand bytes from shared memory per FLOP than the
+// 1-CTA kernel above (the GEMM's pair kernel measured +13 % over its 1-CTA
+// form under the same power cap).  The softmax is unchanged and local: each
+// CTA's TMEM holds S, P and O of its own 128-row tiles.  Barriers: Q and K/V
+// TMA completions of both CTAs count on the leader's q_full / kv_full; the
+// leader's commits multicast to both CTAs' kv_empty / s_full / o_done; P
+// parts are released on the leader's p_part by one lane per softmax warp of
+// both CTAs (8 arrivals).  Both CTAs run the quad's key range (the larger of
+// the two causal limits); a CTA past the sequence's last query computes
+// discarded rows.
+// SB_ATTN_PAIR=1: the CTA-pair kernel below instead of the 1-CTA kernel
+// (A/B switch, read once per process).  Measured on the configs[1] step
+// (profiles/r02/attn_pair_ab.txt): the pair runs ~4.5 % higher clocks under
+// the 1 kW cap (less operand traffic per FLOP) but ~6 % less work per clock
+// (the pair's MMAs wait on both CTAs' softmax; a quad's second pair may be
+// empty; the quad's causal limit covers both CTAs): 261.4-261.9K vs
+// 265.1-265.9K tokens/s, so the 1-CTA kernel stays the default.
+inline bool pair_mode() {
+  static const bool on = [] {
+    const char* e = std::getenv("SB_ATTN_PAIR");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+namespace pairk {
+
+constexpr int kStages = 8;
+constexpr int kHalf = 16384;       // one CTA's share of a K or V tile
+constexpr int kHalfAtom = 8192;    // 64 key rows x 128 B (K half, one 64-dim atom)
+constexpr int kSmemBytes = 2 * kTileBytes + kStages * kHalf + 1024;
+
+struct Smem {
+  uint64_t q_full;
+  uint64_t kv_full[kStages];
+  uint64_t kv_empty[kStages];
+  uint64_t s_full[2];
+  uint64_t p_part[2][4];
+  uint64_t o_done[2];
+  uint32_t tmem_base;
+};
+
+// kPSplit: P released to the issuer in this many parts per tile (2 measured
+// best for the pair: each release is a remote arrive); kSpin: the issuer
+// spins on those arrivals instead of a suspended wait (measured faster).
+template <int kPSplit, bool kSpin>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_continuation_attention_pair(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                                  const __grid_constant__ CUtensorMap tm_v, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = base;                    // [2 tiles][2 atoms][16 KB]
+  uint8_t* sKV = base + 2 * kTileBytes;  // [kStages][16 KB]
+  __shared__ Smem ss;
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint32_t rank = cluster_rank();
+  const int item = blockIdx.x >> 1;
+  int quad, kvh, seq;
+  if (p.work) {
+    seq = p.work[2 * item];
+    kvh = p.work[2 * item + 1] >> 16;
+    quad = p.work[2 * item + 1] & 0xFFFF;
+  } else {
+    const int quads = (p.pairs_per_seq + 1) >> 1;
+    quad = item % quads;
+    kvh = (item / quads) % p.n_kv_heads;
+    seq = item / (quads * p.n_kv_heads);
+  }
+  const int q0 = p.q_off[seq];
+  const int q_len = p.q_off[seq + 1] - q0;
+  const int kv_len = p.kv_len[seq];
+  const int first_q = (2 * quad + static_cast<int>(rank)) * 2 * p.tpt;  // this CTA's row 0 of tile 0
+  const int quad_q = quad * 4 * p.tpt;
+  // the item exists only if the quad has queries: both CTAs run (the MMAs span the pair)
+  if (quad_q >= q_len) return;
+  const int prefix = kv_len - q_len;
+  const int kv_limit = prefix + min(q_len, quad_q + 4 * p.tpt);
+  const int n_kv = (kv_limit + 127) / 128;
+
+  if (tid == 0) {
+    mbar_init(&ss.q_full, 1);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&ss.kv_full[i], 1);
+      mbar_init(&ss.kv_empty[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&ss.s_full[t], 1);
+      for (int i = 0; i < 4; ++i) mbar_init(&ss.p_part[t][i], 8);
+      mbar_init(&ss.o_done[t], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc2(&ss.tmem_base);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = ss.tmem_base;
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs: their halves) =====================
+    if (elect_one()) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      const uint32_t q_full0 = mapa(&ss.q_full, 0);
+      if (rank == 0) mbar_arrive_expect_tx(&ss.q_full, 4 * kTileBytes);
+      for (int t = 0; t < 2; ++t)
+        for (int a = 0; a < 2; ++a)
+          tma_load_3d_pair(sQ + t * kTileBytes + a * kAtomBytes, &tm_q, q_full0, a * 64, kvh * p.group,
+                           q0 + first_q + t * p.tpt);
+      const int32_t* trow = p.table + static_cast<int64_t>(seq) * p.max_blocks;
+      int rows[8], next_rows[8];
+      auto fetch_rows = [&](int j, int (&r)[8]) {
+#pragma unroll
+        for (int pg = 0; pg < 8; ++pg) {
+          const int jb = j * 8 + pg;
+          const int page = (jb * 16 < kv_limit) ? __ldg(trow + jb) : -1;
+          r[pg] = page >= 0 ? (page * p.n_kv_heads + kvh) * 16 : p.oob_row;
+        }
+      };
+      fetch_rows(0, rows);
+      for (int i = 0; i < 2 * n_kv; ++i) {
+        const int j = i >> 1, which = i & 1, stage = i % kStages;
+        if (which == 0 && j + 1 < n_kv) fetch_rows(j + 1, next_rows);
+        mbar_wait_suspend(&ss.kv_empty[stage], ((i / kStages) & 1) ^ 1);
+        const uint32_t full0 = mapa(&ss.kv_full[stage], 0);
+        if (rank == 0) mbar_arrive_expect_tx(&ss.kv_full[stage], 2 * kHalf);
+        uint8_t* dst = sKV + stage * kHalf;
+        if (which == 0) {
+          // K: keys [64 rank, 64 rank + 64) = pages 4 rank .. 4 rank + 3, both 64-dim atoms
+#pragma unroll
+          for (int pp = 0; pp < 4; ++pp)
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+              tma_load_2d_pair(dst + a * kHalfAtom + pp * 2048, &tm_k, full0, a * 64, rank ? rows[4 + pp] : rows[pp]);
+        } else {
+          // V: dims [64 rank, 64 rank + 64) of all 128 keys
+#pragma unroll
+          for (int pg = 0; pg < 8; ++pg)
+            tma_load_2d_pair(dst + pg * 2048, &tm_v, full0, static_cast<int>(rank) * 64, rows[pg]);
+          if (j + 1 < n_kv)
+#pragma unroll
+            for (int pg = 0; pg < 8; ++pg) rows[pg] = next_rows[pg];
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader only) =====================
+    if (rank == 0 && elect_one()) {
+      const uint32_t idesc_qk = idesc_bf16_f32(256, 128, 0, 0);
+      const uint32_t idesc_pv = idesc_bf16_f32(256, 128, 0, 1);
+      const uint32_t sq = smem_u32(sQ), skv = smem_u32(sKV);
+      mbar_wait_suspend(&ss.q_full, 0);
+      auto wait_stage = [&](int i) { mbar_wait_suspend(&ss.kv_full[i % kStages], (i / kStages) & 1); };
+      auto qk = [&](int t, int j) {
+        const uint32_t kb = skv + ((2 * j) % kStages) * kHalf;
+        const uint32_t qb = sq + t * kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t qoff = (kk >> 2) * kAtomBytes + (kk & 3) * 32;
+          const uint32_t koff = (kk >> 2) * kHalfAtom + (kk & 3) * 32;
+          mma_ss2(tmem + t * 128, smem_desc_sw128(qb + qoff, 16, 1024), smem_desc_sw128(kb + koff, 16, 1024),
+                  idesc_qk, kk > 0);
+        }
+        mma_commit2(&ss.s_full[t]);
+      };
+      auto pv = [&](int t, int j) {
+        const uint32_t vb = skv + ((2 * j + 1) % kStages) * kHalf;
+#pragma unroll
+        for (int part = 0; part < kPSplit; ++part) {
+          if (kSpin)
+            mbar_wait(&ss.p_part[t][part], j & 1);
+          else
+            mbar_wait_suspend(&ss.p_part[t][part], j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = part * (8 / kPSplit); kk < (part + 1) * (8 / kPSplit); ++kk)
+            mma_ts2(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, smem_desc_sw128(vb + kk * 2048, kAtomBytes, 1024),
+                    idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit2(&ss.o_done[t]);
+      };
+      wait_stage(0);
+      tc_fence_after();
+      qk(0, 0);
+      qk(1, 0);
+      mma_commit2(&ss.kv_empty[0]);
+      for (int j = 0; j < n_kv; ++j) {
+        wait_stage(2 * j + 1);
+        tc_fence_after();
+        pv(0, j);
+        if (j + 1 < n_kv) {
+          wait_stage(2 * j + 2);
+          tc_fence_after();
+          qk(0, j + 1);
+        }
+        pv(1, j);
+        mma_commit2(&ss.kv_empty[(2 * j + 1) % kStages]);
+        if (j + 1 < n_kv) {
+          qk(1, j + 1);
+          mma_commit2(&ss.kv_empty[(2 * j + 2) % kStages]);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== softmax (one query row per thread; as the 1-CTA kernel) =====================
+    const int t = (warp - 4) >> 2;
+    const int r = tid - 128 - t * 128;
+    const int lane = tid & 31;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t s_col = tmem + lane_off + t * 128;
+    const uint32_t o_col = tmem + lane_off + 256 + t * 128;
+    const int qidx = first_q + t * p.tpt + r / p.group;
+    const int qpos = prefix + qidx;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      mbar_wait_suspend(&ss.s_full[t], j & 1);
+      tc_fence_after();
+      uint32_t sv[128];
+      tmem_ld32(s_col + 0, *reinterpret_cast<uint32_t(*)[32]>(sv + 0));
+      tmem_ld32(s_col + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+      tmem_ld32(s_col + 64, *reinterpret_cast<uint32_t(*)[32]>(sv + 64));
+      tmem_ld32(s_col + 96, *reinterpret_cast<uint32_t(*)[32]>(sv + 96));
+      tmem_wait_ld();
+      float* s = reinterpret_cast<float*>(sv);
+      const int kbase = j * 128;
+      if (kbase + 127 > qpos) {
+#pragma unroll
+        for (int k = 0; k < 128; ++k)
+          if (kbase + k > qpos) s[k] = -INFINITY;
+      }
+      float mk[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mk[i] = fmax3(s[i], s[8 + i], s[16 + i]);
+#pragma unroll
+      for (int k = 24; k + 16 <= 120; k += 16)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mk[i] = fmax3(mk[i], s[k + i], s[k + 8 + i]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mk[i] = fmaxf(mk[i], s[120 + i]);
+      const float mx = fmaxf(fmax3(mk[0], mk[1], mk[2]), fmax3(fmax3(mk[3], mk[4], mk[5]), mk[6], mk[7])) *
+                       p.scale_log2;
+      const float m_new = fmaxf(m_used, mx);
+      const bool need = m_new > m_used + 8.f;
+      float factor = 1.f;
+      if (need) {
+        factor = ex2(m_used - m_new);
+        m_used = m_new;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+        mbar_wait_suspend(&ss.o_done[t], (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint32_t v[16];
+          tmem_ld16(o_col + c * 16, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] = __float_as_uint(__uint_as_float(v[k]) * factor);
+          tmem_st16(o_col + c * 16, v);
+        }
+      }
+      l *= factor;
+      const float neg_m = -m_used;
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t w[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          float a0, a1;
+          ffma2(a0, a1, s[32 * c + 2 * k], s[32 * c + 2 * k + 1], p.scale_log2, neg_m);
+          float e0, e1;
+          if ((k & 3) == 3) {
+            ex2_poly2(a0, a1, e0, e1);
+          } else {
+            e0 = ex2(a0);
+            e1 = ex2(a1);
+          }
+          fadd2(acc[2 * (k & 3)], acc[2 * (k & 3) + 1], e0, e1);
+          w[k] = pack_bf16x2(e0, e1);
+        }
+        tmem_st16(s_col + c * 16, w);
+        if ((c + 1) % (4 / kPSplit) == 0) {  // release this part of P (one arrival per warp, on the leader)
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote_relaxed(mapa(&ss.p_part[t][c / (4 / kPSplit)], 0));
+        }
+      }
+      fadd2(acc[0], acc[1], acc[2], acc[3]);
+      fadd2(acc[4], acc[5], acc[6], acc[7]);
+      fadd2(acc[0], acc[1], acc[4], acc[5]);
+      l += acc[0] + acc[1];
+    }
+    mbar_wait_suspend(&ss.o_done[t], (n_kv - 1) & 1);
+    tc_fence_after();
+    const bool valid = qidx < q_len;
+    const float inv = (valid && l > 0.f) ? 1.f / l : 0.f;
+    __nv_bfloat16* orow =
+        p.out + (static_cast<int64_t>(q0 + qidx) * p.n_q_heads + kvh * p.group + (r % p.group)) * 128;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t v[32];
+      tmem_ld32(o_col + c * 32, v);
+      tmem_wait_ld();
+      if (valid) {
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(v[8 * k + 0]) * inv, __uint_as_float(v[8 * k + 1]) * inv);
+          w.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * inv, __uint_as_float(v[8 * k + 3]) * inv);
+          w.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * inv, __uint_as_float(v[8 * k + 5]) * inv);
+          w.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * inv, __uint_as_float(v[8 * k + 7]) * inv);
+          dst[k] = w;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc2(tmem);
+  }
+}
+
+}  // namespace pairk
+
 // fp32 continuation attention (CUDA cores): the same op on fp32 pages, for
 // the fp32 precision contract (outputs within 1e-5 of an fp32 reference) —
 // e.g. the toy 2-layer model of BASELINE configs[0] whose reference path is
@@ -552,19 +891,34 @@ extern "C" int sb_continuation_attention(const void* q, const void* k_pool, cons
     prm.oob_row = static_cast<int32_t>(kv_rows);
     prm.scale_log2 = softmax_scale * 1.4426950408889634f;
     prm.work = d_work;
-    auto kern = attn::k_continuation_attention;
     // the attribute is per device context: set once per device, thread-safe
     static std::once_flag attr_once[64];
     int dev = 0;
     SB_CUDA(cudaGetDevice(&dev));
     cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once[dev & 63], [&] {
-      attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::kSmemBytes);
+      attr_err = cudaFuncSetAttribute(attn::k_continuation_attention, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      attn::kSmemBytes);
     });
     SB_CUDA(attr_err);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (attn::pair_mode()) {  // work items are quads of query tiles, two CTAs each
+      const int64_t quads = (prm.pairs_per_seq + 1) / 2;
+      const int64_t items = d_work ? static_cast<int64_t>(n_work) : static_cast<int64_t>(n_seqs) * n_kv_heads * quads;
+      if (items <= 0) return int(SB_OK);
+      auto kern = attn::pairk::k_continuation_attention_pair<2, true>;
+      static std::once_flag pair_once[64];
+      std::call_once(pair_once[dev & 63], [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::pairk::kSmemBytes);
+      });
+      SB_CUDA(attr_err);
+      kern<<<static_cast<unsigned>(2 * items), attn::kThreads, attn::pairk::kSmemBytes, st>>>(tm_q, tm_k, tm_v, prm);
+      SB_CHECK_LAUNCH();
+      return int(SB_OK);
+    }
     const int64_t grid = d_work ? static_cast<int64_t>(n_work) : static_cast<int64_t>(n_seqs) * n_kv_heads * prm.pairs_per_seq;
     if (grid <= 0) return int(SB_OK);
-    kern<<<static_cast<unsigned>(grid), attn::kThreads, attn::kSmemBytes, static_cast<cudaStream_t>(stream)>>>(
+    attn::k_continuation_attention<<<static_cast<unsigned>(grid), attn::kThreads, attn::kSmemBytes, st>>>(
         tm_q, tm_k, tm_v, prm);
     SB_CHECK_LAUNCH();
     return int(SB_OK);
@@ -594,7 +948,8 @@ extern "C" int sb_attention_work_list(const int32_t* h_q_offsets, const int32_t*
                                       int32_t n_q_heads, int32_t n_kv_heads, int32_t* out, int32_t cap, int32_t* n_out) {
   return guard([&] {
     if (n_kv_heads <= 0 || n_q_heads % n_kv_heads) throw Error(SB_ERR_INVALID, "n_q_heads % n_kv_heads != 0");
-    const int tpt = 128 / (n_q_heads / n_kv_heads);
+    // pair mode: one item per quad of query tiles (CTA pair), else per pair of tiles
+    const int tpt = (128 / (n_q_heads / n_kv_heads)) * (attn::pair_mode() ? 2 : 1);
     // LPT over (sequence, kv head) groups, each group's tiles adjacent so the
     // CTAs running together share the group's K/V pages in L2; inside a
     // group the longest tiles (largest causal key range) go first.

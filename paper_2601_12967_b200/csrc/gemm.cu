@@ -388,7 +388,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       epilogue_tile(p, tbase, row, nt);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_remote(mapa(&ss.acc_empty[a], 0));
+      if (lane == 0) mbar_arrive_remote_relaxed(mapa(&ss.acc_empty[a], 0));
     }
   }
   tc_fence_before();

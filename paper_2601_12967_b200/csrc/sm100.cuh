@@ -257,6 +257,14 @@ __device__ __forceinline__ void mma_commit2(uint64_t* bar) {
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
+// Relaxed remote arrive: no generic-memory release (the .release form costs a
+// GPU-scope MEMBAR per arrive).  For handing TMEM data to the pair's MMA
+// issuer: the data is ordered by tcgen05.wait::st / wait::ld +
+// tcgen05.fence::before_thread_sync ahead of the arrive, and by the issuer's
+// wait + tcgen05.fence::after_thread_sync behind it.
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
 __device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(dst_smem))
                : "memory");

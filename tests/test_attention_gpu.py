@@ -215,3 +215,17 @@ def test_continuation_attention_f32_matches_fp32(case):
     ref = ref_attention(q.double(), kp.double(), vp.double(), qo.cpu(), kl.cpu(), tb, 1 / math.sqrt(128))
     err = ((out.double() - ref).abs().max() / ref.abs().max()).item()
     assert err <= REL_TOL_F32, err
+
+
+@pytest.mark.gpu
+def test_pair_attention_kernel():
+    """The default launch is the 1-CTA kernel; the same tests with
+    SB_ATTN_PAIR=1 run the CTA-pair kernel (cta_group::2, the A/B arm)."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SB_ATTN_PAIR="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.abspath(__file__), "-k",
+                        "not pair_attention"], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
