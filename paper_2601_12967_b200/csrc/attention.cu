@@ -124,6 +124,134 @@ __device__ __forceinline__ void fadd2(float& a0, float& a1, float b0, float b1) 
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(r));
 }
 
+// The softmax warpgroups of both kernels: warps 4-7 own query tile 0, warps
+// 8-11 tile 1, one TMEM lane (= one query row) per thread.  Online softmax with
+// a lazy rescale (O is rescaled in TMEM only when the running max grows by
+// more than 2^8), P written as packed bf16 over the first 64 columns of S and
+// released to the MMA issuer in kPSplit parts through `release(tile, part)`
+// (after tcgen05.wait::st + fence::before_thread_sync), then O / l -> bf16.
+template <int kPSplit, class SmemT, class Release>
+__device__ __forceinline__ void softmax_warpgroup(const Params& p, SmemT& ss, uint32_t tmem, int tid, int warp,
+                                                  int first_q, int prefix, int q_len, int q0, int kvh, int n_kv,
+                                                  Release&& release) {
+  const int t = (warp - 4) >> 2;  // tile of this warpgroup
+  const int r = tid - 128 - t * 128;
+  const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+  const uint32_t s_col = tmem + lane_off + t * 128;
+  const uint32_t o_col = tmem + lane_off + 256 + t * 128;
+  const int qidx = first_q + t * p.tpt + r / p.group;
+  const int qpos = prefix + qidx;  // absolute key position of this query
+  float m_used = -INFINITY, l = 0.f;
+  for (int j = 0; j < n_kv; ++j) {
+    mbar_wait_suspend(&ss.s_full[t], j & 1);
+    tc_fence_after();
+    // raw scores: four TMEM loads in flight, one wait
+    uint32_t sv[128];
+    tmem_ld32(s_col + 0, *reinterpret_cast<uint32_t(*)[32]>(sv + 0));
+    tmem_ld32(s_col + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+    tmem_ld32(s_col + 64, *reinterpret_cast<uint32_t(*)[32]>(sv + 64));
+    tmem_ld32(s_col + 96, *reinterpret_cast<uint32_t(*)[32]>(sv + 96));
+    tmem_wait_ld();
+    float* s = reinterpret_cast<float*>(sv);
+    const int kbase = j * 128;
+    if (kbase + 127 > qpos) {
+#pragma unroll
+      for (int k = 0; k < 128; ++k)
+        if (kbase + k > qpos) s[k] = -INFINITY;
+    }
+    // row max: 8 independent 3-input max chains, then a short tree
+    float mk[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mk[i] = fmax3(s[i], s[8 + i], s[16 + i]);
+#pragma unroll
+    for (int k = 24; k + 16 <= 120; k += 16)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mk[i] = fmax3(mk[i], s[k + i], s[k + 8 + i]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mk[i] = fmaxf(mk[i], s[120 + i]);
+    const float mx = fmaxf(fmax3(mk[0], mk[1], mk[2]), fmax3(fmax3(mk[3], mk[4], mk[5]), mk[6], mk[7])) *
+                     p.scale_log2;
+    const float m_new = fmaxf(m_used, mx);
+    const bool need = m_new > m_used + 8.f;
+    float factor = 1.f;
+    if (need) {
+      factor = ex2(m_used - m_new);  // 0 on the first tile (m_used = -inf)
+      m_used = m_new;
+    }
+    if (j > 0 && __any_sync(0xffffffffu, need)) {
+      // rescale this warp's rows of O in TMEM once PV_{j-1} has landed
+      mbar_wait_suspend(&ss.o_done[t], (j - 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t v[16];
+        tmem_ld16(o_col + c * 16, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = __float_as_uint(__uint_as_float(v[k]) * factor);
+        tmem_st16(o_col + c * 16, v);
+      }
+    }
+    l *= factor;
+    // p = 2^(s*scale - m): one FFMA2 per pair, MUFU ex2, 4 packed partial sums
+    const float neg_m = -m_used;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t w[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        float a0, a1;
+        ffma2(a0, a1, s[32 * c + 2 * k], s[32 * c + 2 * k + 1], p.scale_log2, neg_m);
+        float e0, e1;
+        if ((k & 3) == 3) {  // a quarter of the pairs on the FMA pipes
+          ex2_poly2(a0, a1, e0, e1);
+        } else {
+          e0 = ex2(a0);
+          e1 = ex2(a1);
+        }
+        fadd2(acc[2 * (k & 3)], acc[2 * (k & 3) + 1], e0, e1);
+        w[k] = pack_bf16x2(e0, e1);
+      }
+      tmem_st16(s_col + c * 16, w);
+      if ((c + 1) % (4 / kPSplit) == 0) {  // release this part of P to the MMA issuer
+        tmem_wait_st();
+        tc_fence_before();
+        release(t, c / (4 / kPSplit));
+      }
+    }
+    fadd2(acc[0], acc[1], acc[2], acc[3]);
+    fadd2(acc[4], acc[5], acc[6], acc[7]);
+    fadd2(acc[0], acc[1], acc[4], acc[5]);
+    l += acc[0] + acc[1];
+  }
+  // ---- epilogue: O / l -> bf16 -> global
+  mbar_wait_suspend(&ss.o_done[t], (n_kv - 1) & 1);
+  tc_fence_after();
+  const bool valid = qidx < q_len;
+  const float inv = (valid && l > 0.f) ? 1.f / l : 0.f;
+  __nv_bfloat16* orow =
+      p.out + (static_cast<int64_t>(q0 + qidx) * p.n_q_heads + kvh * p.group + (r % p.group)) * 128;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t v[32];
+    tmem_ld32(o_col + c * 32, v);
+    tmem_wait_ld();
+    if (valid) {
+      uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint4 w;
+        w.x = pack_bf16x2(__uint_as_float(v[8 * k + 0]) * inv, __uint_as_float(v[8 * k + 1]) * inv);
+        w.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * inv, __uint_as_float(v[8 * k + 3]) * inv);
+        w.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * inv, __uint_as_float(v[8 * k + 5]) * inv);
+        w.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * inv, __uint_as_float(v[8 * k + 7]) * inv);
+        dst[k] = w;
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     k_continuation_attention(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                              const __grid_constant__ CUtensorMap tm_v, const Params p) {
@@ -275,122 +403,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ===================== softmax (one query row per thread) =====================
-    const int t = (warp - 4) >> 2;  // tile of this warpgroup
-    const int r = tid - 128 - t * 128;
-    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const uint32_t s_col = tmem + lane_off + t * 128;
-    const uint32_t o_col = tmem + lane_off + 256 + t * 128;
-    const int qidx = first_q + t * p.tpt + r / p.group;
-    const int qpos = prefix + qidx;  // absolute key position of this query
-    float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_kv; ++j) {
-      mbar_wait_suspend(&ss.s_full[t], j & 1);
-      tc_fence_after();
-      // raw scores: four TMEM loads in flight, one wait
-      uint32_t sv[128];
-      tmem_ld32(s_col + 0, *reinterpret_cast<uint32_t(*)[32]>(sv + 0));
-      tmem_ld32(s_col + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
-      tmem_ld32(s_col + 64, *reinterpret_cast<uint32_t(*)[32]>(sv + 64));
-      tmem_ld32(s_col + 96, *reinterpret_cast<uint32_t(*)[32]>(sv + 96));
-      tmem_wait_ld();
-      float* s = reinterpret_cast<float*>(sv);
-      const int kbase = j * 128;
-      if (kbase + 127 > qpos) {
-#pragma unroll
-        for (int k = 0; k < 128; ++k)
-          if (kbase + k > qpos) s[k] = -INFINITY;
-      }
-      // row max: 8 independent 3-input max chains, then a short tree
-      float mk[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) mk[i] = fmax3(s[i], s[8 + i], s[16 + i]);
-#pragma unroll
-      for (int k = 24; k + 16 <= 120; k += 16)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) mk[i] = fmax3(mk[i], s[k + i], s[k + 8 + i]);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) mk[i] = fmaxf(mk[i], s[120 + i]);
-      const float mx = fmaxf(fmax3(mk[0], mk[1], mk[2]), fmax3(fmax3(mk[3], mk[4], mk[5]), mk[6], mk[7])) *
-                       p.scale_log2;
-      const float m_new = fmaxf(m_used, mx);
-      const bool need = m_new > m_used + 8.f;
-      float factor = 1.f;
-      if (need) {
-        factor = ex2(m_used - m_new);  // 0 on the first tile (m_used = -inf)
-        m_used = m_new;
-      }
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
-        // rescale this warp's rows of O in TMEM once PV_{j-1} has landed
-        mbar_wait_suspend(&ss.o_done[t], (j - 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint32_t v[16];
-          tmem_ld16(o_col + c * 16, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int k = 0; k < 16; ++k) v[k] = __float_as_uint(__uint_as_float(v[k]) * factor);
-          tmem_st16(o_col + c * 16, v);
-        }
-      }
-      l *= factor;
-      // p = 2^(s*scale - m): one FFMA2 per pair, MUFU ex2, 4 packed partial sums
-      const float neg_m = -m_used;
-      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t w[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          float a0, a1;
-          ffma2(a0, a1, s[32 * c + 2 * k], s[32 * c + 2 * k + 1], p.scale_log2, neg_m);
-          float e0, e1;
-          if ((k & 3) == 3) {  // a quarter of the pairs on the FMA pipes
-            ex2_poly2(a0, a1, e0, e1);
-          } else {
-            e0 = ex2(a0);
-            e1 = ex2(a1);
-          }
-          fadd2(acc[2 * (k & 3)], acc[2 * (k & 3) + 1], e0, e1);
-          w[k] = pack_bf16x2(e0, e1);
-        }
-        tmem_st16(s_col + c * 16, w);
-        if ((c + 1) % (4 / kPSplit) == 0) {  // release this part of P to the MMA warp
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(&ss.p_part[t][c / (4 / kPSplit)]);
-        }
-      }
-      fadd2(acc[0], acc[1], acc[2], acc[3]);
-      fadd2(acc[4], acc[5], acc[6], acc[7]);
-      fadd2(acc[0], acc[1], acc[4], acc[5]);
-      l += acc[0] + acc[1];
-    }
-    // ---- epilogue: O / l -> bf16 -> global
-    mbar_wait_suspend(&ss.o_done[t], (n_kv - 1) & 1);
-    tc_fence_after();
-    const bool valid = qidx < q_len;
-    const float inv = (valid && l > 0.f) ? 1.f / l : 0.f;
-    __nv_bfloat16* orow =
-        p.out + (static_cast<int64_t>(q0 + qidx) * p.n_q_heads + kvh * p.group + (r % p.group)) * 128;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t v[32];
-      tmem_ld32(o_col + c * 32, v);
-      tmem_wait_ld();
-      if (valid) {
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          uint4 w;
-          w.x = pack_bf16x2(__uint_as_float(v[8 * k + 0]) * inv, __uint_as_float(v[8 * k + 1]) * inv);
-          w.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * inv, __uint_as_float(v[8 * k + 3]) * inv);
-          w.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * inv, __uint_as_float(v[8 * k + 5]) * inv);
-          w.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * inv, __uint_as_float(v[8 * k + 7]) * inv);
-          dst[k] = w;
-        }
-      }
-    }
+    softmax_warpgroup<kPSplit>(p, ss, tmem, tid, warp, first_q, prefix, q_len, q0, kvh, n_kv,
+                               [&](int tile, int part) { mbar_arrive(&ss.p_part[tile][part]); });
   }
   tc_fence_before();
   __syncthreads();
@@ -611,119 +625,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ===================== softmax (one query row per thread; as the 1-CTA kernel) =====================
-    const int t = (warp - 4) >> 2;
-    const int r = tid - 128 - t * 128;
     const int lane = tid & 31;
-    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const uint32_t s_col = tmem + lane_off + t * 128;
-    const uint32_t o_col = tmem + lane_off + 256 + t * 128;
-    const int qidx = first_q + t * p.tpt + r / p.group;
-    const int qpos = prefix + qidx;
-    float m_used = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_kv; ++j) {
-      mbar_wait_suspend(&ss.s_full[t], j & 1);
-      tc_fence_after();
-      uint32_t sv[128];
-      tmem_ld32(s_col + 0, *reinterpret_cast<uint32_t(*)[32]>(sv + 0));
-      tmem_ld32(s_col + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
-      tmem_ld32(s_col + 64, *reinterpret_cast<uint32_t(*)[32]>(sv + 64));
-      tmem_ld32(s_col + 96, *reinterpret_cast<uint32_t(*)[32]>(sv + 96));
-      tmem_wait_ld();
-      float* s = reinterpret_cast<float*>(sv);
-      const int kbase = j * 128;
-      if (kbase + 127 > qpos) {
-#pragma unroll
-        for (int k = 0; k < 128; ++k)
-          if (kbase + k > qpos) s[k] = -INFINITY;
-      }
-      float mk[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) mk[i] = fmax3(s[i], s[8 + i], s[16 + i]);
-#pragma unroll
-      for (int k = 24; k + 16 <= 120; k += 16)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) mk[i] = fmax3(mk[i], s[k + i], s[k + 8 + i]);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) mk[i] = fmaxf(mk[i], s[120 + i]);
-      const float mx = fmaxf(fmax3(mk[0], mk[1], mk[2]), fmax3(fmax3(mk[3], mk[4], mk[5]), mk[6], mk[7])) *
-                       p.scale_log2;
-      const float m_new = fmaxf(m_used, mx);
-      const bool need = m_new > m_used + 8.f;
-      float factor = 1.f;
-      if (need) {
-        factor = ex2(m_used - m_new);
-        m_used = m_new;
-      }
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
-        mbar_wait_suspend(&ss.o_done[t], (j - 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint32_t v[16];
-          tmem_ld16(o_col + c * 16, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int k = 0; k < 16; ++k) v[k] = __float_as_uint(__uint_as_float(v[k]) * factor);
-          tmem_st16(o_col + c * 16, v);
-        }
-      }
-      l *= factor;
-      const float neg_m = -m_used;
-      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t w[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          float a0, a1;
-          ffma2(a0, a1, s[32 * c + 2 * k], s[32 * c + 2 * k + 1], p.scale_log2, neg_m);
-          float e0, e1;
-          if ((k & 3) == 3) {
-            ex2_poly2(a0, a1, e0, e1);
-          } else {
-            e0 = ex2(a0);
-            e1 = ex2(a1);
-          }
-          fadd2(acc[2 * (k & 3)], acc[2 * (k & 3) + 1], e0, e1);
-          w[k] = pack_bf16x2(e0, e1);
-        }
-        tmem_st16(s_col + c * 16, w);
-        if ((c + 1) % (4 / kPSplit) == 0) {  // release this part of P (one arrival per warp, on the leader)
-          tmem_wait_st();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_remote_relaxed(mapa(&ss.p_part[t][c / (4 / kPSplit)], 0));
-        }
-      }
-      fadd2(acc[0], acc[1], acc[2], acc[3]);
-      fadd2(acc[4], acc[5], acc[6], acc[7]);
-      fadd2(acc[0], acc[1], acc[4], acc[5]);
-      l += acc[0] + acc[1];
-    }
-    mbar_wait_suspend(&ss.o_done[t], (n_kv - 1) & 1);
-    tc_fence_after();
-    const bool valid = qidx < q_len;
-    const float inv = (valid && l > 0.f) ? 1.f / l : 0.f;
-    __nv_bfloat16* orow =
-        p.out + (static_cast<int64_t>(q0 + qidx) * p.n_q_heads + kvh * p.group + (r % p.group)) * 128;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t v[32];
-      tmem_ld32(o_col + c * 32, v);
-      tmem_wait_ld();
-      if (valid) {
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          uint4 w;
-          w.x = pack_bf16x2(__uint_as_float(v[8 * k + 0]) * inv, __uint_as_float(v[8 * k + 1]) * inv);
-          w.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * inv, __uint_as_float(v[8 * k + 3]) * inv);
-          w.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * inv, __uint_as_float(v[8 * k + 5]) * inv);
-          w.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * inv, __uint_as_float(v[8 * k + 7]) * inv);
-          dst[k] = w;
-        }
-      }
-    }
+    softmax_warpgroup<kPSplit>(p, ss, tmem, tid, warp, first_q, prefix, q_len, q0, kvh, n_kv, [&](int tile, int part) {
+      __syncwarp();  // one arrival per warp, on the leader
+      if (lane == 0) mbar_arrive_remote_relaxed(mapa(&ss.p_part[tile][part], 0));
+    });
   }
   tc_fence_before();
   cluster_sync();
