@@ -406,6 +406,8 @@ void gemm_bf16(const void* x, const void* w, void* y, int64_t rows, int64_t n, i
                cudaStream_t stream) {
   if (rows <= 0 || n <= 0) return;
   if (k <= 0 || (k % 8) || (n % 8)) throw Error(SB_ERR_UNSUPPORTED, "gemm: k and n must be positive multiples of 8");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(y)) & 15)
+    throw Error(SB_ERR_UNSUPPORTED, "gemm: x, w and y must be 16-byte aligned (TMA / vector stores)");
   if (rows >= (int64_t(1) << 31) || n >= (int64_t(1) << 30) || k >= (int64_t(1) << 31))
     throw Error(SB_ERR_UNSUPPORTED, "gemm: dimensions exceed 32-bit TMA coordinates");
   const int64_t w_rows = mode == kSwiGLU ? 2 * n : n;

@@ -124,6 +124,9 @@ def test_unsupported_shape_is_an_error():
         _gemm(x, w, y, 16, 16, 12, STORE)  # k not a multiple of 8
     with pytest.raises(ValueError):
         _gemm(x, w, y, 16, 16, 16, 9)  # unknown mode
+    y2 = torch.empty(16 * 16 + 1, device="cuda", dtype=torch.bfloat16)[1:]  # 2-byte offset
+    with pytest.raises(errors.Unsupported):
+        _gemm(x, w, y2, 16, 16, 16, STORE)
     del _lib
 
 
