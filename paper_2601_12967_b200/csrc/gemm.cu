@@ -3,7 +3,10 @@
 //   Y[rows, n] (op)= X[rows, k] · W[n, k]^T      (bf16 in, fp32 accumulate)
 // X and W are row-major (nn.Linear layout), i.e. both operands K-major.
 //
-// Persistent, warp-specialised, one 192-thread CTA per SM:
+// Two persistent kernels: k_gemm_pair (CTA pairs, 256 x 256 tiles; every
+// launch with more than 128 rows, see the pair section below) and k_gemm
+// (1 CTA, 128 x 256 tiles; few rows, e.g. the LM head over the last tokens).
+// Both are warp-specialised, one 192-thread CTA per SM:
 //   warp 4      TMA producer: 128x64 X tile + 256x64 W tile per stage
 //               (SWIZZLE_128B, 4-stage ring, mbarrier transaction counts)
 //   warp 5      one elected lane issues tcgen05.mma (M=128, N=256, K=16; four
