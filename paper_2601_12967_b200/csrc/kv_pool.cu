@@ -1190,7 +1190,8 @@ struct CoopBuf {
 };
 // SB_SELECT_PROF slots: 0/1 k_plan start/end, 2/3 k_score first/last CTA entry, 4 k_score last exit,
 // 5/6 k_select_coop first/last entry, 7 CTA 0 after the prologue, 8+2p / 9+2p last arrival at / CTA 0
-// leaving grid barrier p (p < 6), 20 CTA 0 sort start, 21 CTA 0 end
+// leaving grid barrier p (p < 6), 20 CTA 0 sort start, 21 CTA 0 end, 29 / 30 CTA 0 rank step: keys loaded /
+// ranks written, 31 the rank step's key count M
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -1798,6 +1799,8 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
       }
     }
     __syncthreads();
+    if (cta == 0) tp_set(G, 29);  // keys loaded
+    if (cta == 0 && t == 0 && G.tprof) G.tprof[31] = static_cast<unsigned long long>(M);
     const int64_t per = (M + n_cta - 1) / n_cta, r_lo = cta * per, r_hi = min(M, r_lo + per);
     const int lane = t & 31, nw = blockDim.x >> 5;
     for (int64_t i = r_lo + (t >> 5); i < r_hi; i += nw) {
@@ -1810,6 +1813,10 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
         S.taken[c] = 0;
         S.rank_of[k & P.idmask] = static_cast<int32_t>(c);
       }
+    }
+    if (cta == 0 && G.tprof) {  // CTA 0's ranks written (each warp's last one)
+      __syncthreads();
+      tp_set(G, 30);
     }
     if (cta == 0 && t == 0) {
       S.scal[S_K] = K;
@@ -2979,8 +2986,9 @@ struct sb_kv_cache {
               "prologue %.2f", mode, us(1), us(2), us(3), us(4), us(5), us(6), us(7));
       for (int p = 0; p < 6; ++p)
         if (h[8 + 2 * p]) fprintf(stderr, " sync%d %.2f->%.2f", p, us(8 + 2 * p), us(9 + 2 * p));
-      fprintf(stderr, " sort %.2f end %.2f | hist0 %.2f hist1 %.2f compact %.2f gather %.2f | cta0 %.2f %.2f %.2f\n",
-              us(20), us(21), us(22), us(23), us(24), us(25), us(26), us(27), us(28));
+      fprintf(stderr, " sort %.2f end %.2f | hist0 %.2f hist1 %.2f compact %.2f gather %.2f | cta0 %.2f %.2f %.2f"
+              " | rank: keys_loaded %.2f ranked %.2f M %llu\n",
+              us(20), us(21), us(22), us(23), us(24), us(25), us(26), us(27), us(28), us(29), us(30), h[31]);
       {
         unsigned long long hc[2 * 160 + 33] = {};
         SB_CUDA(cudaMemcpy(hc, G.tprof + 32, sizeof(hc), cudaMemcpyDeviceToHost));
