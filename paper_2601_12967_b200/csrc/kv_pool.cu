@@ -1187,6 +1187,7 @@ struct CoopBuf {
   int64_t slice;             // blocks per score slice (multiple of 4)
   int64_t sort_keys;         // keys k_select_coop's dynamic shared memory holds (its final sort)
   unsigned long long* tprof; // SB_SELECT_PROF=1: phase timestamps (%globaltimer) of the last evict, else null
+  int64_t rank_early_max = 6144;  // radix passes stop once <= this many keys remain (SB_RANK_EARLY)
 };
 // SB_SELECT_PROF slots: 0/1 k_plan start/end, 2/3 k_score first/last CTA entry, 4 k_score last exit,
 // 5/6 k_select_coop first/last entry, 7 CTA 0 after the prologue, 8+2p / 9+2p last arrival at / CTA 0
@@ -1728,7 +1729,7 @@ __device__ __forceinline__ void select_body(const Pool& P, const Scratch& S, con
       // (O(M^2) compares spread over the grid: ~2 us at 4K keys, ~7 us at
       // 8K, where another radix pass costs ~3-4 us): gather them all and let
       // the rank step pick the K smallest
-      if ((K - need) + static_cast<int64_t>(cnt_b) <= min(G.sort_keys, kRankEarlyMax)) break;
+      if ((K - need) + static_cast<int64_t>(cnt_b) <= min(G.sort_keys, G.rank_early_max)) break;
       if (!staged && !compacted && hi_bit > 0) {
         const int lane = t & 31;
         auto append = [&](bool take, uint64_t k, unsigned long long* ctr, uint64_t* dst) {
@@ -3346,6 +3347,10 @@ int sb_kv_create(int64_t block_size, int64_t capacity_blocks, int32_t policy, in
         const size_t avail = (static_cast<size_t>(smem_optin) - fa.sharedSizeBytes) & ~size_t(15);
         c->coop_smem = std::min(avail, std::max(full, sort_min));
         c->G.sort_keys = static_cast<int64_t>(c->coop_smem / sizeof(uint64_t));
+        {
+          const char* re = getenv("SB_RANK_EARLY");
+          c->G.rank_early_max = re ? std::max<int64_t>(64, std::atoll(re)) : kRankEarlyMax;
+        }
         SB_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScoreSmem)));
         {
           SB_CUDA(cudaFuncSetAttribute(k_select_coop, cudaFuncAttributeMaxDynamicSharedMemorySize,
